@@ -1,0 +1,224 @@
+/* cpdb -- C ABI of the B200-native CP-ALS-QR hot path (libcpdb.so).
+ *
+ * This is the drop-in boundary: the reference has no FFI of its own (it is
+ * the header-only C++ library `cpd`, /root/reference/proj/include/cpd), so the
+ * entry points below are exactly the calls its C++ API needs when it is
+ * re-pointed at the GPU.  The C++ headers in include/cpd/*.hpp keep the
+ * reference names and signatures and call only this ABI; INTEGRATION.md shows
+ * the CMake/ctypes bindings.  Each entry point cites the reference interface
+ * it replaces (path:line under /root/reference/proj/include/cpd).
+ *
+ * Conventions
+ *  - plain pointers and sizes only; every tensor is FP64, row-major with the
+ *    LAST index fastest (tensor.hpp:42-47), matrices row-major;
+ *  - every call returns a status code (CPDB_OK == 0); cpdb_last_error() holds
+ *    the message of the last failure on the calling thread.  The C++ headers
+ *    rethrow the reference's exception type for each code (cli.hpp:230-250
+ *    maps the same classes to exit codes);
+ *  - a context owns one device, one stream and every device buffer; calls on
+ *    one context are synchronous at return and not thread-safe (the reference
+ *    is single-threaded);
+ *  - there is no CPU fallback: without a usable B200 every compute call fails
+ *    with CPDB_CUDA_ERROR.
+ */
+#ifndef CPDB_H
+#define CPDB_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes ------------------------------------------------------- */
+#define CPDB_OK 0
+#define CPDB_INVALID_ARGUMENT 1     /* std::invalid_argument                       */
+#define CPDB_STALE_INTERMEDIATE 2   /* stale_intermediate_error dim_tree.hpp:21-23  */
+#define CPDB_SINGULAR_TRIANGULAR 3  /* singular_triangular_error linalg.hpp:19-26   */
+#define CPDB_LOGIC_ERROR 4          /* std::logic_error (missing cache source ...)  */
+#define CPDB_CUDA_ERROR 5           /* device / driver failure (no fallback)        */
+#define CPDB_NCCL_ERROR 6
+#define CPDB_OUT_OF_MEMORY 7
+
+#define CPDB_MAX_ORDER 8
+#define CPDB_ROOT_KEY 0xFFFFFFFFu   /* "the input tensor X" as a step source       */
+
+typedef struct cpdb_ctx cpdb_ctx;
+
+/* reference: solvers.hpp:56-66 TraceRow */
+typedef struct {
+    uint64_t iteration;                    /* 1-based sweep                      */
+    uint32_t order;                        /* entries used in update_order       */
+    uint32_t update_order[CPDB_MAX_ORDER]; /* 0-based modes                      */
+    uint32_t pad0;
+    double fitness;
+    double raw_radicand;
+    double wall_seconds;                   /* device clock since the solve began */
+    uint64_t root_ttm_count;               /* cumulative (dim_tree.hpp:143-158)  */
+    uint64_t flops;                        /* cumulative TTM flops               */
+    double beta_used;
+    int32_t regularized;
+    int32_t pad1;
+} cpdb_trace_row;
+
+/* reference: solvers.hpp:25-50 SolverConfig.  extrapolate=1 selects
+ * als_qr_bre (forces branch reuse, solvers.hpp:329-336); 0 selects cp_als_qr
+ * with `strategy` (solvers.hpp:317-322). */
+typedef struct {
+    uint64_t rank;
+    uint64_t max_iterations;
+    double fitness_threshold;
+    int32_t strategy;      /* 0 naive, 1 dim-tree, 2 branch-reuse (dim_tree.hpp:25) */
+    int32_t extrapolate;
+    double alpha;
+    int32_t has_beta_override;
+    int32_t pad0;
+    double beta_override;
+    double activation_gap;
+    uint64_t seed;         /* initial factors: Rng(seed) N(0,1), solvers.hpp:116-122 */
+} cpdb_config;
+
+/* Sweep-boundary solver state (resume / teacher forcing).  Everything
+ * run_qr carries between sweeps except the branch-reuse cache, which is
+ * rebuilt from X and the factors (freshness invariant dim_tree.hpp:109-111).
+ * Buffers are caller-owned host memory; on return they hold the end state. */
+typedef struct {
+    uint64_t sweeps_done;
+    double* lambda;        /* R                                                  */
+    double* factors;       /* concatenated I_k x R, mode order                   */
+    double* q0_history;    /* concatenated R^(N-1) x R per mode, reference row order */
+    uint32_t history_mask; /* bit n: history of mode n valid                     */
+    int32_t has_active_beta;
+    double active_beta;
+    int32_t has_prev_fitness;
+    int32_t pad0;
+    double prev_fitness;
+} cpdb_state;
+
+/* q0_observer (solvers.hpp:37-39): Q0 before extrapolation, reference row order */
+typedef void (*cpdb_q0_observer)(void* user, uint64_t sweep, uint32_t mode, const double* q0,
+                                 uint64_t rows, uint64_t cols);
+
+/* Device-measured timing of the last cpdb_solve (CUDA events on the solve
+ * stream).  Root TTM = a step whose source is X (dim_tree.hpp:526). */
+typedef struct {
+    uint64_t sweeps;
+    double solve_ms;          /* first sweep start -> last sweep end               */
+    double sweep1_ms;         /* sweep 1 (dim-tree sweep, two root TTMs)           */
+    uint64_t root_ttms;       /* root TTM launches timed                           */
+    double root_ttm_ms;       /* summed root TTM kernel time                       */
+    double root_ttm_flops;    /* algorithmic 2*|Y|*I_c summed over timed launches  */
+    double root_ttm_bytes;    /* algorithmic 8*(|X| + |Y| + I_c*R) summed          */
+    double branch_ttm_ms;     /* non-root TTM steps                                */
+    double mode_update_ms;    /* Z-QR, V-GEMM, solve, normalise, factor QR, fit    */
+    double comm_ms;           /* NCCL reductions (sharded contexts)                */
+    uint64_t kernel_launches; /* device kernels launched by the solve              */
+} cpdb_profile;
+
+/* ---- version / device ----------------------------------------------------- */
+const char* cpdb_version(void);
+const char* cpdb_last_error(void);
+/* 1 when a device of compute capability 10.x is usable */
+int cpdb_device_ok(int device);
+
+/* ---- context ---------------------------------------------------------------- */
+int cpdb_create(int device, cpdb_ctx** out);
+/* One rank of a mode-1 (index 0) sharded run: X's leading mode is split in
+ * contiguous slabs over `world` GPUs and TTMs that contract it are summed with
+ * NCCL all-reduce.  nccl_id: 128 bytes from
+ * cpdb_nccl_unique_id on rank 0, broadcast by the caller. */
+int cpdb_create_sharded(int device, int rank, int world, const void* nccl_id, cpdb_ctx** out);
+int cpdb_nccl_unique_id(void* out128);
+void cpdb_destroy(cpdb_ctx* ctx);
+/* Row range of the leading mode owned by `rank` (host-only, no device). */
+int cpdb_shard_rows(uint64_t extent0, int rank, int world, uint64_t* begin, uint64_t* count);
+
+/* ---- the tensor X (device-resident) ------------------------------------------ */
+/* Upload from host memory.  Sharded contexts take the rank's slab of the
+ * leading mode (rows [begin, begin+count) from cpdb_shard_rows) and the
+ * GLOBAL dims. */
+int cpdb_tensor_set(cpdb_ctx* ctx, const double* host, const uint64_t* dims, uint32_t order);
+/* Borrow an existing device buffer (no copy; caller keeps it alive). */
+int cpdb_tensor_set_device(cpdb_ctx* ctx, const double* device_ptr, const uint64_t* dims,
+                           uint32_t order);
+/* Fill X on the device with the BASELINE construction (DESIGN.md "Synthetic
+ * inputs"): kind 0 i.i.d. N(0,1) factors, kind 1 congruent/log-scaled
+ * columns; + rho-relative Gaussian noise.  Counter-based RNG: the bytes depend
+ * on (seed, dims, rank) only, not on the shard layout. */
+int cpdb_tensor_synth(cpdb_ctx* ctx, int32_t kind, const uint64_t* dims, uint32_t order,
+                      uint64_t rank, double rho, uint64_t seed);
+int cpdb_tensor_get(cpdb_ctx* ctx, double* host);
+/* ||X||^2 (tensor.hpp:394-399 inner(x, x)), deterministic reduction */
+int cpdb_tensor_norm_sq(cpdb_ctx* ctx, double* out);
+
+/* ---- the solver (solvers.hpp:215-336) ------------------------------------------ */
+/* Runs cp_als_qr / als_qr_bre on the context's X entirely in HBM.  state may
+ * be NULL (fresh run).  trace holds max_iterations rows.  factors_per_sweep
+ * (max_iterations x sum I_k R) and lambda_per_sweep (max_iterations x R) are
+ * optional per-sweep dumps for parity checks. */
+int cpdb_solve(cpdb_ctx* ctx, const cpdb_config* cfg, cpdb_state* state, cpdb_trace_row* trace,
+               uint64_t* trace_len, double* out_lambda, double* out_factors,
+               double* factors_per_sweep, double* lambda_per_sweep, cpdb_q0_observer observer,
+               void* observer_user);
+int cpdb_profile_get(cpdb_ctx* ctx, cpdb_profile* out);
+/* Enable/disable per-kernel event timing inside cpdb_solve (default on; off
+ * removes the events from the stream).  CUDA-graph capture of the sweeps is
+ * used when `graphs` is 1 (default). */
+int cpdb_set_options(cpdb_ctx* ctx, int32_t timing, int32_t graphs);
+
+/* ---- dense primitives on host buffers (device compute) ------------------------ */
+int cpdb_ttm(cpdb_ctx* ctx, const double* t, const uint64_t* dims, uint32_t order,
+             const double* b, uint64_t b_rows, uint32_t mode, double* out); /* tensor.hpp:288 */
+int cpdb_unfold(cpdb_ctx* ctx, const double* t, const uint64_t* dims, uint32_t order,
+                uint32_t mode, double* out);                                   /* tensor.hpp:217 */
+int cpdb_khatri_rao(cpdb_ctx* ctx, const double* const* mats, const uint64_t* rows,
+                    uint32_t count, uint64_t cols, double* out);               /* tensor.hpp:343 */
+int cpdb_thin_qr(cpdb_ctx* ctx, const double* a, uint64_t m, uint64_t n, double* q,
+                 double* r);                                                   /* linalg.hpp:39 */
+int cpdb_solve_rows_lower(cpdb_ctx* ctx, const double* l, uint64_t n, const double* rhs,
+                          uint64_t rows, double* out, int64_t* bad_column);    /* linalg.hpp:192 */
+int cpdb_normalize_columns(cpdb_ctx* ctx, const double* a, uint64_t m, uint64_t n, double* out,
+                           double* weights);                                   /* linalg.hpp:225 */
+int cpdb_extrapolate_q0(cpdb_ctx* ctx, const double* now, const double* prev, uint64_t rows,
+                        uint64_t cols, double beta, double alpha, double* out); /* solvers.hpp:75 */
+int cpdb_fitness_fast_qr(cpdb_ctx* ctx, double norm_x_sq, const double* v, const double* a_hat,
+                         uint64_t rows, const double* r0, const double* r_n, const double* lambda,
+                         uint64_t r, double* fitness, double* raw);            /* kruskal.hpp:109 */
+int cpdb_inner(cpdb_ctx* ctx, const double* a, const double* b, uint64_t n, double* out);
+/* select_beta (solvers.hpp:92-101) is host logic: returns 1 and sets *beta
+ * when extrapolation activates, 0 when it stays off. */
+int cpdb_select_beta(double fitness_prev, double fitness_now, double gap, double* beta);
+
+/* ---- scheduler (host metadata, dim_tree.hpp:191-634) ------------------------- */
+/* Steps flattened as 6 x int64: {iteration, block, mode, source, contract, produces}. */
+int cpdb_schedule_build(uint32_t order, int32_t strategy, uint64_t iterations, int64_t* steps,
+                        uint64_t cap_steps, uint64_t* n_steps, uint64_t* cycle /*[2]*/);
+int cpdb_schedule_validate(uint32_t order, const int64_t* steps, uint64_t n_steps,
+                           uint64_t iterations);
+int cpdb_retained_keys(uint32_t order, const int64_t* steps, uint64_t n_steps,
+                       uint64_t iterations, uint64_t cycle_start, uint64_t cycle_length,
+                       uint64_t iteration, uint64_t block, uint32_t* keys, uint64_t cap,
+                       uint64_t* n_keys);
+int cpdb_measured_cost(uint32_t order, int32_t strategy, const uint64_t* dims, uint64_t rank,
+                       uint64_t iterations, uint64_t* total_flops, uint64_t* root_ttms);
+int cpdb_closed_form_cost(uint32_t order, int32_t strategy, const uint64_t* dims, uint64_t rank,
+                          uint64_t* total);
+int cpdb_leading_flop_coefficient(uint32_t order, int32_t strategy, uint64_t* coeff);
+
+/* ---- device-resident execute() (dim_tree.hpp:473-544) ------------------------- */
+/* One scheduled TTM on the device: reads X (source == CPDB_ROOT_KEY) or the
+ * cache slot `source`, contracts `contract` with Q (I_c x R host matrix, the
+ * reference passes transpose(Q), dim_tree.hpp:519) and writes cache slot
+ * `produces`.  Freshness stamps and eviction policy stay in the caller
+ * (include/cpd/dim_tree.hpp), exactly as the reference keeps them on the host. */
+int cpdb_exec_step(cpdb_ctx* ctx, uint32_t source, uint32_t contract, uint32_t produces,
+                   const double* q, uint64_t rank);
+int cpdb_cache_dims(cpdb_ctx* ctx, uint32_t key, uint64_t* dims /*[order]*/, int32_t* present);
+int cpdb_cache_get(cpdb_ctx* ctx, uint32_t key, double* host);
+int cpdb_cache_drop(cpdb_ctx* ctx, uint32_t key);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

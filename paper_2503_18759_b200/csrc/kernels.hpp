@@ -1,0 +1,119 @@
+// Launch interface of the libcpdb device kernels (host-callable).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cpdb {
+
+// ---------------------------------------------------------------- K1/K2 TTM
+struct TtmArgs {
+    const double* x;   // source [outer][K][inner]
+    double* y;         // result [outer][R][inner]
+    const double* q;   // Q (K x R row-major) -- fallback path
+    const double* qp;  // Q packed by pack_q -- tensor-core paths
+    uint64_t outer, K, inner;
+    uint32_t R, Rp;
+};
+enum class TtmPath { groups, rows, simple };
+TtmPath ttm_path(const TtmArgs& a);
+cudaError_t launch_ttm(const TtmArgs& a, cudaStream_t s, int sms);
+uint32_t ttm_kpad(uint64_t K);
+uint32_t ttm_rpad(uint32_t R);
+cudaError_t pack_q(const double* q, double* qp, uint32_t K, uint32_t R, cudaStream_t s);
+
+// ---------------------------------------------------------------- K6 norms
+constexpr int kNormBlocks = 1184;  // fixed (8 x 148): deterministic partition
+cudaError_t norm_sq(const double* x, uint64_t n, double* partials, double* out, cudaStream_t s);
+cudaError_t dot_dev(const double* a, const double* b, uint64_t n, double* partials, double* out,
+                    cudaStream_t s);
+
+// ---------------------------------------------------------------- K3 Z-QR
+// Q0 / R0 of Z = KhatriRao(R_k, k != n) with Z's rows in the NATURAL order of
+// the final Y (row-major over the other modes, ascending; the last fastest).
+struct ZqrArgs {
+    const double* rmats[8];  // R_k (R x R, upper), k != n, ascending mode order
+    uint32_t nm;             // N - 1
+    uint32_t R;
+    uint64_t zrows;          // R^(N-1)
+    double* q1;              // zrows x R scratch
+    double* q0;              // zrows x R out
+    double* r0;              // R x R out
+    double* work;            // zqr_work_doubles(R, grid)
+    int* status;             // device flag: non-zero = Cholesky breakdown
+};
+size_t zqr_work_doubles(uint32_t R);
+cudaError_t launch_zqr(const ZqrArgs& a, cudaStream_t s, int sms);
+
+// ---------------------------------------------------------------- K4 V-GEMM
+// V[i][r] = sum_k Y(i,k) P[k][r] with Y(i, o*J + j) = y[(o*I + i)*J + j] and
+// P = Q0 (+ beta*(Q0 - alpha*H) when extrap), optionally also Vfit with P = Q0.
+struct VgemmArgs {
+    const double* y;
+    const double* q0;
+    const double* hist;  // may be null when !extrap
+    double beta, alpha;
+    int extrap;
+    int dual;            // also produce the unextrapolated V (fitness)
+    uint64_t I, J, O;    // rows, inner, outer  (K = O*J)
+    uint32_t R;
+    double* vpart;       // nsplit x I x R
+    double* vfitpart;    // nsplit x I x R (dual)
+    uint32_t nsplit;     // out: split count used
+};
+cudaError_t launch_vgemm(VgemmArgs& a, cudaStream_t s, int sms);
+uint32_t vgemm_max_split();
+
+// ---------------------------------------------------------------- finisher
+// Per-mode tail: reduce V partials, A_hat = V R0^-T, normalise (lambda),
+// CholQR2 of the factor -> Q_n, R_n, packed Q_n, and (last mode) the
+// fast-QR fitness.  mode_init: factor given in `a_out`, QR only.
+struct FinishArgs {
+    int init;              // 1: only QR (+pack) of a_out
+    const double* vpart;   // nsplit x I x R
+    const double* vfitpart;
+    uint32_t nsplit;
+    int dual;
+    const double* r0;      // R x R
+    uint64_t I;
+    uint32_t R;
+    double* v_out;         // I x R  (V used for the fitness)
+    double* a_out;         // I x R  normalised factor A_n
+    double* q_out;         // I x R
+    double* qp_out;        // packed Q_n for the TTM kernels
+    double* r_out;         // R x R
+    double* lambda;        // R
+    double* scratch;       // I x (R+1) when the working matrix does not fit in smem
+    int fitness;           // compute fitness
+    double norm_x_sq;
+    double* fit_out;       // [fitness, raw]
+    int* status;           // 1 singular R0 (+col<<8), 2 Cholesky breakdown
+};
+cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s);
+// out[e] = sum_{p < nsplit} part[p*n + e]  (fixed order)
+cudaError_t reduce_splits(const double* part, uint32_t nsplit, uint64_t n, double* out,
+                          cudaStream_t s);
+
+// ---------------------------------------------------------------- misc
+// normalize_columns (linalg.hpp:225-242) with the reference's exact
+// operation order (sequential column sums, no FMA contraction).
+cudaError_t normalize_exact(double* a, uint64_t m, uint32_t n, double* weights, cudaStream_t s);
+// Householder thin QR, reference algorithm (linalg.hpp:39-99), one CTA.
+cudaError_t householder_qr(const double* a, uint64_t m, uint32_t n, double* work, double* q,
+                           double* r, cudaStream_t s);
+// Row-major gather: out[j] = in[perm[j]] rows of width w.
+cudaError_t permute_rows(const double* in, double* out, const uint64_t* perm, uint64_t rows,
+                         uint32_t w, cudaStream_t s);
+// Synthetic BASELINE tensors on the device (counter-based RNG, synth.cu).
+// pass1 writes the noiseless slab and scal[0..1] = (sum X^2, sum E^2) of the
+// slab; sharded callers all-reduce scal before pass2 adds rho-scaled noise.
+cudaError_t synth_pass1(double* x, const uint64_t* dims_host, const uint64_t* dims_dev,
+                        uint32_t order, uint64_t rank, int32_t kind, uint64_t seed,
+                        uint64_t row_begin, uint64_t row_count, double* factors,
+                        double* partials, double* scal, cudaStream_t s);
+cudaError_t synth_pass2(double* x, const uint64_t* dims_host, uint32_t order, uint64_t rank,
+                        uint64_t seed, uint64_t row_begin, uint64_t row_count, const double* scal,
+                        double rho, cudaStream_t s);
+size_t synth_partials_doubles();
+
+}  // namespace cpdb

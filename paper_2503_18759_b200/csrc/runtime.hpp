@@ -1,0 +1,126 @@
+// Device runtime of libcpdb: the context behind the C ABI (include/cpdb.h).
+//
+// A context owns one B200, one stream and every device buffer of a solve:
+// the tensor X (whole, or this rank's slab of the leading mode), the
+// branch-reuse intermediate cache (one persistent buffer per free-mode set,
+// dim_tree.hpp:112-139 semantics: valid flag + per-mode version stamps), the
+// factor state (A_n, Q_n, packed Q_n, R_n, lambda; factor_state.hpp:18-48),
+// the per-mode Q0 history and the scratch of the mode-update kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <utility>
+#include <string>
+#include <vector>
+
+#include "cpdb.h"
+#include "kernels.hpp"
+#include "schedule.hpp"
+
+namespace cpdb {
+
+struct Fail {
+    int code;
+    std::string what;
+};
+
+[[noreturn]] void fail(int code, const std::string& what);
+void check_cuda(cudaError_t e, const char* where);
+#define CPDB_CK(expr) ::cpdb::check_cuda((expr), #expr)
+
+// Growable device allocation (never shrinks; freed with the context).
+struct DevBuf {
+    double* p = nullptr;
+    size_t n = 0;  // doubles
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+        o.p = nullptr;
+        o.n = 0;
+    }
+    ~DevBuf();
+    double* ensure(size_t doubles);
+    void swap(DevBuf& o) noexcept {
+        std::swap(p, o.p);
+        std::swap(n, o.n);
+    }
+};
+
+struct Slot {
+    DevBuf buf;
+    bool valid = false;
+    std::vector<uint64_t> dims;    // local extents
+    std::vector<uint64_t> stamps;  // 0 = mode not absorbed
+    bool sharded = false;          // leading mode free and split across ranks
+};
+
+struct Timer {
+    cudaEvent_t a = nullptr, b = nullptr;
+    int kind = 0;  // 0 root ttm, 1 branch ttm, 2 comm
+    double flops = 0, bytes = 0;
+};
+
+}  // namespace cpdb
+
+struct cpdb_ctx {
+    int device = 0;
+    int sms = 148;
+    cudaStream_t stream = nullptr;
+
+    // sharding: leading mode split in contiguous slabs
+    int rank = 0, world = 1;
+    void* comm = nullptr;  // ncclComm_t
+    uint64_t row_begin = 0, rows = 0;
+
+    // X
+    const double* x = nullptr;
+    cpdb::DevBuf xown;
+    std::vector<uint64_t> dims;   // global extents
+    std::vector<uint64_t> ldims;  // local extents (ldims[0] = rows)
+    bool norm_valid = false;
+    double norm_x_sq = 0.0;
+
+    // cache slots for the device execute() API (dim_tree.hpp:473-544)
+    std::map<uint32_t, cpdb::Slot> slots;
+
+    // scratch
+    cpdb::DevBuf scratch_a, scratch_b, scratch_c, scratch_d, partials;
+    int* dstatus = nullptr;
+    double* pinned = nullptr;  // 64 doubles of pinned host memory
+
+    cpdb_profile prof{};
+    bool timing = true;
+    bool graphs = true;
+    uint64_t launches = 0;
+
+    ~cpdb_ctx();
+};
+
+namespace cpdb {
+
+// X-side helpers
+uint64_t numel(const std::vector<uint64_t>& d);
+void require_tensor(cpdb_ctx* c);
+double ctx_norm_sq(cpdb_ctx* c);
+void allreduce_sum(cpdb_ctx* c, double* dev, size_t n);
+void allgather(cpdb_ctx* c, double* dev_full, size_t per_rank);
+
+// The device-resident run_qr (solvers.hpp:215-336).
+void solve(cpdb_ctx* c, const cpdb_config& cfg, cpdb_state* state, cpdb_trace_row* trace,
+           uint64_t* trace_len, double* out_lambda, double* out_factors, double* fps,
+           double* lps, cpdb_q0_observer observer, void* user);
+
+// Natural (Y row-major) <-> reference (Khatri-Rao, descending fold) row order
+// of Z / Q0 for mode n: digit reversal over the N-1 other modes.
+std::vector<uint64_t> natural_to_reference(uint32_t order, uint64_t R);
+
+// One TTM of the execute() chain on device buffers: contracts `c` of a
+// tensor with local extents `sd` using factor Q (I_c x R) / packed Qp.
+void run_ttm(cpdb_ctx* ctx, const double* src, const std::vector<uint64_t>& sd, uint32_t c,
+             const double* q, const double* qp, uint32_t R, double* dst);
+
+}  // namespace cpdb

@@ -1,0 +1,78 @@
+// Dimension-tree contraction scheduler (host metadata, native C++).
+//
+// B200-side restatement of the reference scheduler
+// (/root/reference/proj/include/cpd/dim_tree.hpp):
+//   plans            dim_tree.hpp:191-331 (naive / dim-tree / branch-reuse 3 & 4)
+//   build            dim_tree.hpp:386-426
+//   validate         dim_tree.hpp:335-379 (structure + version simulation)
+//   retained_keys    dim_tree.hpp:433-465 (cache eviction look-ahead)
+//   measured_cost    dim_tree.hpp:549-570
+//   closed_form_cost dim_tree.hpp:579-621
+// The plans are the same fixed data; the code is organised around the device
+// runtime's needs: every step also carries whether it is a root TTM and the
+// distinct sweep "patterns" a CUDA graph can be captured for.
+#pragma once
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace cpdb {
+
+using ModeSet = uint32_t;
+
+enum class Strategy : int32_t { naive = 0, dim_tree = 1, branch_reuse = 2 };
+
+struct Step {
+    ModeSet source;
+    uint32_t contract;
+    ModeSet produces;
+};
+
+struct Update {
+    uint32_t mode;
+    std::vector<Step> steps;
+};
+
+struct Sweep {
+    std::vector<Update> updates;
+};
+
+struct Plan {
+    uint32_t order = 0;
+    Strategy strategy = Strategy::naive;
+    std::vector<Sweep> sweeps;
+    uint64_t cycle_start = 0;
+    uint64_t cycle_length = 1;
+
+    ModeSet root() const { return (1u << order) - 1u; }
+    std::vector<uint32_t> update_order(uint64_t i) const;
+    // Index of the first sweep with the same step structure as sweep i
+    // (sweeps of one pattern can share a captured CUDA graph).
+    uint64_t pattern_of(uint64_t i) const;
+};
+
+// Error classes surfaced through the C ABI (status codes in include/cpdb.h).
+struct SchedError {
+    int code;  // CPDB_INVALID_ARGUMENT / CPDB_LOGIC_ERROR / CPDB_STALE_INTERMEDIATE
+    std::string what;
+};
+
+// Throws SchedError.
+Plan build_plan(uint32_t order, Strategy strategy, uint64_t sweeps);
+void validate_plan(const Plan& p);
+std::vector<ModeSet> retained_keys(const Plan& p, uint64_t sweep, uint32_t block);
+
+struct Cost {
+    uint64_t flops = 0;
+    uint64_t roots = 0;
+};
+Cost measured_cost(const Plan& p, const std::vector<uint64_t>& dims, uint64_t rank,
+                   uint64_t sweeps);
+uint64_t closed_form_cost(uint32_t order, Strategy s, const std::vector<uint64_t>& dims,
+                          uint64_t rank);
+uint64_t leading_flop_coefficient(uint32_t order, Strategy s);
+
+inline uint32_t popcount(ModeSet s) { return static_cast<uint32_t>(__builtin_popcount(s)); }
+
+}  // namespace cpdb

@@ -1,0 +1,183 @@
+"""GPU: the device-resident CP-ALS-QR solver against the CPU oracle.
+
+Tolerances (BASELINE.json north star): relative fitness and factor error
+<= 1e-10 per sweep, identical trace length, update order, beta-activation
+sweep and integer flops / root-TTM counts.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+META = json.load(open(os.path.join(ROOT, "tests", "golden", "golden_meta.json")))
+FIT_TOL = 1e-10
+FACTOR_TOL = 1e-10
+
+
+def cfg_of(rank, iters, seed=0, strategy="branch-reuse", **kw):
+    import paper_2503_18759_b200 as cpd
+    return cpd.SolverConfig(rank=rank, max_iterations=iters, seed=seed, strategy=strategy, **kw)
+
+
+def compare(gpu, ora, *, fit_tol=FIT_TOL, factor_tol=FACTOR_TOL, check_factors=True):
+    assert len(gpu.trace) == len(ora.trace)
+    for g, o in zip(gpu.trace, ora.trace):
+        assert g.iteration == o["iteration"]
+        assert g.update_order == o["update_order"]
+        assert g.flops == o["flops"] and g.root_ttm_count == o["root_ttm_count"]
+        assert g.beta_used == o["beta_used"], (g.iteration, g.beta_used, o["beta_used"])
+        assert abs(g.fitness - o["fitness"]) <= fit_tol * max(abs(o["fitness"]), 1e-300), \
+            (g.iteration, g.fitness, o["fitness"])
+    if check_factors:
+        for k, (fg, fo) in enumerate(zip(gpu.model.factors, ora.factors)):
+            err = np.linalg.norm(fg - fo) / np.linalg.norm(fo)
+            assert err <= factor_tol, (k, err)
+        assert np.linalg.norm(gpu.model.lam - ora.lam) / np.linalg.norm(ora.lam) <= factor_tol
+
+
+@pytest.mark.parametrize("dims,rank", [((9, 8, 7), 3), ((7, 6, 5, 4), 3), ((10, 10, 10), 4),
+                                       ((16, 24, 20), 5), ((12, 10, 8, 16), 4)])
+@pytest.mark.parametrize("variant", ["naive", "dim-tree", "branch-reuse", "bre"])
+def test_small_trajectories(ctx, port, dims, rank, variant):
+    import paper_2503_18759_b200 as cpd
+    x = port.rng_normals(31, int(np.prod(dims))).reshape(dims)
+    if variant == "bre":
+        g = cpd.als_qr_bre(x, cfg_of(rank, 12, seed=3), ctx=ctx)
+        o = port.solve(x, rank, 12, extrapolate=True, seed=3)
+    else:
+        g = cpd.cp_als_qr(x, cfg_of(rank, 12, seed=3, strategy=variant), ctx=ctx)
+        o = port.solve(x, rank, 12, extrapolate=False, strategy=variant, seed=3)
+    # random (non-low-rank) tensors converge slowly: compare at 1e-9 of fitness
+    compare(g, o, fit_tol=1e-9, factor_tol=1e-8)
+
+
+def test_c1_full_config(ctx, port, golden):
+    """BASELINE config 1: 100^3 R10 + 1e-2 noise, 50 sweeps ALS-QR-BRE."""
+    import paper_2503_18759_b200 as cpd
+    x = port.synth_baseline(0, (100, 100, 100), 10, 1e-2, META["truth_seeds"]["c1"])
+    g = cpd.als_qr_bre(x, cfg_of(10, 50, seed=META["init_seed"]), ctx=ctx, dump_per_sweep=True)
+    o = port.solve(x, 10, 50, extrapolate=True, seed=META["init_seed"], dump_per_sweep=True)
+    compare(g, o)
+    assert np.array_equal([t.fitness for t in g.trace][:0], [])
+    first = next(t.iteration for t in g.trace if t.beta_used != 0.0)
+    assert first == 8
+    for s in range(50):
+        for k in range(3):
+            fo = o.factors_per_sweep[s][k]
+            assert np.linalg.norm(g.factors_per_sweep[s][k] - fo) / np.linalg.norm(fo) <= FACTOR_TOL
+    assert np.array_equal(np.array([t.fitness for t in o.trace]), golden["c1_fitness"])
+
+
+def test_c4_ill_conditioned_reduced(ctx, port):
+    """C4 construction (congruence 0.9, log-scaled columns, 1e-4 noise) at 48^3 R20."""
+    import paper_2503_18759_b200 as cpd
+    x = port.synth_baseline(1, (48, 48, 48), 20, 1e-4, META["truth_seeds"]["c4"])
+    g = cpd.als_qr_bre(x, cfg_of(20, 60, seed=META["init_seed"]), ctx=ctx)
+    o = port.solve(x, 20, 60, extrapolate=True, seed=META["init_seed"])
+    compare(g, o, factor_tol=1e-8)
+
+
+def test_c3_shape_4th_order_reduced(ctx, port):
+    import paper_2503_18759_b200 as cpd
+    x = port.synth_baseline(0, (24, 24, 24, 24), 16, 1e-2, META["truth_seeds"]["c3"])
+    g = cpd.als_qr_bre(x, cfg_of(16, 20, seed=META["init_seed"]), ctx=ctx)
+    o = port.solve(x, 16, 20, extrapolate=True, seed=META["init_seed"])
+    compare(g, o)
+
+
+def test_q0_structure_observed(ctx, port):
+    """solver_test.cpp:182-195"""
+    import paper_2503_18759_b200 as cpd
+    x = port.rng_normals(557, 9 * 8 * 7).reshape(9, 8, 7)
+    seen = []
+
+    def obs(sweep, mode, q0):
+        seen.append((sweep, mode))
+        assert abs(q0[0, 0] - 1.0) <= 1e-12
+        assert np.abs(q0[0, 1:]).max() <= 1e-12
+        assert np.abs(q0[1:, 0]).max() <= 1e-12
+
+    cpd.cp_als_qr(x, cfg_of(3, 4, seed=11, q0_observer=obs), ctx=ctx)
+    assert len(seen) == 12
+
+
+def test_beta_zero_and_gate(ctx, port):
+    """solver_test.cpp:226-249: beta 0 == plain branch reuse; gap 0 never fires."""
+    import paper_2503_18759_b200 as cpd
+    x = port.rng_normals(577, 8 * 7 * 6).reshape(8, 7, 6)
+    a = cpd.als_qr_bre(x, cfg_of(3, 6, seed=21, beta_override=0.0), ctx=ctx)
+    b = cpd.cp_als_qr(x, cfg_of(3, 6, seed=21), ctx=ctx)
+    assert [t.fitness for t in a.trace] == [t.fitness for t in b.trace]
+    for fa, fb in zip(a.model.factors, b.model.factors):
+        assert np.array_equal(fa, fb)
+    c = cpd.als_qr_bre(x, cfg_of(3, 6, seed=23, activation_gap=0.0), ctx=ctx)
+    assert all(t.beta_used == 0.0 for t in c.trace)
+
+
+def test_deterministic(ctx, port):
+    """solver_test.cpp:272-282: bit-identical traces across runs."""
+    import paper_2503_18759_b200 as cpd
+    x = port.rng_normals(593, 7 * 6 * 5).reshape(7, 6, 5)
+    r1 = cpd.cp_als_qr(x, cfg_of(2, 6, seed=77), ctx=ctx)
+    r2 = cpd.cp_als_qr(x, cfg_of(2, 6, seed=77), ctx=ctx)
+    assert [(t.fitness, t.raw_radicand) for t in r1.trace] == \
+        [(t.fitness, t.raw_radicand) for t in r2.trace]
+
+
+def test_rejections(ctx, port):
+    import paper_2503_18759_b200 as cpd
+    x = port.rng_normals(571, 6 * 5 * 2).reshape(6, 5, 2)
+    with pytest.raises(ValueError):
+        cpd.cp_als_qr(x, cfg_of(3, 3), ctx=ctx)
+    with pytest.raises(ValueError):
+        cpd.cp_als_qr(np.zeros((4, 4, 4)), cfg_of(2, 3), ctx=ctx)
+    with pytest.raises(ValueError):
+        cpd.cp_als_qr(x, cfg_of(2, 0), ctx=ctx)
+
+
+def test_early_stop_on_threshold(ctx, port):
+    """solver_test.cpp:284-294: an exact low-rank tensor stops early."""
+    import paper_2503_18759_b200 as cpd
+    a = [port.rng_normals(600 + k, d * 2).reshape(d, 2) for k, d in enumerate((6, 5, 4))]
+    x = np.einsum("ir,jr,kr->ijk", *a)
+    r = cpd.cp_als_qr(x, cfg_of(2, 50, seed=3, fitness_threshold=0.999), ctx=ctx)
+    assert len(r.trace) < 50 and r.trace[-1].fitness >= 0.999
+
+
+def test_teacher_forced_one_sweep(ctx, port):
+    """load the oracle state at sweep k, run one GPU sweep, compare
+    with the oracle's sweep k+1 -- separates kernel error from drift."""
+    import paper_2503_18759_b200 as cpd
+    from oracle.pyoracle import SweepState
+    x = port.synth_baseline(1, (40, 40, 40), 8, 1e-4, 77)
+    for k in (1, 2, 5, 9):
+        s0 =port.solve(x, 8, k, extrapolate=True, seed=7, state=SweepState(
+            0, np.ones(8), port_init(port, x.shape, 8, 7)))
+        st = s0.state
+        o = port.solve(x, 8, 1, extrapolate=True, seed=7, state=SweepState(**st))
+        g = ctx_solve_state(ctx, x, 8, st)
+        assert g.trace[0].iteration == k + 1
+        assert g.trace[0].flops == o.trace[0]["flops"]
+        assert abs(g.trace[0].fitness - o.trace[0]["fitness"]) <= 1e-12
+        for fg, fo in zip(g.model.factors, o.factors):
+            assert np.linalg.norm(fg - fo) / np.linalg.norm(fo) <= 1e-12
+
+
+def port_init(port, dims, rank, seed):
+    draws = port.rng_normals(seed, sum(d * rank for d in dims))
+    out, off = [], 0
+    for d in dims:
+        out.append(port.normalize_columns(draws[off:off + d * rank].reshape(d, rank))[0])
+        off += d * rank
+    return out
+
+
+def ctx_solve_state(ctx, x, rank, st):
+    import paper_2503_18759_b200 as cpd
+    ctx.set_tensor(x)
+    state = cpd.SweepState(**st)
+    return ctx.solve(cfg_of(rank, 1, seed=7), extrapolate=True, state=state)
