@@ -62,14 +62,13 @@ def test_c1_full_config(ctx, port, golden):
     g = cpd.als_qr_bre(x, cfg_of(10, 50, seed=META["init_seed"]), ctx=ctx, dump_per_sweep=True)
     o = port.solve(x, 10, 50, extrapolate=True, seed=META["init_seed"], dump_per_sweep=True)
     compare(g, o)
-    assert np.array_equal([t.fitness for t in g.trace][:0], [])
     first = next(t.iteration for t in g.trace if t.beta_used != 0.0)
     assert first == 8
     for s in range(50):
         for k in range(3):
             fo = o.factors_per_sweep[s][k]
             assert np.linalg.norm(g.factors_per_sweep[s][k] - fo) / np.linalg.norm(fo) <= FACTOR_TOL
-    assert np.array_equal(np.array([t.fitness for t in o.trace]), golden["c1_fitness"])
+    assert np.array_equal(np.array([t["fitness"] for t in o.trace]), golden["c1_fitness"])
 
 
 def test_c4_ill_conditioned_reduced(ctx, port):
@@ -155,16 +154,18 @@ def test_teacher_forced_one_sweep(ctx, port):
     from oracle.pyoracle import SweepState
     x = port.synth_baseline(1, (40, 40, 40), 8, 1e-4, 77)
     for k in (1, 2, 5, 9):
-        s0 =port.solve(x, 8, k, extrapolate=True, seed=7, state=SweepState(
+        s0 = port.solve(x, 8, k, extrapolate=True, seed=7, state=SweepState(
             0, np.ones(8), port_init(port, x.shape, 8, 7)))
         st = s0.state
         o = port.solve(x, 8, 1, extrapolate=True, seed=7, state=SweepState(**st))
         g = ctx_solve_state(ctx, x, 8, st)
         assert g.trace[0].iteration == k + 1
         assert g.trace[0].flops == o.trace[0]["flops"]
-        assert abs(g.trace[0].fitness - o.trace[0]["fitness"]) <= 1e-12
+        # one sweep from identical state: only kernel rounding separates the
+        # two; the radicand cancels ~3 digits at fit 0.999 (SURVEY.md 8c floor)
+        assert abs(g.trace[0].fitness - o.trace[0]["fitness"]) <= FIT_TOL * o.trace[0]["fitness"]
         for fg, fo in zip(g.model.factors, o.factors):
-            assert np.linalg.norm(fg - fo) / np.linalg.norm(fo) <= 1e-12
+            assert np.linalg.norm(fg - fo) / np.linalg.norm(fo) <= 1e-11
 
 
 def port_init(port, dims, rank, seed):
