@@ -161,6 +161,18 @@ int cpdb_solve(cpdb_ctx* ctx, const cpdb_config* cfg, cpdb_state* state, cpdb_tr
                uint64_t* trace_len, double* out_lambda, double* out_factors,
                double* factors_per_sweep, double* lambda_per_sweep, cpdb_q0_observer observer,
                void* observer_user);
+/* The same run as a resumable session: begin = run_qr setup
+ * (solvers.hpp:217-241), run = n more sweeps of the loop (:243-302), end =
+ * model + sweep-boundary state (:304-308).  cfg->max_iterations bounds the
+ * plan; *finished is set once it is exhausted or the fitness threshold hit. */
+typedef struct cpdb_session cpdb_session;
+int cpdb_session_begin(cpdb_ctx* ctx, const cpdb_config* cfg, const cpdb_state* state,
+                       cpdb_session** out);
+int cpdb_session_run(cpdb_session* s, uint64_t sweeps, cpdb_trace_row* trace, uint64_t* rows,
+                     int32_t* finished);
+int cpdb_session_end(cpdb_session* s, cpdb_state* state, double* out_lambda,
+                     double* out_factors);
+void cpdb_session_destroy(cpdb_session* s);
 int cpdb_profile_get(cpdb_ctx* ctx, cpdb_profile* out);
 /* Enable/disable per-kernel event timing inside cpdb_solve (default on; off
  * removes the events from the stream).  CUDA-graph capture of the sweeps is

@@ -182,6 +182,10 @@ class Context:
         _raise(_lib().cpdb_set_options(self._h, int(timing), int(graphs)))
 
     # ---- solver
+    def session(self, cfg: "SolverConfig", *, extrapolate: bool) -> "SolverSession":
+        """Resumable run_qr (cpdb_session_*): begin now, then run(n) sweeps at a time."""
+        return SolverSession(self, cfg, extrapolate)
+
     def solve(self, cfg: "SolverConfig", *, extrapolate: bool, init: Optional["KruskalModel"] = None,
               state: Optional["SweepState"] = None, dump_per_sweep: bool = False) -> "SolveResult":
         dims = self.dims
@@ -259,6 +263,58 @@ class Context:
                 active_beta=float(st.active_beta) if st.has_active_beta else None,
                 prev_fitness=float(st.prev_fitness) if st.has_prev_fitness else None)
         return res
+
+
+def _config(cfg: "SolverConfig", extrapolate: bool) -> _cpdb.Config:
+    return _cpdb.Config(rank=int(cfg.rank), max_iterations=int(cfg.max_iterations),
+                        fitness_threshold=float(cfg.fitness_threshold),
+                        strategy=_strategy(cfg.strategy), extrapolate=1 if extrapolate else 0,
+                        alpha=float(cfg.alpha),
+                        has_beta_override=0 if cfg.beta_override is None else 1,
+                        beta_override=0.0 if cfg.beta_override is None else float(cfg.beta_override),
+                        activation_gap=float(cfg.activation_gap), seed=int(cfg.seed))
+
+
+class SolverSession:
+    """begin / run(n) / end over the context's tensor (include/cpdb.h)."""
+
+    def __init__(self, ctx: Context, cfg: "SolverConfig", extrapolate: bool):
+        self.ctx, self.cfg = ctx, cfg
+        self._c = _config(cfg, extrapolate)
+        h = C.c_void_p()
+        _raise(_lib().cpdb_session_begin(ctx.handle, C.byref(self._c), None, C.byref(h)))
+        self._h = h
+        self.finished = False
+
+    def run(self, sweeps: int) -> List["TraceRow"]:
+        rows = (_cpdb.TraceRow * max(int(sweeps), 1))()
+        n = C.c_uint64()
+        fin = C.c_int32()
+        _raise(_lib().cpdb_session_run(self._h, int(sweeps), rows, C.byref(n), C.byref(fin)))
+        self.finished = bool(fin.value)
+        return [TraceRow.from_c(rows[i]) for i in range(n.value)]
+
+    def end(self) -> "KruskalModel":
+        R = int(self.cfg.rank)
+        lam = np.empty(R)
+        fac = np.empty(sum(d * R for d in self.ctx.dims))
+        _raise(_lib().cpdb_session_end(self._h, None, _p(lam), _p(fac)))
+        out, off = [], 0
+        for d in self.ctx.dims:
+            out.append(fac[off:off + d * R].reshape(d, R).copy())
+            off += d * R
+        return KruskalModel(lam, out)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            _lib().cpdb_session_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 _DEFAULT: Optional[Context] = None

@@ -109,6 +109,11 @@ SIGNATURES = {
     "cpdb_tensor_norm_sq": (C.c_int, [CTX, P]),
     "cpdb_solve": (C.c_int, [CTX, C.POINTER(Config), C.POINTER(State), C.POINTER(TraceRow), U64P,
                              P, P, P, P, Q0Observer, C.c_void_p]),
+    "cpdb_session_begin": (C.c_int, [CTX, C.POINTER(Config), C.POINTER(State), C.POINTER(C.c_void_p)]),
+    "cpdb_session_run": (C.c_int, [C.c_void_p, C.c_uint64, C.POINTER(TraceRow), U64P,
+                                   C.POINTER(C.c_int32)]),
+    "cpdb_session_end": (C.c_int, [C.c_void_p, C.POINTER(State), P, P]),
+    "cpdb_session_destroy": (None, [C.c_void_p]),
     "cpdb_profile_get": (C.c_int, [CTX, C.POINTER(Profile)]),
     "cpdb_set_options": (C.c_int, [CTX, C.c_int32, C.c_int32]),
     "cpdb_ttm": (C.c_int, [CTX, P, U64P, C.c_uint32, P, C.c_uint64, C.c_uint32, P]),

@@ -14,6 +14,7 @@
 #include "prims.hpp"
 #include "runtime.hpp"
 #include "schedule.hpp"
+#include "session.hpp"
 
 using cpdb::Fail;
 using cpdb::fail;
@@ -283,6 +284,52 @@ int cpdb_solve(cpdb_ctx* c, const cpdb_config* cfg, cpdb_state* state, cpdb_trac
         cpdb::solve(c, *cfg, state, trace, trace_len, out_lambda, out_factors, factors_per_sweep,
                     lambda_per_sweep, observer, observer_user);
     });
+}
+
+int cpdb_session_begin(cpdb_ctx* c, const cpdb_config* cfg, const cpdb_state* state,
+                       cpdb_session** out) {
+    if (!out) return CPDB_INVALID_ARGUMENT;
+    *out = nullptr;
+    cpdb_session* ss = new (std::nothrow) cpdb_session();
+    if (!ss) return CPDB_OUT_OF_MEMORY;
+    const int rc = guarded([&] {
+        use_device(c);
+        if (!cfg) fail(CPDB_INVALID_ARGUMENT, "null config");
+        ss->s.begin(c, *cfg, state);
+    });
+    if (rc != CPDB_OK) {
+        delete ss;
+        return rc;
+    }
+    *out = ss;
+    return CPDB_OK;
+}
+
+int cpdb_session_run(cpdb_session* ss, uint64_t sweeps, cpdb_trace_row* trace, uint64_t* rows,
+                     int32_t* finished) {
+    return guarded([&] {
+        if (!ss) fail(CPDB_INVALID_ARGUMENT, "null session");
+        use_device(ss->s.c);
+        const uint64_t n = ss->s.run(sweeps, trace, nullptr, nullptr, nullptr, nullptr);
+        if (rows) *rows = n;
+        if (finished)
+            *finished = (ss->s.converged || ss->s.done >= ss->s.plan.sweeps.size()) ? 1 : 0;
+    });
+}
+
+int cpdb_session_end(cpdb_session* ss, cpdb_state* state, double* out_lambda,
+                     double* out_factors) {
+    return guarded([&] {
+        if (!ss) fail(CPDB_INVALID_ARGUMENT, "null session");
+        use_device(ss->s.c);
+        ss->s.end(state, out_lambda, out_factors);
+    });
+}
+
+void cpdb_session_destroy(cpdb_session* ss) {
+    if (!ss) return;
+    if (ss->s.c) cudaSetDevice(ss->s.c->device);
+    delete ss;
 }
 
 int cpdb_profile_get(cpdb_ctx* c, cpdb_profile* out) {

@@ -1,0 +1,604 @@
+// The device-resident CP-ALS-QR driver (B200 replacement of detail::run_qr,
+// /root/reference/proj/include/cpd/solvers.hpp:215-309) as a resumable
+// session: begin() is the run_qr setup (:217-241), run(n) executes n sweeps of
+// the loop (:243-302), end() returns the model (:304-308) and the
+// sweep-boundary state.  cpdb_solve = begin + run(max_iterations) + end.
+//
+// The host keeps exactly what the reference keeps on the host -- the plan,
+// factor versions and cache stamps (freshness is checked before every cached
+// read, dim_tree.hpp:506-513), the beta state machine and the stop test --
+// and every tensor and matrix lives in HBM.  Per mode update n (solvers.hpp:
+// 249-289) the stream carries
+//   launch_zqr     Q0, R0 of Khatri-Rao(R_k, k != n)           (:250-255)
+//   launch_ttm...  the scheduled TTM chain, cache in HBM        (:267)
+//   launch_vgemm   V = Y_(n) Q0_hat, extrapolation fused        (:258-271,277-284)
+//   launch_finish  A_hat, normalise, lambda, factor QR, fitness (:272-275,291)
+// and the host synchronises once per sweep to read the fitness scalar.
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+
+#include "comm.hpp"
+#include "cpd/rng.hpp"
+#include "runtime.hpp"
+#include "session.hpp"
+
+namespace cpdb {
+namespace {
+
+std::string set_name(uint32_t s, uint32_t order) {
+    std::string out = "Y(";
+    bool first = true;
+    for (uint32_t m = 0; m < order; ++m)
+        if (s & (1u << m)) {
+            if (!first) out += ',';
+            out += std::to_string(m + 1);
+            first = false;
+        }
+    return out + ")";
+}
+
+}  // namespace
+
+cudaEvent_t EventPool::get() {
+    cudaEvent_t e;
+    if (!free_.empty()) {
+        e = free_.back();
+        free_.pop_back();
+    } else {
+        CPDB_CK(cudaEventCreate(&e));
+    }
+    used.push_back(e);
+    return e;
+}
+
+void EventPool::recycle() {
+    free_.insert(free_.end(), used.begin(), used.end());
+    used.clear();
+}
+
+EventPool::~EventPool() {
+    for (auto e : free_) cudaEventDestroy(e);
+    for (auto e : used) cudaEventDestroy(e);
+}
+
+Session::~Session() {
+    if (c && c->stream) cudaStreamSynchronize(c->stream);
+    if (t_start) cudaEventDestroy(t_start);
+}
+
+// ---------------------------------------------------------------- setup
+void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* state) {
+    c = ctx;
+    cfg = config;
+    // SolverConfig::validate (solvers.hpp:41-49) and run_qr guards (:217-224)
+    if (cfg.rank == 0) fail(CPDB_INVALID_ARGUMENT, "SolverConfig: rank must be >= 1");
+    if (cfg.max_iterations == 0)
+        fail(CPDB_INVALID_ARGUMENT, "SolverConfig: need at least one iteration");
+    if (!(cfg.fitness_threshold >= 0.0 && cfg.fitness_threshold <= 1.0))
+        fail(CPDB_INVALID_ARGUMENT, "SolverConfig: fitness threshold must be in [0,1]");
+    if (!std::isfinite(cfg.alpha) || !std::isfinite(cfg.activation_gap))
+        fail(CPDB_INVALID_ARGUMENT, "SolverConfig: alpha and activation gap must be finite");
+    if (cfg.strategy < 0 || cfg.strategy > 2) fail(CPDB_INVALID_ARGUMENT, "unknown strategy");
+    require_tensor(c);
+    order = static_cast<uint32_t>(c->dims.size());
+    if (order < 2) fail(CPDB_INVALID_ARGUMENT, "cp_als_qr: tensor order must be >= 2");
+    if (order > CPDB_MAX_ORDER) fail(CPDB_INVALID_ARGUMENT, "cp_als_qr: order above 8");
+    nx2 = ctx_norm_sq(c);
+    if (nx2 == 0.0) fail(CPDB_INVALID_ARGUMENT, "cp_als_qr: zero-norm tensor");
+    for (uint32_t k = 0; k < order; ++k)
+        if (cfg.rank > c->dims[k])
+            fail(CPDB_INVALID_ARGUMENT,
+                 "cp_als_qr: rank must not exceed any mode extent (compact QR)");
+    if (cfg.rank > 64)
+        fail(CPDB_INVALID_ARGUMENT, "cp_als_qr: ranks above 64 are not supported on the device");
+    R = static_cast<uint32_t>(cfg.rank);
+    Rp = ttm_rpad(R);
+    extrap = cfg.extrapolate != 0;
+    const Strategy strategy =
+        extrap ? Strategy::branch_reuse : static_cast<Strategy>(cfg.strategy);
+    done = state ? state->sweeps_done : 0;
+    first_sweep = done;
+    try {
+        plan = build_plan(order, strategy, done + cfg.max_iterations);
+    } catch (const SchedError& e) {
+        fail(e.code, e.what);
+    }
+    sharded = c->world > 1;
+    s = c->stream;
+    zrows = 1;
+    for (uint32_t k = 1; k < order; ++k) zrows *= R;
+    maxI = 0;
+    nfac = 0;
+    for (uint64_t d : c->dims) {
+        maxI = std::max(maxI, d);
+        nfac += d * R;
+    }
+    c->prof = cpdb_profile{};
+    launches0 = c->launches;
+
+    // ---- factor state (factor_state.hpp:28-34) -----------------------------
+    fb.resize(order);
+    for (uint32_t k = 0; k < order; ++k) {
+        const uint64_t I = c->dims[k];
+        fb[k].a.ensure(I * R);
+        fb[k].q.ensure(I * R);
+        fb[k].qp.ensure(uint64_t(ttm_kpad(I)) * Rp);
+        fb[k].r.ensure(uint64_t(R) * R);
+    }
+    lam.ensure(R);
+    {
+        std::vector<double> init(nfac);
+        const bool given = state && state->factors;
+        if (given) {
+            std::memcpy(init.data(), state->factors, nfac * sizeof(double));
+        } else {
+            cpd::Rng rng(cfg.seed);  // initial_factors, solvers.hpp:116-122
+            for (double& v : init) v = rng.normal();
+        }
+        uint64_t off = 0;
+        for (uint32_t k = 0; k < order; ++k) {
+            const uint64_t I = c->dims[k];
+            CPDB_CK(cudaMemcpyAsync(fb[k].a.p, init.data() + off, I * R * sizeof(double),
+                                    cudaMemcpyHostToDevice, s));
+            if (!given) {
+                CPDB_CK(normalize_exact(fb[k].a.p, I, R, nullptr, s));
+                c->launches += 1;
+            }
+            off += I * R;
+        }
+        std::vector<double> l(R, 1.0);
+        if (state && state->lambda) l.assign(state->lambda, state->lambda + R);
+        CPDB_CK(cudaMemcpyAsync(lam.p, l.data(), R * sizeof(double), cudaMemcpyHostToDevice, s));
+        CPDB_CK(cudaStreamSynchronize(s));
+    }
+    fscratch.ensure(maxI * (R + 1));
+    vout.ensure(maxI * R);
+    fitbuf.ensure(8);
+    q0buf.ensure(zrows * R);
+    q1buf.ensure(zrows * R);
+    r0buf.ensure(uint64_t(R) * R);
+    zwork.ensure(zqr_work_doubles(R) + uint64_t(4 * c->sms) * R * R);
+    vfull.ensure(maxI * R);
+    vfitfull.ensure(maxI * R);
+    versions.assign(order, 1);
+    CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
+    for (uint32_t k = 0; k < order; ++k) qr_factor(k);
+    pack_local0();
+
+    // ---- Q0 history (reference row order on the host side) -----------------
+    perm = natural_to_reference(order, R);
+    hist.resize(order);
+    has_hist.assign(order, false);
+    for (uint32_t n = 0; n < order; ++n) hist[n].ensure(zrows * R);
+    if (state && state->q0_history) {
+        std::vector<double> nat(zrows * R);
+        for (uint32_t n = 0; n < order; ++n) {
+            if (!(state->history_mask & (1u << n))) continue;
+            const double* ref = state->q0_history + uint64_t(n) * zrows * R;
+            for (uint64_t i = 0; i < zrows; ++i)
+                std::memcpy(&nat[i * R], ref + perm[i] * R, R * sizeof(double));
+            CPDB_CK(cudaMemcpyAsync(hist[n].p, nat.data(), zrows * R * sizeof(double),
+                                    cudaMemcpyHostToDevice, s));
+            CPDB_CK(cudaStreamSynchronize(s));
+            has_hist[n] = true;
+        }
+    }
+    if (extrap && cfg.has_beta_override) {
+        has_beta = true;
+        beta = cfg.beta_override;
+    }
+    if (extrap && state && state->has_active_beta && !has_beta) {
+        has_beta = true;
+        beta = state->active_beta;
+    }
+    has_prev = state && state->has_prev_fitness;
+    prev_fit = has_prev ? state->prev_fitness : 0.0;
+
+    // cost accounting continues from the sweeps already done (dim_tree.hpp:523-526)
+    total = done > 0 ? measured_cost(plan, c->dims, R, done) : Cost{};
+
+    // rebuild the retained intermediates from X and the current factors
+    if (done > 0) {
+        for (uint32_t key : retained_keys(plan, done - 1, order - 1)) {
+            if (cache.count(key)) continue;
+            std::vector<uint64_t> d = c->ldims;
+            const double* cur = c->x;
+            bool cur_sharded = sharded;
+            DevBuf tmp[2];
+            int w = 0;
+            for (uint32_t k = order; k-- > 0;) {
+                if (key & (1u << k)) continue;
+                std::vector<uint64_t> nd = d;
+                nd[k] = R;
+                double* out = tmp[w].ensure(numel(nd));
+                ttm_step(cur, d, cur_sharded, k, out, false);
+                if (k == 0) cur_sharded = false;
+                cur = out;
+                d = nd;
+                w ^= 1;
+            }
+            Slot& sl = cache[key];
+            sl.buf.ensure(numel(d));
+            CPDB_CK(cudaMemcpyAsync(sl.buf.p, cur, numel(d) * sizeof(double),
+                                    cudaMemcpyDeviceToDevice, s));
+            sl.valid = true;
+            sl.dims = d;
+            sl.sharded = sharded && (key & 1u);
+            sl.stamps.assign(order, 0);
+            for (uint32_t k = 0; k < order; ++k)
+                if (!(key & (1u << k))) sl.stamps[k] = versions[k];
+            CPDB_CK(cudaStreamSynchronize(s));
+        }
+        events.recycle();
+        timers.clear();
+    }
+    ybuf.resize(order);
+    for (uint32_t n = 0; n < order; ++n) ybuf[n].ensure(numel(local_dims_of(1u << n)));
+    CPDB_CK(cudaEventCreate(&t_start));
+    CPDB_CK(cudaEventRecord(t_start, s));
+    CPDB_CK(cudaStreamSynchronize(s));
+}
+
+std::vector<uint64_t> Session::local_dims_of(uint32_t key) const {
+    std::vector<uint64_t> d(order);
+    for (uint32_t k = 0; k < order; ++k) d[k] = (key & (1u << k)) ? c->ldims[k] : R;
+    return d;
+}
+
+void Session::qr_factor(uint32_t k) {
+    FinishArgs f{};
+    f.init = 1;
+    f.I = c->dims[k];
+    f.R = R;
+    f.a_out = fb[k].a.p;
+    f.q_out = fb[k].q.p;
+    f.qp_out = fb[k].qp.p;
+    f.r_out = fb[k].r.p;
+    f.lambda = lam.p;
+    f.scratch = fscratch.p;
+    f.status = c->dstatus;
+    f.v_out = vout.p;
+    CPDB_CK(launch_finish(f, s));
+    c->launches += 1;
+}
+
+// Sharded runs contract the leading mode with this rank's rows of Q_0 only;
+// they get their own packed copy (no row-alignment constraint).
+void Session::pack_local0() {
+    if (!sharded) return;
+    qp0_local.ensure(uint64_t(ttm_kpad(c->rows)) * Rp);
+    CPDB_CK(pack_q(fb[0].q.p + c->row_begin * R, qp0_local.p, uint32_t(c->rows), R, s));
+    c->launches += 1;
+}
+
+void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, bool src_sharded,
+                       uint32_t k, double* dst, bool is_root) {
+    const double* q = fb[k].q.p;
+    const double* qp = fb[k].qp.p;
+    if (k == 0 && src_sharded) {
+        q += c->row_begin * R;
+        qp = qp0_local.p;
+    }
+    Timer t;
+    if (c->timing) {
+        t.a = events.get();
+        t.b = events.get();
+        t.kind = is_root ? 0 : 1;
+        CPDB_CK(cudaEventRecord(t.a, s));
+    }
+    run_ttm(c, src, sd, k, q, qp, R, dst);
+    if (c->timing) {
+        CPDB_CK(cudaEventRecord(t.b, s));
+        const uint64_t nin = numel(sd);
+        const uint64_t nout = nin / sd[k] * R;
+        t.flops = 2.0 * double(nout) * double(sd[k]);
+        t.bytes = 8.0 * (double(nin) + double(nout) + double(sd[k]) * R);
+        timers.push_back(t);
+    }
+    if (src_sharded && k == 0 && sharded) {
+        Timer tc;
+        if (c->timing) {
+            tc.a = events.get();
+            tc.b = events.get();
+            tc.kind = 2;
+            CPDB_CK(cudaEventRecord(tc.a, s));
+        }
+        allreduce_sum(c, dst, numel(sd) / sd[k] * R);
+        if (c->timing) {
+            CPDB_CK(cudaEventRecord(tc.b, s));
+            timers.push_back(tc);
+        }
+    }
+}
+
+// ---------------------------------------------------------------- one mode update
+void Session::mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer, void* user,
+                          double& beta_used) {
+    const Sweep& sw = plan.sweeps[sweep - 1];
+    const uint32_t n = sw.updates[b].mode;
+    const bool last = (b == order - 1);
+    const uint32_t root = plan.root();
+
+    // 1-2. Khatri-Rao + QR of the other R_k -> Q0, R0 (solvers.hpp:250-255)
+    ZqrArgs z{};
+    uint32_t t = 0;
+    for (uint32_t k = 0; k < order; ++k)
+        if (k != n) z.rmats[t++] = fb[k].r.p;
+    z.nm = order - 1;
+    z.R = R;
+    z.zrows = zrows;
+    z.q1 = q1buf.p;
+    z.q0 = q0buf.p;
+    z.r0 = r0buf.p;
+    z.work = zwork.p;
+    z.status = c->dstatus;
+    CPDB_CK(launch_zqr(z, s, c->sms));
+    c->launches += 4;
+    if (observer) {
+        std::vector<double> nat(zrows * R), ref(zrows * R);
+        CPDB_CK(cudaMemcpyAsync(nat.data(), q0buf.p, zrows * R * sizeof(double),
+                                cudaMemcpyDeviceToHost, s));
+        CPDB_CK(cudaStreamSynchronize(s));
+        for (uint64_t i = 0; i < zrows; ++i)
+            std::memcpy(&ref[perm[i] * R], &nat[i * R], R * sizeof(double));
+        observer(user, sweep, n, ref.data(), zrows, R);
+    }
+    // 3. extrapolation gate (solvers.hpp:260-265)
+    const bool use_ex = extrap && has_beta && beta != 0.0 && has_hist[n];
+    if (use_ex) beta_used = beta;
+
+    // 4. the scheduled TTM chain (execute, dim_tree.hpp:496-541)
+    for (const Step& st : sw.updates[b].steps) {
+        const double* src;
+        std::vector<uint64_t> sd;
+        std::vector<uint64_t> stamp(order, 0);
+        bool src_sh;
+        if (st.source == root) {
+            src = c->x;
+            sd = c->ldims;
+            src_sh = sharded;
+        } else {
+            auto it = cache.find(st.source);
+            if (it == cache.end() || !it->second.valid)
+                fail(CPDB_LOGIC_ERROR, "execute: scheduled source " + set_name(st.source, order) +
+                                           " missing from cache");
+            for (uint32_t m = 0; m < order; ++m)
+                if (it->second.stamps[m] && it->second.stamps[m] != versions[m])
+                    fail(CPDB_STALE_INTERMEDIATE,
+                         "execute: stale intermediate " + set_name(st.source, order));
+            src = it->second.buf.p;
+            sd = it->second.dims;
+            stamp = it->second.stamps;
+            src_sh = it->second.sharded;
+        }
+        std::vector<uint64_t> od = sd;
+        od[st.contract] = R;
+        double* dst =
+            (st.produces == (1u << n)) ? ybuf[n].p : cache[st.produces].buf.ensure(numel(od));
+        ttm_step(src, sd, src_sh, st.contract, dst, st.source == root);
+        // global-extent flop count, exactly as the reference counts it
+        uint64_t gout = 1;
+        for (uint32_t k = 0; k < order; ++k)
+            gout *= (st.produces & (1u << k)) ? c->dims[k] : uint64_t(R);
+        total.flops += 2ull * gout * c->dims[st.contract];
+        if (st.source == root) ++total.roots;
+        stamp[st.contract] = versions[st.contract];
+        if (st.produces != (1u << n)) {
+            Slot& sl = cache[st.produces];
+            sl.valid = true;
+            sl.dims = od;
+            sl.stamps = stamp;
+            sl.sharded = src_sh && st.contract != 0;
+        }
+    }
+    const std::vector<ModeSet> keep = retained_keys(plan, sweep - 1, b);
+    for (auto& kv : cache)
+        if (std::find(keep.begin(), keep.end(), kv.first) == keep.end()) kv.second.valid = false;
+
+    // 5. V = Y_(n) Q0_hat (+ the unextrapolated V for the fitness, :277-284)
+    const std::vector<uint64_t> yd = local_dims_of(1u << n);
+    VgemmArgs v{};
+    v.y = ybuf[n].p;
+    v.q0 = q0buf.p;
+    v.hist = use_ex ? hist[n].p : nullptr;
+    v.beta = beta;
+    v.alpha = cfg.alpha;
+    v.extrap = use_ex ? 1 : 0;
+    v.dual = (last && use_ex) ? 1 : 0;
+    v.I = yd[n];
+    v.O = 1;
+    for (uint32_t k = 0; k < n; ++k) v.O *= R;
+    v.J = 1;
+    for (uint32_t k = n + 1; k < order; ++k) v.J *= R;
+    v.R = R;
+    const size_t part = size_t(vgemm_max_split()) * v.I * R;
+    v.vpart = vpart.ensure(part);
+    v.vfitpart = v.dual ? vfitpart.ensure(part) : nullptr;
+    CPDB_CK(launch_vgemm(v, s, c->sms));
+    c->launches += 1;
+    const double* vsrc = v.vpart;
+    const double* vfsrc = v.vfitpart;
+    uint32_t nsplit = v.nsplit;
+    if (sharded && n == 0) {
+        // this rank's rows of V -> the full V on every rank
+        CPDB_CK(reduce_splits(v.vpart, nsplit, v.I * R, vfull.p + c->row_begin * R, s));
+        allgather(c, vfull.p, v.I * R);
+        vsrc = vfull.p;
+        if (v.dual) {
+            CPDB_CK(reduce_splits(v.vfitpart, nsplit, v.I * R, vfitfull.p + c->row_begin * R, s));
+            allgather(c, vfitfull.p, v.I * R);
+            vfsrc = vfitfull.p;
+        }
+        c->launches += v.dual ? 2 : 1;
+        nsplit = 1;
+    }
+    // 6-9. A_hat, lambda, factor QR, fitness (solvers.hpp:272-292)
+    FinishArgs f{};
+    f.init = 0;
+    f.vpart = vsrc;
+    f.vfitpart = vfsrc;
+    f.nsplit = nsplit;
+    f.dual = v.dual;
+    f.r0 = r0buf.p;
+    f.I = c->dims[n];
+    f.R = R;
+    f.v_out = vout.p;
+    f.a_out = fb[n].a.p;
+    f.q_out = fb[n].q.p;
+    f.qp_out = fb[n].qp.p;
+    f.r_out = fb[n].r.p;
+    f.lambda = lam.p;
+    f.scratch = fscratch.p;
+    f.fitness = last ? 1 : 0;
+    f.norm_x_sq = nx2;
+    f.fit_out = fitbuf.p;
+    f.status = c->dstatus;
+    CPDB_CK(launch_finish(f, s));
+    c->launches += 1;
+    if (n == 0) pack_local0();
+    ++versions[n];
+    if (extrap) {
+        hist[n].swap(q0buf);  // the history keeps the unextrapolated Q0 (:265)
+        has_hist[n] = true;
+    }
+}
+
+// ---------------------------------------------------------------- sweeps
+uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, double* lps,
+                      cpdb_q0_observer observer, void* user) {
+    uint64_t rows_out = 0;
+    const uint64_t last_sweep = plan.sweeps.size();
+    while (rows_out < nsweeps && !converged && done < last_sweep) {
+        const uint64_t sweep = done + 1;
+        const Sweep& sw = plan.sweeps[sweep - 1];
+        double beta_used = 0.0;
+        CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
+        for (uint32_t b = 0; b < order; ++b) mode_update(sweep, b, observer, user, beta_used);
+        cudaEvent_t e_end = events.get();
+        CPDB_CK(cudaEventRecord(e_end, s));
+        CPDB_CK(cudaMemcpyAsync(c->pinned, fitbuf.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        CPDB_CK(cudaMemcpyAsync(c->pinned + 2, c->dstatus, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CPDB_CK(cudaStreamSynchronize(s));
+        int status;
+        std::memcpy(&status, c->pinned + 2, sizeof(int));
+        if (status) {
+            if ((status & 0xFF) == 1)
+                fail(CPDB_SINGULAR_TRIANGULAR,
+                     "triangular solve: diagonal entry of column " + std::to_string(status >> 8) +
+                         " is ~0 (rank-deficient Khatri-Rao factor)");
+            fail(CPDB_SINGULAR_TRIANGULAR,
+                 "Cholesky QR breakdown: rank-deficient Khatri-Rao or factor matrix");
+        }
+        const double fit = c->pinned[0], raw = c->pinned[1];
+        float ms = 0.f;
+        CPDB_CK(cudaEventElapsedTime(&ms, t_start, e_end));
+        if (sweep == first_sweep + 1) c->prof.sweep1_ms = ms;
+        c->prof.solve_ms = ms;
+        for (const Timer& t : timers) {
+            float tm = 0.f;
+            CPDB_CK(cudaEventElapsedTime(&tm, t.a, t.b));
+            if (t.kind == 0) {
+                c->prof.root_ttms += 1;
+                c->prof.root_ttm_ms += tm;
+                c->prof.root_ttm_flops += t.flops;
+                c->prof.root_ttm_bytes += t.bytes;
+            } else if (t.kind == 1) {
+                c->prof.branch_ttm_ms += tm;
+            } else {
+                c->prof.comm_ms += tm;
+            }
+        }
+        timers.clear();
+        events.recycle();
+        if (trace) {
+            cpdb_trace_row& row = trace[rows_out];
+            std::memset(&row, 0, sizeof row);
+            row.iteration = sweep;
+            row.order = order;
+            for (uint32_t b = 0; b < order; ++b) row.update_order[b] = sw.updates[b].mode;
+            row.fitness = fit;
+            row.raw_radicand = raw;
+            row.wall_seconds = ms * 1e-3;
+            row.root_ttm_count = total.roots;
+            row.flops = total.flops;
+            row.beta_used = beta_used;
+        }
+        if (fps) {
+            uint64_t off = 0;
+            for (uint32_t k = 0; k < order; ++k) {
+                CPDB_CK(cudaMemcpy(fps + rows_out * nfac + off, fb[k].a.p,
+                                   c->dims[k] * R * sizeof(double), cudaMemcpyDeviceToHost));
+                off += c->dims[k] * R;
+            }
+        }
+        if (lps)
+            CPDB_CK(cudaMemcpy(lps + rows_out * R, lam.p, R * sizeof(double), cudaMemcpyDeviceToHost));
+        ++rows_out;
+        ++done;
+        // beta gate (solvers.hpp:297-300)
+        if (extrap && !has_beta && !cfg.has_beta_override && sweep >= 2 && has_prev) {
+            double b = 0.0;
+            if (cpdb_select_beta(prev_fit, fit, cfg.activation_gap, &b)) {
+                has_beta = true;
+                beta = b;
+            }
+        }
+        prev_fit = fit;
+        has_prev = true;
+        if (fit >= cfg.fitness_threshold) converged = true;  // :301
+    }
+    c->prof.sweeps = done - first_sweep;
+    c->prof.mode_update_ms =
+        c->prof.solve_ms - c->prof.root_ttm_ms - c->prof.branch_ttm_ms - c->prof.comm_ms;
+    c->prof.kernel_launches = c->launches - launches0;
+    return rows_out;
+}
+
+// ---------------------------------------------------------------- results
+void Session::end(cpdb_state* state, double* out_lambda, double* out_factors) {
+    auto get_factors = [&](double* dst) {
+        uint64_t off = 0;
+        for (uint32_t k = 0; k < order; ++k) {
+            CPDB_CK(cudaMemcpy(dst + off, fb[k].a.p, c->dims[k] * R * sizeof(double),
+                               cudaMemcpyDeviceToHost));
+            off += c->dims[k] * R;
+        }
+    };
+    if (out_lambda) CPDB_CK(cudaMemcpy(out_lambda, lam.p, R * sizeof(double), cudaMemcpyDeviceToHost));
+    if (out_factors) get_factors(out_factors);
+    if (!state) return;
+    state->sweeps_done = done;
+    if (state->lambda)
+        CPDB_CK(cudaMemcpy(state->lambda, lam.p, R * sizeof(double), cudaMemcpyDeviceToHost));
+    if (state->factors) get_factors(state->factors);
+    if (state->q0_history) {
+        state->history_mask = 0;
+        std::vector<double> nat(zrows * R);
+        for (uint32_t n = 0; n < order; ++n) {
+            if (!has_hist[n]) continue;
+            CPDB_CK(cudaMemcpy(nat.data(), hist[n].p, zrows * R * sizeof(double),
+                               cudaMemcpyDeviceToHost));
+            double* ref = state->q0_history + uint64_t(n) * zrows * R;
+            for (uint64_t i = 0; i < zrows; ++i)
+                std::memcpy(ref + perm[i] * R, &nat[i * R], R * sizeof(double));
+            state->history_mask |= 1u << n;
+        }
+    }
+    state->has_active_beta = has_beta ? 1 : 0;
+    state->active_beta = has_beta ? beta : 0.0;
+    state->has_prev_fitness = has_prev ? 1 : 0;
+    state->prev_fitness = has_prev ? prev_fit : 0.0;
+}
+
+void solve(cpdb_ctx* c, const cpdb_config& cfg, cpdb_state* state, cpdb_trace_row* trace,
+           uint64_t* trace_len, double* out_lambda, double* out_factors, double* fps,
+           double* lps, cpdb_q0_observer observer, void* user) {
+    Session ss;
+    ss.begin(c, cfg, state);
+    const uint64_t n = ss.run(cfg.max_iterations, trace, fps, lps, observer, user);
+    if (trace_len) *trace_len = n;
+    ss.end(state, out_lambda, out_factors);
+}
+
+}  // namespace cpdb

@@ -1,0 +1,74 @@
+// Solver session: the device-resident run_qr state between calls.
+#pragma once
+
+#include <cstdint>
+#include <map>
+#include <vector>
+
+#include "runtime.hpp"
+
+namespace cpdb {
+
+struct EventPool {
+    std::vector<cudaEvent_t> free_, used;
+    cudaEvent_t get();
+    void recycle();
+    ~EventPool();
+};
+
+struct FactorBufs {
+    DevBuf a, q, qp, r;  // A_n, Q_n, packed Q_n, R_n
+};
+
+struct Session {
+    cpdb_ctx* c = nullptr;
+    cpdb_config cfg{};
+    Plan plan;
+    uint32_t order = 0, R = 0, Rp = 0;
+    bool extrap = false, sharded = false;
+    uint64_t done = 0, first_sweep = 0;
+    uint64_t zrows = 1, maxI = 0, nfac = 0;
+    double nx2 = 0.0;
+    cudaStream_t s = nullptr;
+    uint64_t launches0 = 0;
+
+    std::vector<FactorBufs> fb;
+    DevBuf lam, qp0_local;
+    DevBuf fscratch, vpart, vfitpart, vfull, vfitfull, vout, fitbuf, q0buf, q1buf, r0buf, zwork;
+    std::vector<DevBuf> hist, ybuf;
+    std::vector<bool> has_hist;
+    std::vector<uint64_t> versions;
+    std::vector<uint64_t> perm;
+    std::map<uint32_t, Slot> cache;
+
+    bool has_beta = false, has_prev = false, converged = false;
+    double beta = 0.0, prev_fit = 0.0;
+    Cost total;
+
+    EventPool events;
+    std::vector<Timer> timers;
+    cudaEvent_t t_start = nullptr;
+
+    ~Session();
+    void begin(cpdb_ctx* ctx, const cpdb_config& cfg, const cpdb_state* state);
+    // Runs up to n sweeps (stops early on convergence or at max_iterations);
+    // returns the number of trace rows written.
+    uint64_t run(uint64_t n, cpdb_trace_row* trace, double* fps, double* lps,
+                 cpdb_q0_observer observer, void* user);
+    void end(cpdb_state* state, double* out_lambda, double* out_factors);
+
+private:
+    std::vector<uint64_t> local_dims_of(uint32_t key) const;
+    void qr_factor(uint32_t k);
+    void pack_local0();
+    void ttm_step(const double* src, const std::vector<uint64_t>& sd, bool src_sharded,
+                  uint32_t k, double* dst, bool is_root);
+    void mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer, void* user,
+                     double& beta_used);
+};
+
+}  // namespace cpdb
+
+struct cpdb_session {
+    cpdb::Session s;
+};
