@@ -79,6 +79,7 @@ void init_ctx(cpdb_ctx* c, int device) {
     CPDB_CK(cudaSetDevice(device));
     c->sms = p.multiProcessorCount;
     CPDB_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+    CPDB_CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
     CPDB_CK(cudaMalloc(&c->dstatus, 64));
     CPDB_CK(cudaMemset(c->dstatus, 0, 64));
     CPDB_CK(cudaMallocHost(&c->pinned, 64 * sizeof(double)));

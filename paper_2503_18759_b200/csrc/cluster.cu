@@ -1,0 +1,475 @@
+// Mode-update kernels as 8-CTA thread-block clusters (sm_100a DSMEM).
+//
+// The per-mode small-matrix work of CP-ALS-QR is a chain of row-parallel
+// triangular solves separated by R x R reductions (two Grams per
+// CholeskyQR2).  One CTA is FP64-throughput bound and a grid-wide barrier
+// costs microseconds; a cluster gives 8 SMs and barrier.cluster in a few
+// hundred cycles, with the Gram partials reduced through distributed shared
+// memory (rank 0 reads the other ranks' smem in a fixed order ->
+// deterministic).  Row solves are register-resident and lane-parallel, Grams
+// run on DMMA (rowalg.cuh).
+//
+//   finish_cluster_kernel   A_hat = V R0^-T, lambda, A_n, CholQR2(A_n) -> Q_n,
+//                           R_n, packed Q_n, fitness   (solvers.hpp:272-292,
+//                           linalg.hpp:192-242, factor_state.hpp:42-47,
+//                           kruskal.hpp:109-128)
+//   zqr_cluster_kernel      Q0, R0 of Khatri-Rao(R_k, k != n) when R^(N-1)
+//                           rows fit the cluster's smem  (solvers.hpp:250-255)
+#include <cooperative_groups.h>
+
+#include <cmath>
+
+#include "kernels.hpp"
+#include "rowalg.cuh"
+
+namespace cg = cooperative_groups;
+
+// phase timestamps for profiling (FinishArgs::ts, rank 0 thread 0)
+#define CPDB_TS(k) \
+    do { if (a.ts && rank == 0 && threadIdx.x == 0) a.ts[k] = globaltimer(); } while (0)
+
+namespace cpdb {
+namespace {
+
+constexpr int kCS = 8;    // cluster size (portable maximum)
+constexpr int kNT = 512;  // threads per CTA
+
+// rank 0: G = sum_r P_r over the cluster, fixed rank order
+__device__ void cluster_reduce(cg::cluster_group& cl, const double* P, int n, double* G) {
+    for (int e = threadIdx.x; e < n; e += kNT) {
+        double s = 0.0;
+#pragma unroll
+        for (int r = 0; r < kCS; ++r) s += cl.map_shared_rank(P, r)[e];
+        G[e] = s;
+    }
+}
+
+// shared-memory plan (doubles)
+template <int RM>
+struct Smem {
+    double *u, *ut, *dinv, *vec, *p, *g, *misc, *w;
+    __device__ Smem(double* sm, int R) {
+        u = sm;               // RM x RM   triangular factor of the row solves
+        ut = u + RM * RM;     // RM x RM   its transpose (LaneRow::utinv)
+        dinv = ut + RM * RM;  // RM
+        vec = dinv + RM;      // RM        1/lambda (or lambda on rank 0)
+        p = vec + RM;         // R x R     Gram partial (read through DSMEM)
+        g = p + R * R;        // R x R     rank 0: reduced Gram -> Cholesky
+        misc = g + R * R;     // 16
+        w = misc + 16;        // per x (R+1), then R x R scratch
+    }
+    static size_t doubles(int R, uint64_t per) {
+        return 2 * size_t(RM) * RM + 2 * RM + 2 * size_t(R) * R + 16 + per * (R + 1) +
+               size_t(R) * R;
+    }
+};
+
+template <int RM>
+__global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
+    using Row = LaneRow<RM>;
+    constexpr int T = Row::T, G = kNT / T;
+    constexpr int KC = (RM * RM + kNT - 1) / kNT;
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = int(cl.block_rank());
+    extern __shared__ double sm[];
+    __shared__ double red[32];
+    __shared__ int flag;
+    const int R = a.R, ld = R + 1;
+    const uint64_t I = a.I;
+    const int per = int((I + kCS - 1) / kCS);
+    const uint64_t r0 = uint64_t(per) * rank;
+    const int rows = int(r0 < I ? (I - r0 < uint64_t(per) ? I - r0 : uint64_t(per)) : 0);
+    Smem<RM> S(sm, R);
+    double* scratch = S.w + per * ld;
+    const int grp = threadIdx.x / T, q = threadIdx.x % T;
+    CPDB_TS(0);
+
+    double xk_part = 0.0;
+    if (!a.init) {
+        stage_tri<RM>(a.r0, R, R, S.u, S.dinv, kNT);
+        stage_tri_t<RM>(a.r0, R, R, S.ut, S.dinv, kNT);
+        __syncthreads();
+        CPDB_TS(16);
+        // R0 singular check (linalg.hpp:199-203), warp-parallel on the staged
+        // copy; every CTA decides identically
+        {
+            const int lane = threadIdx.x & 31;
+            double mx = 0.0;
+            for (int i = lane; i < R; i += 32) mx = fmax(mx, fabs(S.u[i * RM + i]));
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+            int bad = R;
+            for (int i = lane; i < R; i += 32)
+                if (fabs(S.u[i * RM + i]) <= 1e-14 * mx) bad = min(bad, i);
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) bad = min(bad, __shfl_xor_sync(0xffffffffu, bad, o));
+            if (bad < R) {
+                if (rank == 0 && threadIdx.x == 0) *a.status = 1 | (bad << 8);
+                return;  // uniform across the cluster
+            }
+        }
+        CPDB_TS(17);
+        // phase A: A_hat = V R0^-T (+ this row's share of <V_fit, A_hat R0^T>)
+        for (int li = grp; li < rows + (G - rows % G) % G; li += G) {
+            const bool act = li < rows;
+            Row x;
+            x.load(a.vpart + (act ? (r0 + li) : r0) * R, act ? R : 0, q);
+            x.utinv(S.ut, S.dinv, R, q);
+            if (a.fitness) {  // uniform branch: the lane groups shuffle inside
+                // <vf, a_hat R0^T> = sum_k a_hat[k] * (vf R0)[k]
+                Row vf, w;
+                vf.load((a.dual ? a.vfitpart : a.vpart) + (act ? (r0 + li) : r0) * R,
+                        act ? R : 0, q);
+                w.set_times_upper(vf, S.u, R, q);
+#pragma unroll
+                for (int s = 0; s < Row::S; ++s) xk_part = fma(x.t[s], w.t[s], xk_part);
+            }
+            if (act) x.store(S.w + li * ld, R, q);
+        }
+    } else {
+        for (int e = threadIdx.x; e < rows * R; e += kNT)
+            S.w[(e / R) * ld + e % R] = a.a_out[(r0 + e / R) * R + e % R];
+    }
+    __syncthreads();
+    CPDB_TS(1);
+    gram_dmma<kNT>(S.w, ld, rows, R, S.p, R);
+    if (!a.init && a.fitness) {
+        const double x = block_sum<kNT>(xk_part, red);
+        if (threadIdx.x == 0) S.misc[0] = x;
+    }
+    CPDB_TS(2);
+    cl.sync();  // ---- 1: Gram partials of A_hat ready
+    CPDB_TS(3);
+
+    if (rank == 0) {
+        cluster_reduce(cl, S.p, R * R, S.g);
+        if (!a.init && a.fitness && threadIdx.x == 0) {
+            double s = 0.0;
+            for (int r = 0; r < kCS; ++r) s += cl.map_shared_rank(S.misc, r)[0];
+            S.misc[1] = s;  // <V_fit, A_hat R0^T>
+        }
+        __syncthreads();
+        CPDB_TS(4);
+        if (!a.init) {
+            // lambda = column norms of A_hat = sqrt(diag G); G1 = D G D
+            for (int c = threadIdx.x; c < R; c += kNT) {
+                const double l = sqrt(S.g[c * R + c]);
+                scratch[c] = l;                             // lambda (published)
+                S.vec[c] = l < 1e-300 ? 0.0 : __drcp_rn(l);  // 1/lambda
+            }
+            __syncthreads();
+            for (int e = threadIdx.x; e < R * R; e += kNT) {
+                const double li = S.vec[e / R], lj = S.vec[e % R];
+                S.g[e] = (li == 0.0 || lj == 0.0) ? (e / R == e % R ? 1.0 : 0.0)
+                                                   : S.g[e] * li * lj;
+            }
+            __syncthreads();
+        }
+        const bool ok = block_chol<kNT, KC>(S.g, R, R);
+        if (threadIdx.x == 0) S.misc[2] = ok ? 0.0 : 1.0;
+        CPDB_TS(5);
+    }
+    cl.sync();  // ---- 2: lambda (rank 0's scratch), U1 (rank 0's g) published
+    CPDB_TS(6);
+    {
+        const double* g0 = cl.map_shared_rank(S.g, 0);
+        stage_tri<RM>(g0, R, R, S.u, S.dinv, kNT);
+        if (!a.init) {
+            const double* l0 = cl.map_shared_rank(scratch, 0);
+            for (int c = threadIdx.x; c < RM; c += kNT) {
+                const double l = c < R ? l0[c] : 0.0;
+                S.vec[c] = l < 1e-300 ? 0.0 : __drcp_rn(l);
+                if (rank == 0 && c < R) a.lambda[c] = l < 1e-300 ? 0.0 : l;
+            }
+        }
+        if (threadIdx.x == 0) flag = cl.map_shared_rank(S.misc, 0)[2] != 0.0;
+    }
+    cl.sync();  // rank 0 may reuse g / scratch only after every rank copied them
+    CPDB_TS(7);
+    if (flag) {
+        if (rank == 0 && threadIdx.x == 0) *a.status = 2;
+        return;  // uniform: every rank read the same flag
+    }
+    // phase B: A_n = A_hat / lambda (vanishing column -> e1), A1 = A_n U1^-1
+    for (int li = grp; li < rows + (G - rows % G) % G; li += G) {
+        const bool act = li < rows;
+        Row x;
+        x.load(S.w + (act ? li : 0) * ld, act ? R : 0, q);
+        if (!a.init) {
+#pragma unroll
+            for (int s = 0; s < Row::S; ++s) {
+                const int k = s * T + q;
+                if (k < R) {
+                    const double il = S.vec[k];
+                    x.t[s] = il == 0.0 ? ((r0 + li) == 0 ? 1.0 : 0.0) : x.t[s] * il;
+                }
+            }
+            if (act) x.store(a.a_out + (r0 + li) * R, R, q);
+        }
+        x.uinv(S.u, S.dinv, R, q);
+        if (act) x.store(S.w + li * ld, R, q);
+    }
+    __syncthreads();
+    CPDB_TS(8);
+    gram_dmma<kNT>(S.w, ld, rows, R, S.p, R);
+    CPDB_TS(9);
+    cl.sync();  // ---- 3: Gram partials of A1 ready
+    CPDB_TS(10);
+
+    if (rank == 0) {
+        cluster_reduce(cl, S.p, R * R, S.g);
+        __syncthreads();
+        const bool ok = block_chol<kNT, KC>(S.g, R, R);
+        if (threadIdx.x == 0) S.misc[2] = ok ? 0.0 : 1.0;
+        CPDB_TS(11);
+        if (ok) {
+            // R_n = U2 U1 (U1 in S.u, stride RM)
+            for (int e = threadIdx.x; e < R * R; e += kNT) {
+                const int i = e / R, j = e % R;
+                double s = 0.0;
+                for (int p = i; p <= j; ++p) s = fma(S.g[i * R + p], S.u[p * RM + j], s);
+                scratch[e] = i <= j ? s : 0.0;
+                a.r_out[e] = scratch[e];
+            }
+            __syncthreads();
+            if (!a.init && a.fitness) {
+                // ||K||^2 = sum_ij (R0^T R0)_ij l_i (Rn^T Rn)_ij l_j  (kruskal.hpp:457-462)
+                double s = 0.0;
+                for (int e = threadIdx.x; e < R * R; e += kNT) {
+                    const int i = e / R, j = e % R;
+                    double p0 = 0.0, pn = 0.0;
+                    const int top = i < j ? i : j;
+                    for (int p = 0; p <= top; ++p) {
+                        p0 = fma(a.r0[p * R + i], a.r0[p * R + j], p0);
+                        pn = fma(scratch[p * R + i], scratch[p * R + j], pn);
+                    }
+                    s += p0 * a.lambda[i] * pn * a.lambda[j];
+                }
+                const double kk = block_sum<kNT>(s, red);
+                if (threadIdx.x == 0) {
+                    const double raw = a.norm_x_sq - 2.0 * S.misc[1] + kk;
+                    const double rad = raw < 0.0 ? 0.0 : raw;
+                    a.fit_out[0] = 1.0 - sqrt(rad) / sqrt(a.norm_x_sq);
+                    a.fit_out[1] = raw;
+                }
+            }
+            // zero padding rows of the packed Q (k >= I)
+            const uint32_t Rp = ttm_rpad_dev(R);
+            const uint64_t Kpad = ((I + 31) / 32) * 32;
+            for (uint64_t e = I * Rp + threadIdx.x; e < Kpad * Rp; e += kNT) {
+                const uint64_t k = e / Rp, r = e % Rp;
+                a.qp_out[((k >> 2) * Rp + r) * 4 + (k & 3)] = 0.0;
+            }
+        }
+        CPDB_TS(12);
+    }
+    cl.sync();  // ---- 4: U2 (rank 0's g) published
+    CPDB_TS(13);
+    {
+        const double* g0 = cl.map_shared_rank(S.g, 0);
+        stage_tri<RM>(g0, R, R, S.u, S.dinv, kNT);
+        if (threadIdx.x == 0) flag = cl.map_shared_rank(S.misc, 0)[2] != 0.0;
+    }
+    __syncthreads();
+    if (!flag) {
+        // phase C: Q = A1 U2^-1 (+ packed copy [Kpad/4][Rp][4])
+        const uint32_t Rp = ttm_rpad_dev(R);
+        for (int li = grp; li < rows + (G - rows % G) % G; li += G) {
+            const bool act = li < rows;
+            Row x;
+            x.load(S.w + (act ? li : 0) * ld, act ? R : 0, q);
+            x.uinv(S.u, S.dinv, R, q);
+            if (act) {
+                const uint64_t i = r0 + li;
+                x.store(a.q_out + i * R, R, q);
+                double* qp = a.qp_out + ((i >> 2) * Rp) * 4 + (i & 3);
+#pragma unroll
+                for (int s = 0; s < Row::S; ++s) {
+                    const int k = s * T + q;
+                    if (k < int(Rp)) qp[k * 4] = k < R ? x.t[s] : 0.0;
+                }
+            }
+        }
+    } else if (rank == 0 && threadIdx.x == 0) {
+        *a.status = 2;
+    }
+    CPDB_TS(14);
+    cl.sync();  // rank 0's smem must outlive the other ranks' DSMEM reads
+    CPDB_TS(15);
+}
+
+// ---------------------------------------------------------------- Z-QR (small Z)
+template <int RM>
+__global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
+    using Row = LaneRow<RM>;
+    constexpr int T = Row::T, G = kNT / T;
+    constexpr int KC = (RM * RM + kNT - 1) / kNT;
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = int(cl.block_rank());
+    extern __shared__ double sm[];
+    const int R = a.R, nm = a.nm, ld = R + 1;
+    const int per = int((a.zrows + kCS - 1) / kCS);
+    const uint64_t r0 = uint64_t(per) * rank;
+    const int rows = int(r0 < a.zrows ? (a.zrows - r0 < uint64_t(per) ? a.zrows - r0
+                                                                      : uint64_t(per))
+                                      : 0);
+    Smem<RM> S(sm, R);
+    double* mats = S.w + per * ld;  // nm x R x R (after the R x R scratch)
+    mats += R * R;
+    const int grp = threadIdx.x / T, q = threadIdx.x % T;
+
+    for (int t = 0; t < nm; ++t)
+        for (int e = threadIdx.x; e < R * R; e += kNT) mats[t * R * R + e] = a.rmats[t][e];
+    __syncthreads();
+    // G1 = Hadamard_t (R_t^T R_t), computed redundantly by every rank (tiny)
+    for (int e = threadIdx.x; e < R * R; e += kNT) {
+        const int i = e / R, j = e % R;
+        const int lo = i < j ? i : j, hi = i < j ? j : i;
+        double h = 1.0;
+        for (int t = nm - 1; t >= 0; --t) {
+            const double* m = mats + t * R * R;
+            double s = 0.0;
+            for (int k = 0; k <= lo; ++k) s = fma(m[k * R + lo], m[k * R + hi], s);
+            h = (t == nm - 1) ? s : h * s;
+        }
+        S.g[e] = h;
+    }
+    __syncthreads();
+    const bool ok1 = block_chol<kNT, KC>(S.g, R, R);
+    if (!ok1 && rank == 0 && threadIdx.x == 0) *a.status = 2;
+    stage_tri<RM>(S.g, R, R, S.u, S.dinv, kNT);  // U1 (kept in S.g too)
+    __syncthreads();
+    // Q1 = Z U1^-1 on this rank's rows; Z rows are generated in registers
+    // (product in descending mode order like the reference Khatri-Rao fold)
+    for (int li = grp; li < rows + (G - rows % G) % G; li += G) {
+        const bool act = li < rows;
+        Row x;
+        uint64_t rem0 = r0 + (act ? li : 0);
+#pragma unroll
+        for (int s = 0; s < Row::S; ++s) {
+            const int c = s * T + q;
+            double z = 0.0;
+            if (c < R && act) {
+                uint64_t rem = rem0;
+                for (int k = nm - 1; k >= 0; --k) {
+                    const int dig = int(rem % R);
+                    rem /= R;
+                    const double v = mats[(k * R + dig) * R + c];
+                    z = (k == nm - 1) ? v : z * v;
+                }
+            }
+            x.t[s] = z;
+        }
+        x.uinv(S.u, S.dinv, R, q);
+        if (act) x.store(S.w + li * ld, R, q);
+    }
+    __syncthreads();
+    gram_dmma<kNT>(S.w, ld, rows, R, S.p, R);
+    cl.sync();
+    if (rank == 0) {
+        double* u1 = S.w + per * ld;  // keep U1 (stride R) for R0 = U2 U1
+        for (int e = threadIdx.x; e < R * R; e += kNT) u1[e] = S.g[e];
+        __syncthreads();
+        cluster_reduce(cl, S.p, R * R, S.g);
+        __syncthreads();
+        const bool ok2 = block_chol<kNT, KC>(S.g, R, R);
+        if (!ok2 && threadIdx.x == 0) *a.status = 2;
+        for (int e = threadIdx.x; e < R * R; e += kNT) {  // R0 = U2 U1
+            const int i = e / R, j = e % R;
+            double s = 0.0;
+            for (int k = i; k <= j; ++k) s = fma(S.g[i * R + k], u1[k * R + j], s);
+            a.r0[e] = i <= j ? s : 0.0;
+        }
+    }
+    cl.sync();
+    stage_tri<RM>(cl.map_shared_rank(S.g, 0), R, R, S.u, S.dinv, kNT);
+    __syncthreads();
+    for (int li = grp; li < rows + (G - rows % G) % G; li += G) {
+        const bool act = li < rows;
+        Row x;
+        x.load(S.w + (act ? li : 0) * ld, act ? R : 0, q);
+        x.uinv(S.u, S.dinv, R, q);
+        if (act) x.store(a.q0 + (r0 + li) * R, R, q);
+    }
+    cl.sync();
+}
+
+template <class Arg>
+cudaError_t launch_cluster(void (*kern)(Arg), size_t smem, cudaStream_t s, const Arg& arg) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         220 * 1024);
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t c{};
+    c.gridDim = dim3(kCS, 1, 1);
+    c.blockDim = dim3(kNT, 1, 1);
+    c.dynamicSmemBytes = smem;
+    c.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = kCS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    c.attrs = attr;
+    c.numAttrs = 1;
+    return cudaLaunchKernelEx(&c, kern, arg);
+}
+
+int rm_of(uint32_t R) { return R <= 8 ? 8 : R <= 16 ? 16 : R <= 32 ? 32 : 64; }
+
+template <int RM>
+size_t finish_smem_rm(uint64_t I, uint32_t R) {
+    return Smem<RM>::doubles(R, (I + kCS - 1) / kCS) * sizeof(double);
+}
+
+template <int RM>
+size_t zqr_smem_rm(uint64_t zrows, uint32_t R, uint32_t nm) {
+    return (Smem<RM>::doubles(R, (zrows + kCS - 1) / kCS) + size_t(nm) * R * R) * sizeof(double);
+}
+
+}  // namespace
+
+size_t finish_cluster_smem(uint64_t I, uint32_t R) {
+    switch (rm_of(R)) {
+        case 8: return finish_smem_rm<8>(I, R);
+        case 16: return finish_smem_rm<16>(I, R);
+        case 32: return finish_smem_rm<32>(I, R);
+        default: return finish_smem_rm<64>(I, R);
+    }
+}
+
+cudaError_t launch_finish_cluster(const FinishArgs& a, cudaStream_t s) {
+    if (a.R > 64) return cudaErrorInvalidValue;
+    const size_t smem = finish_cluster_smem(a.I, a.R);
+    if (smem > 220 * 1024) return cudaErrorInvalidValue;
+    switch (rm_of(a.R)) {
+        case 8: return launch_cluster<FinishArgs>(finish_cluster_kernel<8>, smem, s, a);
+        case 16: return launch_cluster<FinishArgs>(finish_cluster_kernel<16>, smem, s, a);
+        case 32: return launch_cluster<FinishArgs>(finish_cluster_kernel<32>, smem, s, a);
+        default: return launch_cluster<FinishArgs>(finish_cluster_kernel<64>, smem, s, a);
+    }
+}
+
+static size_t zqr_cluster_smem(uint64_t zrows, uint32_t R, uint32_t nm) {
+    switch (rm_of(R)) {
+        case 8: return zqr_smem_rm<8>(zrows, R, nm);
+        case 16: return zqr_smem_rm<16>(zrows, R, nm);
+        case 32: return zqr_smem_rm<32>(zrows, R, nm);
+        default: return zqr_smem_rm<64>(zrows, R, nm);
+    }
+}
+
+bool zqr_cluster_fits(uint64_t zrows, uint32_t R, uint32_t nm) {
+    return R <= 64 && zqr_cluster_smem(zrows, R, nm) <= 200 * 1024;
+}
+
+cudaError_t launch_zqr_cluster(const ZqrArgs& a, cudaStream_t s) {
+    const size_t smem = zqr_cluster_smem(a.zrows, a.R, a.nm);
+    switch (rm_of(a.R)) {
+        case 8: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<8>, smem, s, a);
+        case 16: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<16>, smem, s, a);
+        case 32: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<32>, smem, s, a);
+        default: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<64>, smem, s, a);
+    }
+}
+
+}  // namespace cpdb

@@ -88,8 +88,17 @@ struct FinishArgs {
     double norm_x_sq;
     double* fit_out;       // [fitness, raw]
     int* status;           // 1 singular R0 (+col<<8), 2 Cholesky breakdown
+    unsigned long long* ts;  // optional phase timestamps (profiling)
 };
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s);
+// variants (cluster.cu / finish.cu): launch_finish picks the cluster kernel
+// when its shared-memory plan fits, else the single-CTA one
+cudaError_t launch_finish_cluster(const FinishArgs& a, cudaStream_t s);
+cudaError_t launch_finish_single(const FinishArgs& a, cudaStream_t s);
+size_t finish_cluster_smem(uint64_t I, uint32_t R);
+bool zqr_cluster_fits(uint64_t zrows, uint32_t R, uint32_t nm);
+cudaError_t launch_zqr_cluster(const ZqrArgs& a, cudaStream_t s);
+cudaError_t launch_zqr_multi(const ZqrArgs& a, cudaStream_t s, int sms);
 // out[e] = sum_{p < nsplit} part[p*n + e]  (fixed order)
 cudaError_t reduce_splits(const double* part, uint32_t nsplit, uint64_t n, double* out,
                           cudaStream_t s);

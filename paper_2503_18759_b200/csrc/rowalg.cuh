@@ -1,0 +1,259 @@
+// Small dense building blocks for the mode-update kernels (R <= 64).
+//
+// The matrices are tiny (I <= a few hundred rows, R <= 64), so latency, not
+// FLOPs, bounds them.  Measured on B200 (tools/probes/, profiles/):
+// dependent LDS ~55 cycles, DFMA 8.6, __syncthreads ~29, shuffle ~25,
+// DDIV ~400 (!), rcp/rsqrt ~70.  Hence:
+//  * a row's triangular solve runs "right-looking" in REGISTERS, spread over
+//    T = RM/8 lanes (lane q owns columns k = 8*i + ... with k % T == q): once
+//    x_j is final its owner broadcasts it with one shuffle and every lane
+//    updates its own partial sums -- the critical path is R x (mul + shfl +
+//    fma) and every lane holds exactly 8 columns;
+//  * Grams W^T W run on the FP64 tensor cores (mma.m8n8k4 -> DMMA);
+//  * no IEEE division inside loops (reciprocals are precomputed).
+#pragma once
+
+#include "device.cuh"
+
+namespace cpdb {
+
+template <int NT>
+__device__ double block_sum(double v, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    v = warp_sum(v);
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (warp == 0) {
+        s = lane < NT / 32 ? red[lane] : 0.0;
+        s = warp_sum(s);
+    }
+    return s;  // valid in warp 0
+}
+
+// ---------------------------------------------------------------- lane rows
+// A row of length <= RM distributed over T = RM/8 lanes: lane q holds
+// x[8*i... ] as t[s] = x[s*T + q], s < 8.
+template <int RM>
+struct LaneRow {
+    static constexpr int T = RM / 8 > 0 ? RM / 8 : 1;
+    static constexpr int S = RM / T;  // slots per lane (8)
+    double t[S];
+
+    __device__ __forceinline__ void load(const double* src, int R, int q) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int k = s * T + q;
+            t[s] = k < R ? src[k] : 0.0;
+        }
+    }
+    __device__ __forceinline__ void store(double* dst, int R, int q) const {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int k = s * T + q;
+            if (k < R) dst[k] = t[s];
+        }
+    }
+    // x <- x U^-1, U upper with stride RM (zero padded, unit diagonal beyond
+    // R), dinv[j] = 1/U[j][j]: right-looking forward substitution.
+    __device__ __forceinline__ void uinv(const double* U, const double* dinv, int R, int q) {
+#pragma unroll
+        for (int j = 0; j < RM; ++j) {
+            if (j < R) {
+                constexpr int dummy = 0;
+                (void)dummy;
+                const int owner = j % T, slot = j / T;
+                double xj = t[slot] * dinv[j];
+                xj = __shfl_sync(0xffffffffu, xj, owner, T);
+                if (q == owner) t[slot] = xj;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    if (s * T + T - 1 > j) {  // compile-time: slot may hold a k > j
+                        const int k = s * T + q;
+                        if (k > j) t[s] = fma(-xj, U[j * RM + k], t[s]);
+                    }
+                }
+            }
+        }
+    }
+    // x <- x U^-T (solve x U^T = v; lower L = U^T), right-looking backward:
+    // x_c = t_c / U[c][c], then t_k -= x_c U[k][c] for k < c -- the
+    // row-wise triangular solve of linalg.hpp:192-216 with L = R0^T.
+    // Ut is U TRANSPOSED (stride RM), so a lane group reads consecutive words.
+    __device__ __forceinline__ void utinv(const double* Ut, const double* dinv, int R, int q) {
+#pragma unroll
+        for (int c = RM - 1; c >= 0; --c) {
+            if (c < R) {
+                const int owner = c % T, slot = c / T;
+                double xc = t[slot] * dinv[c];
+                xc = __shfl_sync(0xffffffffu, xc, owner, T);
+                if (q == owner) t[slot] = xc;
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    if (s * T < c) {  // compile-time: slot may hold a k < c
+                        const int k = s * T + q;
+                        if (k < c) t[s] = fma(-xc, Ut[c * RM + k], t[s]);
+                    }
+                }
+            }
+        }
+    }
+    // this <- v U for upper U (stride RM): t[k] = sum_{j<=k} v[j] U[j][k]
+    __device__ __forceinline__ void set_times_upper(const LaneRow& v, const double* U, int R,
+                                                    int q) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) t[s] = 0.0;
+#pragma unroll
+        for (int j = 0; j < RM; ++j) {
+            if (j < R) {
+                const double vj = __shfl_sync(0xffffffffu, v.t[j / T], j % T, T);
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    if (s * T + T - 1 >= j) {
+                        const int k = s * T + q;
+                        if (k >= j) t[s] = fma(vj, U[j * RM + k], t[s]);
+                    }
+                }
+            }
+        }
+    }
+    // sum over lanes of the group
+    __device__ __forceinline__ static double group_sum(double v) {
+#pragma unroll
+        for (int o = 1; o < T; o <<= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        return v;
+    }
+};
+
+// Triangular factor staged in smem with the compile-time stride RM:
+// entries beyond R are 0 off the diagonal and 1 on it.
+template <int RM>
+__device__ void stage_tri(const double* src, int ld_src, int R, double* dst, double* dinv,
+                          int nthreads) {
+    for (int e = threadIdx.x; e < RM * RM; e += nthreads) {
+        const int i = e / RM, j = e % RM;
+        dst[e] = (i < R && j < R) ? src[i * ld_src + j] : (i == j ? 1.0 : 0.0);
+    }
+    for (int j = threadIdx.x; j < RM; j += nthreads)
+        dinv[j] = j < R ? __drcp_rn(src[j * ld_src + j]) : 1.0;
+}
+
+// Same, transposed: dst[j][i] = src[i][j] (for LaneRow::utinv).
+template <int RM>
+__device__ void stage_tri_t(const double* src, int ld_src, int R, double* dst, double* dinv,
+                            int nthreads) {
+    for (int e = threadIdx.x; e < RM * RM; e += nthreads) {
+        const int i = e / RM, j = e % RM;
+        dst[j * RM + i] = (i < R && j < R) ? src[i * ld_src + j] : (i == j ? 1.0 : 0.0);
+    }
+    for (int j = threadIdx.x; j < RM; j += nthreads)
+        dinv[j] = j < R ? __drcp_rn(src[j * ld_src + j]) : 1.0;
+}
+
+// ---------------------------------------------------------------- Gram on DMMA
+// G[p][q] (full R x R, stride ldg) = sum_i W[i][p] W[i][q] over `rows` rows
+// of W (stride ld), FP64 tensor cores: one warp per 8x8 output tile, k = 4
+// rows per DMMA; fixed order -> deterministic.
+template <int NT>
+__device__ void gram_dmma(const double* w, int ld, int rows, int R, double* g, int ldg,
+                          bool accumulate = false) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int nt = (R + 7) / 8;
+    const int m = lane >> 2, kq = lane & 3;
+    for (int tix = warp; tix < nt * nt; tix += NT / 32) {
+        const int ti = tix / nt, tj = tix % nt;
+        if (tj < ti) continue;
+        const int pa = ti * 8 + m, pb = tj * 8 + m;
+        double c0 = 0.0, c1 = 0.0, d0 = 0.0, d1 = 0.0;
+        int k0 = 0;
+        for (; k0 + 4 < rows; k0 += 8) {
+            const int i0 = k0 + kq, i1 = k0 + 4 + kq;
+            const double a0 = (pa < R) ? w[i0 * ld + pa] : 0.0;
+            const double b0 = (pb < R) ? w[i0 * ld + pb] : 0.0;
+            const double a1 = (pa < R && i1 < rows) ? w[i1 * ld + pa] : 0.0;
+            const double b1 = (pb < R && i1 < rows) ? w[i1 * ld + pb] : 0.0;
+            dmma(c0, c1, a0, b0);
+            dmma(d0, d1, a1, b1);
+        }
+        for (; k0 < rows; k0 += 4) {
+            const int i0 = k0 + kq;
+            const double a0 = (pa < R && i0 < rows) ? w[i0 * ld + pa] : 0.0;
+            const double b0 = (pb < R && i0 < rows) ? w[i0 * ld + pb] : 0.0;
+            dmma(c0, c1, a0, b0);
+        }
+        c0 += d0;
+        c1 += d1;
+        // C[m][2*kq + {0,1}] of the tile; the mirrored copy of a diagonal
+        // tile is written by the lane that owns it, so each entry has one writer
+        const int r = ti * 8 + m, cc = tj * 8 + 2 * kq;
+        if (r < R) {
+            if (cc < R) {
+                const double v = accumulate ? g[r * ldg + cc] + c0 : c0;
+                g[r * ldg + cc] = v;
+                if (ti != tj) g[cc * ldg + r] = v;
+            }
+            if (cc + 1 < R) {
+                const double v = accumulate ? g[r * ldg + cc + 1] + c1 : c1;
+                g[r * ldg + cc + 1] = v;
+                if (ti != tj) g[(cc + 1) * ldg + r] = v;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- Cholesky
+// Right-looking Cholesky of the symmetric R x R matrix g (stride ld) by the
+// whole block, one barrier per step: G[a][b] -= G[j][a] G[j][b] / G[j][j]
+// for j < a <= b (row j is final once step j starts); then
+// U[j][i] = G[j][i] / sqrt(G[j][j]).  In place (strict lower zeroed).
+// Each thread owns fixed entries (precomputed, no per-step index math) and
+// issues all loads of a step before its stores.  Returns false
+// (block-uniform) on a non-positive pivot.
+template <int NT, int KMAX>
+__device__ bool block_chol(double* g, int ld, int R) {
+    int pa[KMAX], pb[KMAX];
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+        const int e = threadIdx.x + k * NT;
+        const bool own = e < R * R && (e % R) >= (e / R);
+        pa[k] = own ? e / R : 1 << 20;
+        pb[k] = own ? e % R : 0;
+    }
+    bool ok = true;
+    for (int j = 0; j < R; ++j) {
+        const double d = g[j * ld + j];
+        if (!(d > 0.0)) {
+            ok = false;  // uniform: every thread read the same d
+            break;
+        }
+        const double inv = __drcp_rn(d);
+        double ga[KMAX], gb[KMAX], gab[KMAX];
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            const bool act = pa[k] > j && pa[k] < R;
+            ga[k] = act ? g[j * ld + pa[k]] : 0.0;
+            gb[k] = act ? g[j * ld + pb[k]] : 0.0;
+            gab[k] = act ? g[pa[k] * ld + pb[k]] : 0.0;
+        }
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k)
+            if (pa[k] > j && pa[k] < R) g[pa[k] * ld + pb[k]] = fma(-ga[k] * inv, gb[k], gab[k]);
+        __syncthreads();
+    }
+    if (!ok) {
+        __syncthreads();
+        return false;
+    }
+    __shared__ double rs[64];
+    for (int j = threadIdx.x; j < R; j += NT) rs[j] = rsqrt(g[j * ld + j]);
+    __syncthreads();
+    for (int e = threadIdx.x; e < R * R; e += NT) {
+        const int i = e / R, k = e % R;
+        g[i * ld + k] = k >= i ? g[i * ld + k] * rs[i] : 0.0;
+    }
+    __syncthreads();
+    return true;
+}
+
+}  // namespace cpdb

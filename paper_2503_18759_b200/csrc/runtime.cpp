@@ -138,4 +138,5 @@ cpdb_ctx::~cpdb_ctx() {
     if (dstatus) cudaFree(dstatus);
     if (pinned) cudaFreeHost(pinned);
     if (stream) cudaStreamDestroy(stream);
+    if (side) cudaStreamDestroy(side);
 }

@@ -70,6 +70,7 @@ struct cpdb_ctx {
     int device = 0;
     int sms = 148;
     cudaStream_t stream = nullptr;
+    cudaStream_t side = nullptr;  // Z-QR overlapped with the TTM chain
 
     // sharding: leading mode split in contiguous slabs
     int rank = 0, world = 1;

@@ -16,6 +16,8 @@
 // and the host synchronises once per sweep to read the fitness scalar.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "comm.hpp"
@@ -64,7 +66,10 @@ EventPool::~EventPool() {
 
 Session::~Session() {
     if (c && c->stream) cudaStreamSynchronize(c->stream);
+    if (c && c->side) cudaStreamSynchronize(c->side);
     if (t_start) cudaEventDestroy(t_start);
+    if (ev_ready) cudaEventDestroy(ev_ready);
+    if (ev_zqr) cudaEventDestroy(ev_zqr);
 }
 
 // ---------------------------------------------------------------- setup
@@ -116,6 +121,8 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     }
     c->prof = cpdb_profile{};
     launches0 = c->launches;
+    CPDB_CK(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
+    CPDB_CK(cudaEventCreateWithFlags(&ev_zqr, cudaEventDisableTiming));
 
     // ---- factor state (factor_state.hpp:28-34) -----------------------------
     fb.resize(order);
@@ -333,13 +340,18 @@ void Session::mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer,
     z.r0 = r0buf.p;
     z.work = zwork.p;
     z.status = c->dstatus;
-    CPDB_CK(launch_zqr(z, s, c->sms));
-    c->launches += 4;
+    // Z-QR depends only on R_k (k != n), final since the previous update's
+    // finisher: it runs on the side stream, overlapped with the TTM chain.
+    CPDB_CK(cudaEventRecord(ev_ready, s));
+    CPDB_CK(cudaStreamWaitEvent(c->side, ev_ready, 0));
+    CPDB_CK(launch_zqr(z, c->side, c->sms));
+    CPDB_CK(cudaEventRecord(ev_zqr, c->side));
+    c->launches += 5;
     if (observer) {
         std::vector<double> nat(zrows * R), ref(zrows * R);
         CPDB_CK(cudaMemcpyAsync(nat.data(), q0buf.p, zrows * R * sizeof(double),
-                                cudaMemcpyDeviceToHost, s));
-        CPDB_CK(cudaStreamSynchronize(s));
+                                cudaMemcpyDeviceToHost, c->side));
+        CPDB_CK(cudaStreamSynchronize(c->side));
         for (uint64_t i = 0; i < zrows; ++i)
             std::memcpy(&ref[perm[i] * R], &nat[i * R], R * sizeof(double));
         observer(user, sweep, n, ref.data(), zrows, R);
@@ -415,30 +427,26 @@ void Session::mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer,
     const size_t part = size_t(vgemm_max_split()) * v.I * R;
     v.vpart = vpart.ensure(part);
     v.vfitpart = v.dual ? vfitpart.ensure(part) : nullptr;
+    CPDB_CK(cudaStreamWaitEvent(s, ev_zqr, 0));
     CPDB_CK(launch_vgemm(v, s, c->sms));
     c->launches += 1;
-    const double* vsrc = v.vpart;
-    const double* vfsrc = v.vfitpart;
-    uint32_t nsplit = v.nsplit;
-    if (sharded && n == 0) {
-        // this rank's rows of V -> the full V on every rank
-        CPDB_CK(reduce_splits(v.vpart, nsplit, v.I * R, vfull.p + c->row_begin * R, s));
+    // split-K partials -> V (this rank's rows; sharded mode-0 updates gather
+    // the full V on every rank)
+    const bool gather = sharded && n == 0;
+    const uint64_t off = gather ? c->row_begin * R : 0;
+    CPDB_CK(reduce_splits(v.vpart, v.nsplit, v.I * R, vfull.p + off, s));
+    if (v.dual) CPDB_CK(reduce_splits(v.vfitpart, v.nsplit, v.I * R, vfitfull.p + off, s));
+    c->launches += v.dual ? 2 : 1;
+    if (gather) {
         allgather(c, vfull.p, v.I * R);
-        vsrc = vfull.p;
-        if (v.dual) {
-            CPDB_CK(reduce_splits(v.vfitpart, nsplit, v.I * R, vfitfull.p + c->row_begin * R, s));
-            allgather(c, vfitfull.p, v.I * R);
-            vfsrc = vfitfull.p;
-        }
-        c->launches += v.dual ? 2 : 1;
-        nsplit = 1;
+        if (v.dual) allgather(c, vfitfull.p, v.I * R);
     }
     // 6-9. A_hat, lambda, factor QR, fitness (solvers.hpp:272-292)
     FinishArgs f{};
     f.init = 0;
-    f.vpart = vsrc;
-    f.vfitpart = vfsrc;
-    f.nsplit = nsplit;
+    f.vpart = vfull.p;
+    f.vfitpart = v.dual ? vfitfull.p : nullptr;
+    f.nsplit = 1;
     f.dual = v.dual;
     f.r0 = r0buf.p;
     f.I = c->dims[n];
@@ -454,8 +462,22 @@ void Session::mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer,
     f.norm_x_sq = nx2;
     f.fit_out = fitbuf.p;
     f.status = c->dstatus;
+    static const bool trace_phases = std::getenv("CPDB_PHASE_TRACE") != nullptr;
+    if (trace_phases) {
+        f.ts = reinterpret_cast<unsigned long long*>(tsbuf.ensure(32));
+        CPDB_CK(cudaMemsetAsync(f.ts, 0, 32 * sizeof(double), s));
+    }
     CPDB_CK(launch_finish(f, s));
     c->launches += 1;
+    if (trace_phases) {
+        unsigned long long ts[32];
+        CPDB_CK(cudaMemcpyAsync(ts, f.ts, sizeof ts, cudaMemcpyDeviceToHost, s));
+        CPDB_CK(cudaStreamSynchronize(s));
+        std::fprintf(stderr, "finish mode %u phases(us):", n);
+        for (int k = 1; k < 19; ++k)
+            std::fprintf(stderr, " %d:%.2f", k, ts[k] ? (ts[k] - ts[0]) * 1e-3 : -1.0);
+        std::fprintf(stderr, "\n");
+    }
     if (n == 0) pack_local0();
     ++versions[n];
     if (extrap) {

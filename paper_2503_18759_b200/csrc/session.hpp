@@ -33,7 +33,7 @@ struct Session {
     uint64_t launches0 = 0;
 
     std::vector<FactorBufs> fb;
-    DevBuf lam, qp0_local;
+    DevBuf lam, qp0_local, tsbuf;
     DevBuf fscratch, vpart, vfitpart, vfull, vfitfull, vout, fitbuf, q0buf, q1buf, r0buf, zwork;
     std::vector<DevBuf> hist, ybuf;
     std::vector<bool> has_hist;
@@ -48,6 +48,7 @@ struct Session {
     EventPool events;
     std::vector<Timer> timers;
     cudaEvent_t t_start = nullptr;
+    cudaEvent_t ev_ready = nullptr, ev_zqr = nullptr;  // main -> side -> main fork/join
 
     ~Session();
     void begin(cpdb_ctx* ctx, const cpdb_config& cfg, const cpdb_state* state);
