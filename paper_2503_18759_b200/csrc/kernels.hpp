@@ -18,6 +18,9 @@ struct TtmArgs {
 enum class TtmPath { groups, rows, simple };
 TtmPath ttm_path(const TtmArgs& a);
 cudaError_t launch_ttm(const TtmArgs& a, cudaStream_t s, int sms);
+// warp-specialised TMA/DMMA kernel (ttm_tma.cu); cudaErrorNotSupported when
+// the shape needs the cp.async kernel of ttm.cu
+cudaError_t launch_ttm_tma(const TtmArgs& a, cudaStream_t s, int sms);
 uint32_t ttm_kpad(uint64_t K);
 uint32_t ttm_rpad(uint32_t R);
 cudaError_t pack_q(const double* q, double* qp, uint32_t K, uint32_t R, cudaStream_t s);

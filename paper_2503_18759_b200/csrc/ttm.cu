@@ -21,6 +21,7 @@
 // one-thread-per-output kernel.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "device.cuh"
 #include "kernels.hpp"
@@ -282,6 +283,14 @@ TtmPath ttm_path(const TtmArgs& a) {
 }
 
 cudaError_t launch_ttm(const TtmArgs& a, cudaStream_t s, int sms) {
+    static const int version = [] {
+        const char* v = std::getenv("CPDB_TTM");
+        return v ? std::atoi(v) : 2;
+    }();
+    if (version >= 2 && a.qp != nullptr) {
+        const cudaError_t e = launch_ttm_tma(a, s, sms);  // warp-specialised TMA path
+        if (e != cudaErrorNotSupported) return e;
+    }
     switch (ttm_path(a)) {
         case TtmPath::groups: return dispatch<kGroups>(a, s, sms);
         case TtmPath::rows: return dispatch<kRows>(a, s, sms);

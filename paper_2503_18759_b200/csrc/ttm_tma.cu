@@ -1,0 +1,345 @@
+// K1/K2 v2: warp-specialised TMA -> DMMA tensor-times-matrix (sm_100a).
+//
+// Same contraction as ttm.cu (cpd::ttm, tensor.hpp:288-315, with B = Q_c^T):
+//     Y[o][r][j] = sum_k X[o][k][j] Q[k][r]
+// One producer warp streams X through a STAGES-deep shared-memory ring with
+// the Tensor Memory Accelerator (one cp.async.bulk.tensor per stage, OOB rows
+// zero-filled -- that is the K and tail padding) plus a 1-D bulk copy of the
+// matching packed-Q chunk; NC consumer warps wait on the stage's mbarrier,
+// issue mma.sync.m8n8k4.f64 (DMMA) from the staged tiles with register double
+// buffering of the fragments, and release the stage with an mbarrier arrive.
+// No __syncthreads in the main loop; one persistent CTA per SM.
+//
+// Staging layouts (chosen so every fragment load is 256 contiguous bytes):
+//   kGroups (inner % 8 == 0): tensor map over X as 4-D {8 j_lo, K, inner/8, outer};
+//            smem stage = [G groups][BK][8]  (G = BJ/8; a box may cover several
+//            o when inner/8 < G)
+//   kRows   (inner == 1, K % 4 == 0): X as 3-D {4 k_lo, M, K/4}; smem stage =
+//            [BK/4][BM][4]
+#include <cuda.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+#include "device.cuh"
+#include "kernels.hpp"
+
+namespace cpdb {
+namespace {
+
+enum Layout { kGroups = 0, kRows = 1 };
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+    asm volatile(
+        "{\n\t"
+        ".reg .pred P1;\n\t"
+        "WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+        "@!P1 bra WAIT_%=;\n\t"
+        "}\n" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                       int c1, int c2, int c3) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+        : "memory");
+}
+__device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
+                                       int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes,
+                                          uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+template <int RB, int CB, int BK, int STAGES, int NC, int LAYOUT>
+struct Cfg {
+    static constexpr int Rp = RB * 8;
+    static constexpr int BJ = NC * CB * 8;   // tile columns (kGroups) / rows (kRows)
+    static constexpr int G = BJ / 8;
+    static constexpr int XS = BK * BJ;       // doubles per X stage
+    static constexpr int QS = BK * Rp;       // doubles per Q stage
+    static constexpr int STAGE = XS + QS;
+    static constexpr int NT = (NC + 1) * 32;
+    static constexpr size_t SMEM = size_t(STAGES) * STAGE * sizeof(double) + 2 * STAGES * 8 + 128;
+};
+
+template <int RB, int CB, int BK, int STAGES, int NC, int LAYOUT>
+__global__ void __launch_bounds__(Cfg<RB, CB, BK, STAGES, NC, LAYOUT>::NT, 1)
+ttm_tma_kernel(const __grid_constant__ CUtensorMap xmap, double* __restrict__ y,
+               const double* __restrict__ qp, uint64_t outer, uint64_t K, uint64_t inner,
+               uint32_t R, uint64_t ntiles, uint32_t nk) {
+    using C = Cfg<RB, CB, BK, STAGES, NC, LAYOUT>;
+    extern __shared__ __align__(128) double smem[];
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
+    uint64_t* empty = full + STAGES;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], NC);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+
+    const uint64_t first = blockIdx.x;
+    const uint64_t my_tiles = first < ntiles ? (ntiles - 1 - first) / gridDim.x + 1 : 0;
+    const uint64_t total = my_tiles * nk;
+    const uint64_t gpo = inner / 8;  // 8-column groups per o (kGroups)
+
+    if (warp == NC) {
+        // ===================== producer: one elected lane issues TMA
+        if (lane == 0) {
+            for (uint64_t t = 0; t < total; ++t) {
+                const int st = int(t % STAGES);
+                const uint32_t ph = uint32_t((t / STAGES) & 1);
+                mbar_wait(&empty[st], ph ^ 1);
+                const uint64_t tile = first + (t / nk) * gridDim.x;
+                const int k0 = int((t % nk) * BK);
+                double* sx = smem + st * C::STAGE;
+                double* sq = sx + C::XS;
+                mbar_expect_tx(&full[st], uint32_t(C::STAGE * sizeof(double)));
+                if (LAYOUT == kGroups) {
+                    const uint64_t g0 = tile * C::G;  // first flat 8-group of the tile
+                    if (gpo >= uint64_t(C::G)) {
+                        tma_4d(sx, &xmap, &full[st], 0, k0, int(g0 % gpo), int(g0 / gpo));
+                    } else {
+                        tma_4d(sx, &xmap, &full[st], 0, k0, 0, int(g0 / gpo));
+                    }
+                } else if constexpr (C::BJ <= 256) {
+                    tma_3d(sx, &xmap, &full[st], 0, int(tile * C::BJ), k0 / 4);
+                } else {
+                    // box rows are capped at 256: one box per (k-quad, 256 rows)
+#pragma unroll
+                    for (int s = 0; s < BK / 4; ++s)
+#pragma unroll
+                        for (int h = 0; h < C::BJ / 256; ++h)
+                            tma_3d(sx + (s * C::BJ + h * 256) * 4, &xmap, &full[st], 0,
+                                   int(tile * C::BJ + h * 256), k0 / 4 + s);
+                }
+                bulk_copy(sq, qp + size_t(k0) * C::Rp, uint32_t(C::QS * sizeof(double)), &full[st]);
+            }
+        }
+        return;
+    }
+
+    // ===================== consumers
+    double acc[RB][CB][2];
+#pragma unroll
+    for (int a = 0; a < RB; ++a)
+#pragma unroll
+        for (int b = 0; b < CB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
+
+    for (uint64_t t = 0; t < total; ++t) {
+        const int st = int(t % STAGES);
+        mbar_wait(&full[st], uint32_t((t / STAGES) & 1));
+        const double* sx = smem + st * C::STAGE;
+        const double* sq = sx + C::XS;
+        double qf[2][RB], xf[2][CB];
+        auto load_frags = [&](int s, int buf) {
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb) qf[buf][rb] = sq[(s * C::Rp + rb * 8) * 4 + lane];
+#pragma unroll
+            for (int cb = 0; cb < CB; ++cb) {
+                const int g = warp * CB + cb;
+                if (LAYOUT == kGroups)
+                    xf[buf][cb] = sx[(g * BK + 4 * s + (lane & 3)) * 8 + (lane >> 2)];
+                else
+                    xf[buf][cb] = sx[(s * C::BJ + g * 8) * 4 + lane];
+            }
+        };
+        load_frags(0, 0);
+#pragma unroll
+        for (int s = 0; s < BK / 4; ++s) {
+            const int cur = s & 1;
+            if (s + 1 < BK / 4) load_frags(s + 1, cur ^ 1);
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+                for (int cb = 0; cb < CB; ++cb) {
+                    if (LAYOUT == kGroups)
+                        dmma(acc[rb][cb][0], acc[rb][cb][1], qf[cur][rb], xf[cur][cb]);
+                    else
+                        dmma(acc[rb][cb][0], acc[rb][cb][1], xf[cur][cb], qf[cur][rb]);
+                }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[st]);
+
+        if (t % nk == nk - 1) {  // tile complete: epilogue straight to HBM
+            const uint64_t tile = first + (t / nk) * gridDim.x;
+#pragma unroll
+            for (int cb = 0; cb < CB; ++cb) {
+                const int g = warp * CB + cb;
+                if (LAYOUT == kGroups) {
+                    const uint64_t gflat = tile * C::G + g;
+                    const uint64_t o = gflat / gpo, j = (gflat % gpo) * 8 + 2 * (lane & 3);
+                    if (o < outer) {
+#pragma unroll
+                        for (int rb = 0; rb < RB; ++rb) {
+                            const uint32_t r = rb * 8 + (lane >> 2);
+                            if (r < R)
+                                *reinterpret_cast<double2*>(y + (o * R + r) * inner + j) =
+                                    make_double2(acc[rb][cb][0], acc[rb][cb][1]);
+                        }
+                    }
+                } else {
+                    const uint64_t m = tile * C::BJ + uint64_t(g) * 8 + (lane >> 2);
+                    if (m < outer) {
+#pragma unroll
+                        for (int rb = 0; rb < RB; ++rb) {
+                            const uint32_t r = rb * 8 + 2 * (lane & 3);
+                            double* dst = y + m * R + r;
+                            if (r + 1 < R && (R % 2 == 0)) {
+                                *reinterpret_cast<double2*>(dst) =
+                                    make_double2(acc[rb][cb][0], acc[rb][cb][1]);
+                            } else {
+                                if (r < R) dst[0] = acc[rb][cb][0];
+                                if (r + 1 < R) dst[1] = acc[rb][cb][1];
+                            }
+                        }
+                    }
+                }
+#pragma unroll
+                for (int rb = 0; rb < RB; ++rb) acc[rb][cb][0] = acc[rb][cb][1] = 0.0;
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------- tensor maps
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                              const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                              const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                              CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeFn encode_fn() {
+    static EncodeFn fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeFn>(p);
+    });
+    return fn;
+}
+
+template <int RB, int CB, int BK, int STAGES, int NC, int LAYOUT>
+cudaError_t launch_v2(const TtmArgs& a, cudaStream_t s, int sms) {
+    using C = Cfg<RB, CB, BK, STAGES, NC, LAYOUT>;
+    EncodeFn enc = encode_fn();
+    if (!enc) return cudaErrorNotSupported;
+    CUtensorMap map;
+    CUresult r;
+    if (LAYOUT == kGroups) {
+        const uint64_t gpo = a.inner / 8;
+        const cuuint64_t dims[4] = {8, a.K, gpo, a.outer};
+        const cuuint64_t strides[3] = {a.inner * 8, 64, a.K * a.inner * 8};
+        cuuint32_t box[4];
+        if (gpo >= uint64_t(C::G)) {
+            if (gpo % C::G != 0) return cudaErrorNotSupported;  // a tile would straddle two o
+            box[0] = 8; box[1] = BK; box[2] = C::G; box[3] = 1;
+        } else {
+            if (C::G % gpo != 0) return cudaErrorNotSupported;
+            box[0] = 8; box[1] = BK; box[2] = cuuint32_t(gpo); box[3] = cuuint32_t(C::G / gpo);
+        }
+        const cuuint32_t estr[4] = {1, 1, 1, 1};
+        r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(a.x), dims, strides,
+                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    } else {
+        const cuuint64_t dims[3] = {4, a.outer, a.K / 4};
+        const cuuint64_t strides[2] = {a.K * 8, 32};
+        const cuuint32_t box[3] = {4, cuuint32_t(C::BJ <= 256 ? C::BJ : 256),
+                                   cuuint32_t(C::BJ <= 256 ? BK / 4 : 1)};
+        const cuuint32_t estr[3] = {1, 1, 1};
+        r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(a.x), dims, strides,
+                box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    }
+    if (r != CUDA_SUCCESS) {
+        static bool warned = false;
+        if (!warned && std::getenv("CPDB_DEBUG")) {
+            std::fprintf(stderr, "cpdb: tensor map encode failed (%d) layout %d outer %llu K %llu "
+                         "inner %llu; using the cp.async kernel\n", int(r), LAYOUT,
+                         (unsigned long long)a.outer, (unsigned long long)a.K,
+                         (unsigned long long)a.inner);
+            warned = true;
+        }
+        return cudaErrorNotSupported;
+    }
+    auto kern = ttm_tma_kernel<RB, CB, BK, STAGES, NC, LAYOUT>;
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(C::SMEM));
+    if (e != cudaSuccess) return e;
+    const uint64_t ncols = LAYOUT == kGroups ? (a.outer * a.inner) / 8 : a.outer;  // groups or rows
+    const uint64_t per_tile = LAYOUT == kGroups ? C::G : C::BJ;
+    const uint64_t ntiles = (ncols + per_tile - 1) / per_tile;
+    const uint32_t nk = static_cast<uint32_t>((a.K + BK - 1) / BK);
+    const uint64_t grid = std::min<uint64_t>(ntiles, uint64_t(sms));
+    if (grid == 0) return cudaSuccess;
+    kern<<<unsigned(grid), C::NT, C::SMEM, s>>>(map, a.y, a.qp, a.outer, a.K, a.inner, a.R, ntiles,
+                                               nk);
+    return cudaGetLastError();
+}
+
+template <int LAYOUT>
+cudaError_t dispatch_v2(const TtmArgs& a, cudaStream_t s, int sms) {
+    // X stage ~32 KB; Q stage small; 5 stages in flight
+    switch (a.Rp / 8) {
+        case 1: return launch_v2<1, 8, 8, 5, 8, LAYOUT>(a, s, sms);
+        case 2: return launch_v2<2, 8, 8, 5, 8, LAYOUT>(a, s, sms);
+        case 3: return launch_v2<3, 4, 16, 5, 8, LAYOUT>(a, s, sms);
+        case 4: return launch_v2<4, 4, 16, 5, 8, LAYOUT>(a, s, sms);
+        case 5: return launch_v2<5, 2, 32, 4, 8, LAYOUT>(a, s, sms);
+        case 6: return launch_v2<6, 2, 32, 4, 8, LAYOUT>(a, s, sms);
+        case 7: return launch_v2<7, 2, 32, 4, 8, LAYOUT>(a, s, sms);
+        case 8: return launch_v2<8, 2, 32, 4, 8, LAYOUT>(a, s, sms);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace
+
+// Returns cudaErrorNotSupported when the shape cannot use the TMA path (the
+// caller falls back to the cp.async kernel).
+cudaError_t launch_ttm_tma(const TtmArgs& a, cudaStream_t s, int sms) {
+    if (a.Rp > 64 || a.R == 0) return cudaErrorNotSupported;
+    if (a.inner % 8 == 0 && a.K < (1u << 31) && a.outer < (1u << 31) && a.inner / 8 < (1u << 31))
+        return dispatch_v2<kGroups>(a, s, sms);
+    if (a.inner == 1 && a.K % 4 == 0 && a.outer < (1u << 31)) return dispatch_v2<kRows>(a, s, sms);
+    return cudaErrorNotSupported;
+}
+
+}  // namespace cpdb
