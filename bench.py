@@ -69,34 +69,46 @@ def workload_name(cfg_name, c):
 
 
 class ClockSampler:
-    """nvidia-smi clocks/throttle reasons during the timed region (recipe's clocks line)."""
+    """nvidia-smi clocks/throttle reasons around the timed region (the recipe's
+    clocks line).  nvidia-smi is started BEFORE the warm-up (its start-up takes
+    driver locks that would stall the timed sweeps) and `mark()`/`stop()`
+    bracket the timed window; samples stamped inside it are summarised (the
+    nearest ones when the window is shorter than the sampling period)."""
 
     FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
 
-    def __init__(self, device):
-        self.device, self.lines, self.proc = device, [], None
+    def __init__(self, device, period_ms=20):
+        self.device, self.period, self.lines, self.proc = device, period_ms, [], None
+        self.t0 = self.t1 = None
 
-    def __enter__(self):
+    def start(self):
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", str(self.period)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            deadline = time.perf_counter() + 10.0
+            while not self.lines and time.perf_counter() < deadline:
+                time.sleep(0.02)
         except Exception:
             self.proc = None
         return self
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
-    def __exit__(self, *exc):
+    def mark(self):
+        self.t0 = time.perf_counter()
+
+    def stop(self):
+        self.t1 = time.perf_counter()
         if self.proc:
-            time.sleep(0.25)
+            time.sleep(max(0.05, 2 * self.period / 1e3))
             self.proc.terminate()
             try:
                 self.proc.wait(2)
@@ -106,7 +118,12 @@ class ClockSampler:
     def summary(self):
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.lines:
+        t0, t1 = self.t0 or 0.0, self.t1 or float("inf")
+        inside = [l for t, l in self.lines if t0 <= t <= t1 + self.period / 1e3]
+        if not inside and self.lines:  # window shorter than the period: nearest samples
+            after = [l for t, l in self.lines if t >= t0]
+            inside = after[:2] if after else [self.lines[-1][1]]
+        for line in inside:
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 7:
                 continue
@@ -200,7 +217,7 @@ def run_reference(args, c, rank, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -234,12 +251,14 @@ def main():
     cfg = cpd.SolverConfig(rank=c["rank"], max_iterations=W + K, seed=INIT_SEED)
 
     # ---- device-timed K sweeps after W warm-up sweeps ---------------------------
+    clocks = ClockSampler(local).start()
     sess = ctx.session(cfg, extrapolate=True)
     warm = sess.run(W)
     p0 = ctx.profile()
     barrier(world)
-    with ClockSampler(local) as clocks:
-        rows = sess.run(K)
+    clocks.mark()
+    rows = sess.run(K)
+    clocks.stop()
     barrier(world)
     p1 = ctx.profile()
     model = sess.end()
@@ -271,7 +290,7 @@ def main():
         except Exception:
             traffic = None
     roof["traffic"] = traffic
-    roof["kernel"] = "ttm_dmma_kernel (root TTM X x_c Q_c^T)"
+    roof["kernel"] = "ttm_tma_kernel (root TTM X x_c Q_c^T, TMA-staged DMMA)"
     roof["algorithmic_flops_per_launch"] = f_launch
     roof["algorithmic_bytes_per_launch"] = b_launch
     roof["avg_launch_ms"] = t_launch * 1e3
