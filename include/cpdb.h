@@ -218,6 +218,21 @@ int cpdb_closed_form_cost(uint32_t order, int32_t strategy, const uint64_t* dims
                           uint64_t* total);
 int cpdb_leading_flop_coefficient(uint32_t order, int32_t strategy, uint64_t* coeff);
 
+/* ---- mode-0 sharding plan (no reference counterpart: the
+ * reference is single-process) ------------------------------------------------
+ * For the steps of cpdb_schedule_build(order, strategy, iterations), in the
+ * same order, flags[i] is a CPDB_SHARD_* bit set and payload[i] the number of
+ * doubles the step exchanges (all-reduce of a partial sum, or the all-gather
+ * of V = I_0 x R after the mode-0 update's last step), for `world` ranks over
+ * dims (global extents).  The device session uses the same rule. */
+#define CPDB_SHARD_SRC_SHARDED 1
+#define CPDB_SHARD_ALLREDUCE 2
+#define CPDB_SHARD_OUT_SHARDED 4
+#define CPDB_SHARD_GATHER_V 8
+int cpdb_shard_plan(uint32_t order, int32_t strategy, uint64_t iterations, const uint64_t* dims,
+                    uint64_t rank, int world, int32_t* flags, uint64_t* payload, uint64_t cap,
+                    uint64_t* n_steps);
+
 /* ---- device-resident execute() (dim_tree.hpp:473-544) ------------------------- */
 /* One scheduled TTM on the device: reads X (source == CPDB_ROOT_KEY) or the
  * cache slot `source`, contracts `contract` with Q (I_c x R host matrix, the

@@ -645,6 +645,26 @@ def measured_cost(order: int, strategy, dims: Sequence[int], rank: int,
     return fl.value, ro.value
 
 
+SHARD_SRC_SHARDED, SHARD_ALLREDUCE, SHARD_OUT_SHARDED, SHARD_GATHER_V = 1, 2, 4, 8
+
+
+def shard_plan(order: int, strategy, iterations: int, dims: Sequence[int], rank: int,
+               world: int) -> Tuple[np.ndarray, np.ndarray]:
+    """Mode-0 sharding plan the device session follows: per
+    scheduled step (cpdb_schedule_build order) the SHARD_* flags and the number
+    of doubles exchanged (all-reduce of a partial sum / all-gather of V)."""
+    d = _u64(dims)
+    n = C.c_uint64()
+    _raise(_lib().cpdb_shard_plan(order, _strategy(strategy), iterations, _up(d), rank, world,
+                                  None, None, 0, C.byref(n)))
+    flags = np.zeros(n.value, dtype=np.int32)
+    payload = np.zeros(n.value, dtype=np.uint64)
+    _raise(_lib().cpdb_shard_plan(order, _strategy(strategy), iterations, _up(d), rank, world,
+                                  flags.ctypes.data_as(C.POINTER(C.c_int32)), _up(payload),
+                                  n.value, C.byref(n)))
+    return flags, payload
+
+
 def closed_form_cost(order: int, strategy, dims: Sequence[int], rank: int) -> int:
     """dim_tree.hpp:579-621"""
     d = _u64(dims)

@@ -138,6 +138,8 @@ SIGNATURES = {
                                      U64P]),
     "cpdb_closed_form_cost": (C.c_int, [C.c_uint32, C.c_int32, U64P, C.c_uint64, U64P]),
     "cpdb_leading_flop_coefficient": (C.c_int, [C.c_uint32, C.c_int32, U64P]),
+    "cpdb_shard_plan": (C.c_int, [C.c_uint32, C.c_int32, C.c_uint64, U64P, C.c_uint64, C.c_int,
+                                  C.POINTER(C.c_int32), U64P, C.c_uint64, U64P]),
     "cpdb_exec_step": (C.c_int, [CTX, C.c_uint32, C.c_uint32, C.c_uint32, P, C.c_uint64]),
     "cpdb_cache_dims": (C.c_int, [CTX, C.c_uint32, U64P, C.POINTER(C.c_int32)]),
     "cpdb_cache_get": (C.c_int, [CTX, C.c_uint32, P]),

@@ -610,6 +610,41 @@ int cpdb_measured_cost(uint32_t order, int32_t strategy, const uint64_t* dims, u
     });
 }
 
+int cpdb_shard_plan(uint32_t order, int32_t strategy, uint64_t iterations, const uint64_t* dims,
+                    uint64_t rank, int world, int32_t* flags, uint64_t* payload, uint64_t cap,
+                    uint64_t* n_steps) {
+    return guarded([&] {
+        if (strategy < 0 || strategy > 2) fail(CPDB_INVALID_ARGUMENT, "unknown strategy");
+        if (world < 1) fail(CPDB_INVALID_ARGUMENT, "shard_plan: world must be >= 1");
+        if (dims == nullptr || n_steps == nullptr) fail(CPDB_INVALID_ARGUMENT, "shard_plan: null");
+        const cpdb::Plan p =
+            cpdb::build_plan(order, static_cast<cpdb::Strategy>(strategy), iterations);
+        const bool dist = world > 1;
+        uint64_t i = 0;
+        for (const auto& sw : p.sweeps)
+            for (const auto& up : sw.updates)
+                for (size_t j = 0; j < up.steps.size(); ++j) {
+                    const cpdb::Step& st = up.steps[j];
+                    int32_t f = cpdb::shard_flags(st.source, st.contract, st.produces, up.mode,
+                                                  dist);
+                    if (j + 1 != up.steps.size()) f &= ~cpdb::kGatherV;
+                    uint64_t words = 0;
+                    if (f & cpdb::kAllReduce) {
+                        words = 1;
+                        for (uint32_t k = 0; k < order; ++k)
+                            words *= (st.produces & (1u << k)) ? dims[k] : rank;
+                    }
+                    if (f & cpdb::kGatherV) words += dims[0] * rank;
+                    if (i < cap) {
+                        if (flags) flags[i] = f;
+                        if (payload) payload[i] = words;
+                    }
+                    ++i;
+                }
+        *n_steps = i;
+    });
+}
+
 int cpdb_closed_form_cost(uint32_t order, int32_t strategy, const uint64_t* dims, uint64_t rank,
                           uint64_t* total) {
     return guarded([&] {

@@ -75,4 +75,27 @@ uint64_t leading_flop_coefficient(uint32_t order, Strategy s);
 
 inline uint32_t popcount(ModeSet s) { return static_cast<uint32_t>(__builtin_popcount(s)); }
 
+// ---- mode-0 sharding ---------------------------------------
+// X is split into contiguous slabs of mode-0 rows.  An intermediate Y(S) is
+// sharded exactly when mode 0 is still free (0 in S): contracting mode 0 of a
+// sharded source yields a partial sum that is all-reduced (the path's only
+// data exchange); every other TTM is local.  The mode-0 update's Y(0) keeps
+// local rows, so its V (I_0 x R) is all-gathered before the replicated tail.
+enum ShardFlag : int32_t {
+    kSrcSharded = 1,   // the step reads a sharded source
+    kAllReduce = 2,    // the step's output is a partial sum -> ncclAllReduce
+    kOutSharded = 4,   // the step's output stays sharded
+    kGatherV = 8,      // last step of the mode-0 update: all-gather V afterwards
+};
+inline bool set_sharded(ModeSet s, bool distributed) { return distributed && (s & 1u); }
+inline int32_t shard_flags(ModeSet source, uint32_t contract, ModeSet produces, uint32_t mode,
+                           bool distributed) {
+    int32_t f = 0;
+    if (set_sharded(source, distributed)) f |= kSrcSharded;
+    if ((f & kSrcSharded) && contract == 0) f |= kAllReduce;
+    if (set_sharded(produces, distributed)) f |= kOutSharded;
+    if (distributed && mode == 0 && produces == 1u) f |= kGatherV;
+    return f;
+}
+
 }  // namespace cpdb

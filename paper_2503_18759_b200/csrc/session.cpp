@@ -211,7 +211,7 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
             if (cache.count(key)) continue;
             std::vector<uint64_t> d = c->ldims;
             const double* cur = c->x;
-            bool cur_sharded = sharded;
+            ModeSet cur_set = plan.root();
             DevBuf tmp[2];
             int w = 0;
             for (uint32_t k = order; k-- > 0;) {
@@ -219,8 +219,9 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
                 std::vector<uint64_t> nd = d;
                 nd[k] = R;
                 double* out = tmp[w].ensure(numel(nd));
-                ttm_step(cur, d, cur_sharded, k, out, false);
-                if (k == 0) cur_sharded = false;
+                const ModeSet next = cur_set & ~(1u << k);
+                ttm_step(cur, d, shard_flags(cur_set, k, next, order, sharded), k, out, false);
+                cur_set = next;
                 cur = out;
                 d = nd;
                 w ^= 1;
@@ -231,7 +232,7 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
                                     cudaMemcpyDeviceToDevice, s));
             sl.valid = true;
             sl.dims = d;
-            sl.sharded = sharded && (key & 1u);
+            sl.sharded = set_sharded(key, sharded);
             sl.stamps.assign(order, 0);
             for (uint32_t k = 0; k < order; ++k)
                 if (!(key & (1u << k))) sl.stamps[k] = versions[k];
@@ -279,11 +280,11 @@ void Session::pack_local0() {
     c->launches += 1;
 }
 
-void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, bool src_sharded,
+void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32_t flags,
                        uint32_t k, double* dst, bool is_root) {
     const double* q = fb[k].q.p;
     const double* qp = fb[k].qp.p;
-    if (k == 0 && src_sharded) {
+    if (k == 0 && (flags & kSrcSharded)) {
         q += c->row_begin * R;
         qp = qp0_local.p;
     }
@@ -303,7 +304,7 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, bool 
         t.bytes = 8.0 * (double(nin) + double(nout) + double(sd[k]) * R);
         timers.push_back(t);
     }
-    if (src_sharded && k == 0 && sharded) {
+    if (flags & kAllReduce) {
         Timer tc;
         if (c->timing) {
             tc.a = events.get();
@@ -365,11 +366,10 @@ void Session::mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer,
         const double* src;
         std::vector<uint64_t> sd;
         std::vector<uint64_t> stamp(order, 0);
-        bool src_sh;
+        const int32_t flags = shard_flags(st.source, st.contract, st.produces, n, sharded);
         if (st.source == root) {
             src = c->x;
             sd = c->ldims;
-            src_sh = sharded;
         } else {
             auto it = cache.find(st.source);
             if (it == cache.end() || !it->second.valid)
@@ -382,13 +382,14 @@ void Session::mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer,
             src = it->second.buf.p;
             sd = it->second.dims;
             stamp = it->second.stamps;
-            src_sh = it->second.sharded;
+            if (it->second.sharded != bool(flags & kSrcSharded))
+                fail(CPDB_LOGIC_ERROR, "execute: shard layout of " + set_name(st.source, order));
         }
         std::vector<uint64_t> od = sd;
         od[st.contract] = R;
         double* dst =
             (st.produces == (1u << n)) ? ybuf[n].p : cache[st.produces].buf.ensure(numel(od));
-        ttm_step(src, sd, src_sh, st.contract, dst, st.source == root);
+        ttm_step(src, sd, flags, st.contract, dst, st.source == root);
         // global-extent flop count, exactly as the reference counts it
         uint64_t gout = 1;
         for (uint32_t k = 0; k < order; ++k)
@@ -401,7 +402,7 @@ void Session::mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer,
             sl.valid = true;
             sl.dims = od;
             sl.stamps = stamp;
-            sl.sharded = src_sh && st.contract != 0;
+            sl.sharded = (flags & kOutSharded) != 0;
         }
     }
     const std::vector<ModeSet> keep = retained_keys(plan, sweep - 1, b);
@@ -432,7 +433,7 @@ void Session::mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer,
     c->launches += 1;
     // split-K partials -> V (this rank's rows; sharded mode-0 updates gather
     // the full V on every rank)
-    const bool gather = sharded && n == 0;
+    const bool gather = (shard_flags(0, 0, 1u << n, n, sharded) & kGatherV) != 0;
     const uint64_t off = gather ? c->row_begin * R : 0;
     CPDB_CK(reduce_splits(v.vpart, v.nsplit, v.I * R, vfull.p + off, s));
     if (v.dual) CPDB_CK(reduce_splits(v.vfitpart, v.nsplit, v.I * R, vfitfull.p + off, s));

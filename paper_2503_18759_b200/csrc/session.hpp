@@ -62,7 +62,7 @@ private:
     std::vector<uint64_t> local_dims_of(uint32_t key) const;
     void qr_factor(uint32_t k);
     void pack_local0();
-    void ttm_step(const double* src, const std::vector<uint64_t>& sd, bool src_sharded,
+    void ttm_step(const double* src, const std::vector<uint64_t>& sd, int32_t flags,
                   uint32_t k, double* dst, bool is_root);
     void mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer, void* user,
                      double& beta_used);
