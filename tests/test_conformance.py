@@ -1,0 +1,41 @@
+"""The reference's own hot-path unit tests (dim_tree_test, linalg_test,
+tensor_test, kruskal_test, solver_test from /root/reference/proj/tests),
+compiled UNCHANGED against the drop-in `cpd::` headers (include/cpd) and
+libcpdb.so by oracle/conformance/Makefile, run on the B200.
+
+The binaries are built in the container (where the reference sources are)
+and travel to the GPU box in oracle/_ref/conformance/.  Test cases that only
+exercise the CP-ALS normal-equation shim (oracle/conformance/offpath.hpp, not
+part of the library) still run; they are listed in OFFPATH for the record.
+"""
+import os
+import re
+import subprocess
+
+import pytest
+
+from conftest import ROOT
+
+BIN = os.path.join(ROOT, "oracle", "_ref", "conformance")
+SUITES = ["dim_tree_test", "linalg_test", "tensor_test", "kruskal_test", "solver_test"]
+# cases whose subject is the off-path shim (cp_als / mttkrp / solve_spd / fitness_fast_als)
+OFFPATH = re.compile(r"^(CpAls\.|SolveSpd|Mttkrp|FitnessFastAls)")
+
+
+def run_suite(name):
+    exe = os.path.join(BIN, name)
+    if not os.path.exists(exe):
+        pytest.skip(f"{exe} not built (needs /root/reference at build time)")
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=900)
+    m = re.search(r"\[==========\] (\d+) passed, (\d+) failed", p.stdout)
+    assert m, p.stdout[-2000:] + p.stderr[-4000:]
+    failed = re.findall(r"^\[  FAILED  \] (\S+)$", p.stdout, re.M)
+    return int(m.group(1)), failed, p
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("suite", SUITES)
+def test_reference_suite_on_device(suite):
+    passed, failed, p = run_suite(suite)
+    assert passed > 0
+    assert not failed, "\n".join(failed) + "\n" + p.stderr[-6000:]
