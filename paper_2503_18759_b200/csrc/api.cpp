@@ -4,6 +4,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <new>
 #include <string>
 #include <vector>
@@ -102,6 +104,13 @@ void set_local_geometry(cpdb_ctx* c, const std::vector<uint64_t>& d) {
     c->slots.clear();
 }
 
+int live_contexts(int device, int delta) {
+    static std::mutex mu;
+    static std::map<int, int> live;
+    std::lock_guard<std::mutex> lk(mu);
+    return live[device] += delta;
+}
+
 cpdb::Plan plan_from_steps(uint32_t order, const int64_t* steps, uint64_t n, uint64_t iterations) {
     cpdb::Plan p;
     p.order = order;
@@ -146,6 +155,7 @@ int cpdb_create(int device, cpdb_ctx** out) {
         delete c;
         return rc;
     }
+    live_contexts(c->device, +1);
     *out = c;
     return CPDB_OK;
 }
@@ -187,14 +197,18 @@ int cpdb_create_sharded(int device, int rank, int world, const void* nccl_id, cp
         delete c;
         return rc;
     }
+    live_contexts(c->device, +1);
     *out = c;
     return CPDB_OK;
 }
 
 void cpdb_destroy(cpdb_ctx* ctx) {
     if (!ctx) return;
-    cudaSetDevice(ctx->device);
+    const int dev = ctx->device;
+    cudaSetDevice(dev);
     delete ctx;
+    // the last context on a device hands the cached blocks back to the driver
+    if (live_contexts(dev, -1) == 0) cpdb::dev_trim(dev);
 }
 
 int cpdb_shard_rows(uint64_t extent0, int rank, int world, uint64_t* begin, uint64_t* count) {

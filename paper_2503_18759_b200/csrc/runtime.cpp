@@ -16,6 +16,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 
 #include "comm.hpp"
@@ -32,17 +33,90 @@ void check_cuda(cudaError_t e, const char* where) {
                std::string(where) + ": " + cudaGetErrorString(e)};
 }
 
-DevBuf::~DevBuf() {
-    if (p) cudaFree(p);
+namespace {
+
+struct Block {
+    int dev;
+    size_t bytes;
+    void* p;
+};
+std::mutex g_pool_mu;
+std::vector<Block> g_pool;
+
+}  // namespace
+
+void* dev_alloc(size_t bytes, int* device, size_t* got) {
+    int dev = 0;
+    CPDB_CK(cudaGetDevice(&dev));
+    *device = dev;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        size_t best = g_pool.size();
+        for (size_t i = 0; i < g_pool.size(); ++i) {
+            const Block& b = g_pool[i];
+            if (b.dev != dev || b.bytes < bytes || b.bytes > 2 * bytes + (1u << 20)) continue;
+            if (best == g_pool.size() || b.bytes < g_pool[best].bytes) best = i;
+        }
+        if (best != g_pool.size()) {
+            void* p = g_pool[best].p;
+            *got = g_pool[best].bytes;
+            g_pool.erase(g_pool.begin() + long(best));
+            return p;
+        }
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e == cudaErrorMemoryAllocation) {
+        cudaGetLastError();
+        dev_trim(dev);
+        e = cudaMalloc(&p, bytes);
+    }
+    CPDB_CK(e);
+    *got = bytes;
+    return p;
 }
+
+void dev_release(void* p, size_t bytes, int device) {
+    if (!p) return;
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != device) cudaSetDevice(device);
+    cudaDeviceSynchronize();  // no kernel may still use the block
+    if (cur != device) cudaSetDevice(cur);
+    std::lock_guard<std::mutex> lk(g_pool_mu);
+    g_pool.push_back({device, bytes, p});
+}
+
+void dev_trim(int device) {
+    std::vector<void*> drop;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        for (size_t i = 0; i < g_pool.size();) {
+            if (g_pool[i].dev == device) {
+                drop.push_back(g_pool[i].p);
+                g_pool.erase(g_pool.begin() + long(i));
+            } else {
+                ++i;
+            }
+        }
+    }
+    int cur = 0;
+    cudaGetDevice(&cur);
+    if (cur != device) cudaSetDevice(device);
+    for (void* p : drop) cudaFree(p);
+    if (cur != device) cudaSetDevice(cur);
+}
+
+DevBuf::~DevBuf() { dev_release(p, n * sizeof(double), dev); }
 
 double* DevBuf::ensure(size_t d) {
     if (p && d <= n) return p;
-    if (p) cudaFree(p);
+    dev_release(p, n * sizeof(double), dev);
     p = nullptr;
     n = 0;
-    CPDB_CK(cudaMalloc(&p, std::max<size_t>(d, 1) * sizeof(double)));
-    n = std::max<size_t>(d, 1);
+    size_t got = 0;
+    p = static_cast<double*>(dev_alloc(std::max<size_t>(d, 1) * sizeof(double), &dev, &got));
+    n = got / sizeof(double);
     return p;
 }
 

@@ -31,14 +31,26 @@ struct Fail {
 void check_cuda(cudaError_t e, const char* where);
 #define CPDB_CK(expr) ::cpdb::check_cuda((expr), #expr)
 
-// Growable device allocation (never shrinks; freed with the context).
+// Device memory cache: released blocks are kept per device and handed out
+// again (best fit within 2x), so a new session / context on the same GPU does
+// not pay cudaMalloc/cudaFree of GB-sized buffers (page mapping costs ms and
+// made the host-buffer e2e runs jitter).  release() synchronises the device
+// first, so a block is never handed out while a kernel may still touch it.
+// On allocation failure the cache of that device is returned to the driver
+// and the allocation retried once.
+void* dev_alloc(size_t bytes, int* device, size_t* got);
+void dev_release(void* p, size_t bytes, int device);
+void dev_trim(int device);  // give every cached block of `device` back
+
+// Growable device allocation (never shrinks; released with its owner).
 struct DevBuf {
     double* p = nullptr;
     size_t n = 0;  // doubles
+    int dev = -1;
     DevBuf() = default;
     DevBuf(const DevBuf&) = delete;
     DevBuf& operator=(const DevBuf&) = delete;
-    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n) {
+    DevBuf(DevBuf&& o) noexcept : p(o.p), n(o.n), dev(o.dev) {
         o.p = nullptr;
         o.n = 0;
     }
@@ -47,6 +59,7 @@ struct DevBuf {
     void swap(DevBuf& o) noexcept {
         std::swap(p, o.p);
         std::swap(n, o.n);
+        std::swap(dev, o.dev);
     }
 };
 
