@@ -19,6 +19,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
@@ -314,18 +315,55 @@ cudaError_t launch_v2(const TtmArgs& a, cudaStream_t s, int sms) {
     return cudaGetLastError();
 }
 
+// Tiles a launch would have with CB column blocks per consumer warp.
+template <int LAYOUT>
+uint64_t tiles_with(const TtmArgs& a, int cb, int nc) {
+    const uint64_t per = uint64_t(nc) * cb * (LAYOUT == kGroups ? 1 : 8);
+    const uint64_t cols = LAYOUT == kGroups ? (a.outer * a.inner) / 8 : a.outer;
+    return (cols + per - 1) / per;
+}
+
+// Pick the widest tile (CB0, CB0/2, CB0/4) that still fills the GPU: score =
+// SM utilisation of the last wave x a per-CB efficiency (narrower tiles
+// re-load Q fragments more often per DMMA).  Branch TTMs on the R-sized
+// intermediates are small (C2: 64 tiles at CB 4), so they drop to CB 2.
+template <int RB, int CB0, int BK, int ST, int LAYOUT>
+cudaError_t launch_adaptive(const TtmArgs& a, cudaStream_t s, int sms) {
+    constexpr int NC = 8;
+    int best = CB0;
+    double best_score = -1.0;
+    for (int cb = CB0; cb >= 1 && cb >= CB0 / 4; cb /= 2) {
+        const uint64_t t = tiles_with<LAYOUT>(a, cb, NC);
+        const double waves = std::ceil(double(t) / sms);
+        const double util = double(t) / (waves * sms);
+        const double eff = cb == CB0 ? 1.0 : (cb == CB0 / 2 ? 0.9 : 0.7);
+        const double score = util * eff;
+        if (score > best_score + 1e-9) {
+            best_score = score;
+            best = cb;
+        }
+    }
+    if constexpr (CB0 >= 4) {
+        if (best == CB0 / 4) return launch_v2<RB, CB0 / 4, BK, ST, NC, LAYOUT>(a, s, sms);
+    }
+    if constexpr (CB0 >= 2) {
+        if (best == CB0 / 2) return launch_v2<RB, CB0 / 2, BK, ST, NC, LAYOUT>(a, s, sms);
+    }
+    return launch_v2<RB, CB0, BK, ST, NC, LAYOUT>(a, s, sms);
+}
+
 template <int LAYOUT>
 cudaError_t dispatch_v2(const TtmArgs& a, cudaStream_t s, int sms) {
-    // X stage ~32 KB; Q stage small; 5 stages in flight
+    // X stage ~32 KB at the widest tile; 4-5 stages in flight
     switch (a.Rp / 8) {
-        case 1: return launch_v2<1, 8, 8, 5, 8, LAYOUT>(a, s, sms);
-        case 2: return launch_v2<2, 8, 8, 5, 8, LAYOUT>(a, s, sms);
-        case 3: return launch_v2<3, 4, 16, 5, 8, LAYOUT>(a, s, sms);
-        case 4: return launch_v2<4, 4, 16, 5, 8, LAYOUT>(a, s, sms);
-        case 5: return launch_v2<5, 2, 32, 4, 8, LAYOUT>(a, s, sms);
-        case 6: return launch_v2<6, 2, 32, 4, 8, LAYOUT>(a, s, sms);
-        case 7: return launch_v2<7, 2, 32, 4, 8, LAYOUT>(a, s, sms);
-        case 8: return launch_v2<8, 2, 32, 4, 8, LAYOUT>(a, s, sms);
+        case 1: return launch_adaptive<1, 8, 8, 5, LAYOUT>(a, s, sms);
+        case 2: return launch_adaptive<2, 8, 8, 5, LAYOUT>(a, s, sms);
+        case 3: return launch_adaptive<3, 4, 16, 5, LAYOUT>(a, s, sms);
+        case 4: return launch_adaptive<4, 4, 16, 5, LAYOUT>(a, s, sms);
+        case 5: return launch_adaptive<5, 2, 32, 4, LAYOUT>(a, s, sms);
+        case 6: return launch_adaptive<6, 2, 32, 4, LAYOUT>(a, s, sms);
+        case 7: return launch_adaptive<7, 2, 32, 4, LAYOUT>(a, s, sms);
+        case 8: return launch_adaptive<8, 2, 32, 4, LAYOUT>(a, s, sms);
     }
     return cudaErrorInvalidValue;
 }

@@ -23,7 +23,7 @@ namespace cpdb {
 namespace {
 
 constexpr int kNT = 512;
-constexpr int kTile = 256;      // Z rows staged per tile
+constexpr int kTile = 256;      // Z rows staged per tile (fewer when R is large)
 constexpr int kMaxParts = 296;  // G2 partials (one per CTA)
 
 // work layout (doubles): [U1 | G2 -> U2 | partials of G2 ...]
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(kNT) zqr_prep_kernel(ZqrArgs a) {
 
 // Q1 = Z U1^-1 tile by tile; per-CTA partial G2 = Q1^T Q1 on DMMA.
 template <int RM>
-__global__ void __launch_bounds__(kNT) zqr_rows_kernel(ZqrArgs a) {
+__global__ void __launch_bounds__(kNT) zqr_rows_kernel(ZqrArgs a, int tile_rows) {
     using Row = LaneRow<RM>;
     constexpr int T = Row::T, G = kNT / T;
     extern __shared__ double sm[];
@@ -67,12 +67,12 @@ __global__ void __launch_bounds__(kNT) zqr_rows_kernel(ZqrArgs a) {
     stage_tri<RM>(a.work, R, R, u, dinv, kNT);
     for (int e = threadIdx.x; e < R * R; e += kNT) part[e] = 0.0;
     const int grp = threadIdx.x / T, q = threadIdx.x % T;
-    const uint64_t ntiles = (a.zrows + kTile - 1) / kTile;
+    const uint64_t ntiles = (a.zrows + tile_rows - 1) / tile_rows;
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-        const uint64_t row0 = t * kTile;
-        const int rows = int(min(uint64_t(kTile), a.zrows - row0));
+        const uint64_t row0 = t * tile_rows;
+        const int rows = int(min(uint64_t(tile_rows), a.zrows - row0));
         __syncthreads();
-        for (int li = grp; li < kTile; li += G) {
+        for (int li = grp; li < tile_rows + (G - tile_rows % G) % G; li += G) {
             const bool act = li < rows;
             Row x;
 #pragma unroll
@@ -168,15 +168,23 @@ __global__ void __launch_bounds__(kNT) zqr_apply_kernel(ZqrArgs a) {
 template <int RM>
 cudaError_t run_multi(const ZqrArgs& a, cudaStream_t s, int sms) {
     const int R = a.R;
-    const size_t rows_smem = (size_t(a.nm) * R * R + RM * RM + RM + size_t(R) * R +
-                              size_t(kTile) * (R + 1)) * sizeof(double);
-    cudaFuncSetAttribute(zqr_rows_kernel<RM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         220 * 1024);
+    const size_t fixed = size_t(a.nm) * R * R + RM * RM + RM + size_t(R) * R;
+    constexpr size_t kBudget = 220 * 1024 / sizeof(double);
+    if (fixed + 32 * size_t(R + 1) > kBudget) return cudaErrorInvalidValue;
+    // rows per staged tile: as many as fit (multiple of 32), at most kTile
+    const int tile = int(std::min<size_t>(kTile, ((kBudget - fixed) / (R + 1)) / 32 * 32));
+    const size_t rows_smem = (fixed + size_t(tile) * (R + 1)) * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(zqr_rows_kernel<RM>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    if (e != cudaSuccess) return e;
     zqr_prep_kernel<RM><<<1, kNT, size_t(R) * R * sizeof(double), s>>>(a);
-    const uint64_t ntiles = (a.zrows + kTile - 1) / kTile;
+    const uint64_t ntiles = (a.zrows + tile - 1) / tile;
     const int grid = int(std::min<uint64_t>(ntiles, uint64_t(std::min(2 * sms, kMaxParts))));
-    zqr_rows_kernel<RM><<<grid, kNT, rows_smem, s>>>(a);
+    zqr_rows_kernel<RM><<<grid, kNT, rows_smem, s>>>(a, tile);
     zqr_reduce_kernel<<<(R * R + kNT - 1) / kNT, kNT, 0, s>>>(a, grid);
+    e = cudaFuncSetAttribute(zqr_fin_kernel<RM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(2 * RM * RM * sizeof(double)));
+    if (e != cudaSuccess) return e;
     zqr_fin_kernel<RM><<<1, kNT, 2 * size_t(R) * R * sizeof(double), s>>>(a);
     const uint64_t groups = (a.zrows + (kNT / LaneRow<RM>::T) - 1) / (kNT / LaneRow<RM>::T);
     const int agrid = int(std::min<uint64_t>(groups, uint64_t(4 * sms)));
