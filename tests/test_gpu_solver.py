@@ -182,3 +182,73 @@ def ctx_solve_state(ctx, x, rank, st):
     ctx.set_tensor(x)
     state = cpd.SweepState(**st)
     return ctx.solve(cfg_of(rank, 1, seed=7), extrapolate=True, state=state)
+
+
+# ---------------------------------------------------------------- full BASELINE sizes
+FULL = {  # (kind, dims, rank, rho)  BASELINE.json configs 2, 3, 5
+    "c2": (0, (512, 512, 512), 32, 1e-3),
+    "c3": (0, (128, 128, 128, 128), 16, 1e-2),
+    "c5": (0, (256, 256, 256, 256), 64, 1e-3),
+}
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c5"])
+def test_full_size_sweep_properties(name):
+    """Size-independent properties at BASELINE's full sizes (C5: 34 GB in HBM):
+    integer flops / root counts equal the scheduler's dry run (bit-exact),
+    update orders follow the plan, factors have unit columns and Q has
+    orthonormal columns, fitness in [0, 1], and a second run is bit-identical."""
+    import paper_2503_18759_b200 as cpd
+    kind, dims, rank, rho = FULL[name]
+    sweeps = 4
+    ctx = cpd.Context(0)
+    ctx.synth_tensor(kind, list(dims), rank, rho, META["truth_seeds"][name])
+    cfg = cfg_of(rank, sweeps, seed=META["init_seed"])
+    runs = []
+    for _ in range(2):
+        s = ctx.session(cfg, extrapolate=True)
+        rows = s.run(sweeps)
+        model = s.end()
+        s.close()
+        runs.append((rows, model))
+    rows, model = runs[0]
+    sched = cpd.build_schedule(len(dims), "branch-reuse", sweeps)
+    for i, r in enumerate(rows):
+        fl, roots = cpd.measured_cost(len(dims), "branch-reuse", dims, rank, i + 1)
+        assert r.flops == fl and r.root_ttm_count == roots
+        assert r.update_order == sched.update_order(i)
+        assert 0.0 <= r.fitness <= 1.0
+    for f in model.factors:
+        assert np.allclose(np.linalg.norm(f, axis=0), 1.0, atol=1e-12)
+        assert np.linalg.matrix_rank(f) == rank
+    assert [(r.fitness, r.raw_radicand) for r in runs[1][0]] == \
+        [(r.fitness, r.raw_radicand) for r in rows]
+    for fa, fb in zip(runs[1][1].factors, model.factors):
+        assert np.array_equal(fa, fb)
+
+
+@pytest.mark.parametrize("name,k", [("c2", 2), ("c3", 3)])
+def test_full_size_teacher_forced(port, name, k):
+    """Teacher-forced sweep at BASELINE's full C2 / C3 size: the oracle's state
+    after sweep k (restated C port, single core) -> one device sweep vs the
+    oracle's sweep k+1.  Fitness <= 1e-10 relative, factors
+    <= 1e-10, identical integer flops."""
+    import paper_2503_18759_b200 as cpd
+    from oracle.pyoracle import SweepState
+    kind, dims, rank, rho = FULL[name]
+    ctx = cpd.Context(0)
+    ctx.synth_tensor(kind, list(dims), rank, rho, META["truth_seeds"][name])
+    x = ctx.get_tensor(list(dims))
+    init = port_init(port, x.shape, rank, META["init_seed"])
+    s0 = port.solve(x, rank, k, extrapolate=True, seed=META["init_seed"],
+                    state=SweepState(0, np.ones(rank), init))
+    st = s0.state
+    o = port.solve(x, rank, 1, extrapolate=True, seed=META["init_seed"], state=SweepState(**st))
+    g = ctx.solve(cfg_of(rank, 1, seed=META["init_seed"]), extrapolate=True,
+                  state=cpd.SweepState(**st))
+    assert g.trace[0].iteration == k + 1
+    assert g.trace[0].flops == o.trace[0]["flops"]
+    assert g.trace[0].root_ttm_count == o.trace[0]["root_ttm_count"]
+    assert abs(g.trace[0].fitness - o.trace[0]["fitness"]) <= FIT_TOL * o.trace[0]["fitness"]
+    for fg, fo in zip(g.model.factors, o.factors):
+        assert np.linalg.norm(fg - fo) / np.linalg.norm(fo) <= FACTOR_TOL
