@@ -68,7 +68,6 @@ template <int RM>
 __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
     using Row = LaneRow<RM>;
     constexpr int T = Row::T, G = kNT / T;
-    constexpr int KC = (RM * RM + kNT - 1) / kNT;
     cg::cluster_group cl = cg::this_cluster();
     const int rank = int(cl.block_rank());
     extern __shared__ double sm[];
@@ -165,7 +164,7 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
             }
             __syncthreads();
         }
-        const bool ok = block_chol<kNT, KC>(S.g, R, R);
+        const bool ok = chol<kNT, RM>(S.g, R, R);
         if (threadIdx.x == 0) S.misc[2] = ok ? 0.0 : 1.0;
         CPDB_TS(5);
     }
@@ -219,7 +218,7 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
     if (rank == 0) {
         cluster_reduce(cl, S.p, R * R, S.g);
         __syncthreads();
-        const bool ok = block_chol<kNT, KC>(S.g, R, R);
+        const bool ok = chol<kNT, RM>(S.g, R, R);
         if (threadIdx.x == 0) S.misc[2] = ok ? 0.0 : 1.0;
         CPDB_TS(11);
         if (ok) {
@@ -303,7 +302,6 @@ template <int RM>
 __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
     using Row = LaneRow<RM>;
     constexpr int T = Row::T, G = kNT / T;
-    constexpr int KC = (RM * RM + kNT - 1) / kNT;
     cg::cluster_group cl = cg::this_cluster();
     const int rank = int(cl.block_rank());
     extern __shared__ double sm[];
@@ -335,7 +333,7 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
         S.g[e] = h;
     }
     __syncthreads();
-    const bool ok1 = block_chol<kNT, KC>(S.g, R, R);
+    const bool ok1 = chol<kNT, RM>(S.g, R, R);
     if (!ok1 && rank == 0 && threadIdx.x == 0) *a.status = 2;
     stage_tri<RM>(S.g, R, R, S.u, S.dinv, kNT);  // U1 (kept in S.g too)
     __syncthreads();
@@ -372,7 +370,7 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
         __syncthreads();
         cluster_reduce(cl, S.p, R * R, S.g);
         __syncthreads();
-        const bool ok2 = block_chol<kNT, KC>(S.g, R, R);
+        const bool ok2 = chol<kNT, RM>(S.g, R, R);
         if (!ok2 && threadIdx.x == 0) *a.status = 2;
         for (int e = threadIdx.x; e < R * R; e += kNT) {  // R0 = U2 U1
             const int i = e / R, j = e % R;

@@ -20,7 +20,6 @@ template <int RM>
 __global__ void __launch_bounds__(kNT) finish_single_kernel(FinishArgs a, int w_in_smem) {
     using Row = LaneRow<RM>;
     constexpr int T = Row::T, G = kNT / T;
-    constexpr int KC = (RM * RM + kNT - 1) / kNT;
     extern __shared__ double sm[];
     __shared__ double red[32];
     const int R = a.R, ld = R + 1;
@@ -82,7 +81,7 @@ __global__ void __launch_bounds__(kNT) finish_single_kernel(FinishArgs a, int w_
         }
         __syncthreads();
     }
-    if (!block_chol<kNT, KC>(g, R, R)) {
+    if (!chol<kNT, RM>(g, R, R)) {
         if (threadIdx.x == 0) *a.status = 2;
         return;
     }
@@ -110,7 +109,7 @@ __global__ void __launch_bounds__(kNT) finish_single_kernel(FinishArgs a, int w_
     __syncthreads();
     gram_dmma<kNT>(w, ld, I, R, g, R);
     __syncthreads();
-    if (!block_chol<kNT, KC>(g, R, R)) {
+    if (!chol<kNT, RM>(g, R, R)) {
         if (threadIdx.x == 0) *a.status = 2;
         return;
     }

@@ -45,8 +45,7 @@ __global__ void __launch_bounds__(kNT) zqr_prep_kernel(ZqrArgs a) {
         g[e] = h;
     }
     __syncthreads();
-    constexpr int KC = (RM * RM + kNT - 1) / kNT;
-    if (!block_chol<kNT, KC>(g, R, R) && threadIdx.x == 0) *a.status = 2;
+    if (!chol<kNT, RM>(g, R, R) && threadIdx.x == 0) *a.status = 2;
     for (int e = threadIdx.x; e < R * R; e += kNT) a.work[e] = g[e];
 }
 
@@ -132,8 +131,7 @@ __global__ void __launch_bounds__(kNT) zqr_fin_kernel(ZqrArgs a) {
         u1[e] = a.work[e];
     }
     __syncthreads();
-    constexpr int KC = (RM * RM + kNT - 1) / kNT;
-    if (!block_chol<kNT, KC>(g, R, R) && threadIdx.x == 0) *a.status = 2;
+    if (!chol<kNT, RM>(g, R, R) && threadIdx.x == 0) *a.status = 2;
     for (int e = threadIdx.x; e < R * R; e += kNT) {
         const int i = e / R, j = e % R;
         double s = 0.0;
