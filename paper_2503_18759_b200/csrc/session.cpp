@@ -59,6 +59,12 @@ void EventPool::recycle() {
     used.clear();
 }
 
+void EventPool::recycle_prefix(size_t n) {
+    n = std::min(n, used.size());
+    free_.insert(free_.end(), used.begin(), used.begin() + long(n));
+    used.erase(used.begin(), used.begin() + long(n));
+}
+
 EventPool::~EventPool() {
     for (auto e : free_) cudaEventDestroy(e);
     for (auto e : used) cudaEventDestroy(e);
@@ -323,9 +329,17 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32
 // ---------------------------------------------------------------- one mode update
 void Session::mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer, void* user,
                           double& beta_used) {
+    mode_update_front(sweep, b, observer, user);
+    mode_update_back(sweep, b, beta_used);
+}
+
+// Steps 1-2 and 4: Z-QR (side stream) and the TTM chain.  Neither depends on
+// the beta decision, so the first update of the next sweep can be issued
+// before the host reads this sweep's fitness (Session::run).
+void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer observer,
+                                void* user) {
     const Sweep& sw = plan.sweeps[sweep - 1];
     const uint32_t n = sw.updates[b].mode;
-    const bool last = (b == order - 1);
     const uint32_t root = plan.root();
 
     // 1-2. Khatri-Rao + QR of the other R_k -> Q0, R0 (solvers.hpp:250-255)
@@ -357,10 +371,6 @@ void Session::mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer,
             std::memcpy(&ref[perm[i] * R], &nat[i * R], R * sizeof(double));
         observer(user, sweep, n, ref.data(), zrows, R);
     }
-    // 3. extrapolation gate (solvers.hpp:260-265)
-    const bool use_ex = extrap && has_beta && beta != 0.0 && has_hist[n];
-    if (use_ex) beta_used = beta;
-
     // 4. the scheduled TTM chain (execute, dim_tree.hpp:496-541)
     for (const Step& st : sw.updates[b].steps) {
         const double* src;
@@ -408,6 +418,17 @@ void Session::mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer,
     const std::vector<ModeSet> keep = retained_keys(plan, sweep - 1, b);
     for (auto& kv : cache)
         if (std::find(keep.begin(), keep.end(), kv.first) == keep.end()) kv.second.valid = false;
+
+}
+
+// Steps 3 and 5-9: extrapolation gate, V, and the mode-update tail.
+void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
+    const Sweep& sw = plan.sweeps[sweep - 1];
+    const uint32_t n = sw.updates[b].mode;
+    const bool last = (b == order - 1);
+    // 3. extrapolation gate (solvers.hpp:260-265)
+    const bool use_ex = extrap && has_beta && beta != 0.0 && has_hist[n];
+    if (use_ex) beta_used = beta;
 
     // 5. V = Y_(n) Q0_hat (+ the unextrapolated V for the fitness, :277-284)
     const std::vector<uint64_t> yd = local_dims_of(1u << n);
@@ -496,13 +517,33 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         const uint64_t sweep = done + 1;
         const Sweep& sw = plan.sweeps[sweep - 1];
         double beta_used = 0.0;
-        CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
-        for (uint32_t b = 0; b < order; ++b) mode_update(sweep, b, observer, user, beta_used);
+        if (!front_issued) CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
+        for (uint32_t b = 0; b < order; ++b) {
+            if (b == 0 && front_issued) {
+                front_issued = false;  // issued ahead of the previous sweep's host sync
+            } else {
+                mode_update_front(sweep, b, observer, user);
+            }
+            mode_update_back(sweep, b, beta_used);
+        }
         cudaEvent_t e_end = events.get();
         CPDB_CK(cudaEventRecord(e_end, s));
         CPDB_CK(cudaMemcpyAsync(c->pinned, fitbuf.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
         CPDB_CK(cudaMemcpyAsync(c->pinned + 2, c->dstatus, sizeof(int), cudaMemcpyDeviceToHost, s));
-        CPDB_CK(cudaStreamSynchronize(s));
+        cudaEvent_t e_fit = events.get();
+        CPDB_CK(cudaEventRecord(e_fit, s));
+        const Cost at_end = total;
+        const size_t ntimers = timers.size(), nevents = events.used.size();
+        // Hide the host round trip: the next sweep's first Z-QR + TTM chain do
+        // not depend on the beta gate, so they go on the stream before the
+        // host waits for this sweep's fitness (wasted only if it converges).
+        const bool more = rows_out + 1 < nsweeps && done + 1 < last_sweep;
+        if (more && observer == nullptr && fps == nullptr) {
+            CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
+            mode_update_front(sweep + 1, 0, nullptr, nullptr);
+            front_issued = true;
+        }
+        CPDB_CK(cudaEventSynchronize(e_fit));
         int status;
         std::memcpy(&status, c->pinned + 2, sizeof(int));
         if (status) {
@@ -518,7 +559,8 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         CPDB_CK(cudaEventElapsedTime(&ms, t_start, e_end));
         if (sweep == first_sweep + 1) c->prof.sweep1_ms = ms;
         c->prof.solve_ms = ms;
-        for (const Timer& t : timers) {
+        for (size_t ti = 0; ti < ntimers; ++ti) {
+            const Timer& t = timers[ti];
             float tm = 0.f;
             CPDB_CK(cudaEventElapsedTime(&tm, t.a, t.b));
             if (t.kind == 0) {
@@ -532,8 +574,8 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
                 c->prof.comm_ms += tm;
             }
         }
-        timers.clear();
-        events.recycle();
+        timers.erase(timers.begin(), timers.begin() + long(ntimers));
+        events.recycle_prefix(nevents);
         if (trace) {
             cpdb_trace_row& row = trace[rows_out];
             std::memset(&row, 0, sizeof row);
@@ -543,8 +585,8 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
             row.fitness = fit;
             row.raw_radicand = raw;
             row.wall_seconds = ms * 1e-3;
-            row.root_ttm_count = total.roots;
-            row.flops = total.flops;
+            row.root_ttm_count = at_end.roots;
+            row.flops = at_end.flops;
             row.beta_used = beta_used;
         }
         if (fps) {

@@ -13,6 +13,7 @@ struct EventPool {
     std::vector<cudaEvent_t> free_, used;
     cudaEvent_t get();
     void recycle();
+    void recycle_prefix(size_t n);  // the first n events handed out since the last recycle
     ~EventPool();
 };
 
@@ -46,6 +47,7 @@ struct Session {
     Cost total;
 
     EventPool events;
+    bool front_issued = false;  // next sweep's first Z-QR + TTM chain already on the stream
     std::vector<Timer> timers;
     cudaEvent_t t_start = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_zqr = nullptr;  // main -> side -> main fork/join
@@ -66,6 +68,8 @@ private:
                   uint32_t k, double* dst, bool is_root);
     void mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer, void* user,
                      double& beta_used);
+    void mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer observer, void* user);
+    void mode_update_back(uint64_t sweep, uint32_t b, double& beta_used);
 };
 
 }  // namespace cpdb
