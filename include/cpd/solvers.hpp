@@ -134,33 +134,11 @@ struct ObserverBridge {
     }
 };
 
-// One solve on a private device context (run_qr, solvers.hpp:215-309).
-inline SolveResult run_qr(const DenseTensor& x, const SolverConfig& cfg,
-                          const std::optional<KruskalModel>& init, bool extrapolate) {
-    cfg.validate();
-    const std::size_t order = x.order();
-    if (order < 2) throw std::invalid_argument("cp_als_qr: tensor order must be >= 2");
-    for (std::size_t k = 0; k < order; ++k)
-        if (cfg.rank > x.shape().extent(k))
-            throw std::invalid_argument(
-                "cp_als_qr: rank must not exceed any mode extent (compact QR)");
-    std::vector<double> init_f, init_l;
-    if (init) {
-        for (const Matrix& f : initial_factors(x, cfg, init))
-            init_f.insert(init_f.end(), f.values().begin(), f.values().end());
-        init_l = initial_lambda(init, cfg.rank);
-    }
-
-    cpdb_ctx* ctx = nullptr;
-    const char* env = std::getenv("CPD_DEVICE");
-    abi::check(cpdb_create(env ? std::atoi(env) : 0, &ctx));
-    struct Guard {
-        cpdb_ctx* c;
-        ~Guard() { cpdb_destroy(c); }
-    } guard{ctx};
-    const std::vector<uint64_t> dims = abi::u64(x.shape().dims());
-    abi::check(cpdb_tensor_set(ctx, x.data(), dims.data(), uint32_t(order)));
-
+// One run on a context that already holds X (dims = its global extents):
+// the device-resident loop of run_qr (solvers.hpp:215-309).
+inline SolveResult run_on_context(cpdb_ctx* ctx, const std::vector<std::size_t>& dims,
+                                  const SolverConfig& cfg, const std::vector<double>* init_f,
+                                  const std::vector<double>* init_l, bool extrapolate) {
     cpdb_config c{};
     c.rank = cfg.rank;
     c.max_iterations = cfg.max_iterations;
@@ -174,19 +152,22 @@ inline SolveResult run_qr(const DenseTensor& x, const SolverConfig& cfg,
     c.seed = cfg.seed;
 
     cpdb_state st{};
-    if (init) {
-        st.factors = init_f.data();
-        st.lambda = init_l.data();
+    std::vector<double> f_copy, l_copy;
+    if (init_f) {
+        f_copy = *init_f;
+        l_copy = *init_l;
+        st.factors = f_copy.data();
+        st.lambda = l_copy.data();
     }
     std::size_t nfac = 0;
-    for (const std::size_t d : x.shape().dims()) nfac += d * cfg.rank;
+    for (const std::size_t d : dims) nfac += d * cfg.rank;
     std::vector<cpdb_trace_row> rows(cfg.max_iterations);
     std::vector<double> lam(cfg.rank), fac(nfac);
     uint64_t n = 0;
     ObserverBridge bridge{&cfg};
-    abi::check(cpdb_solve(ctx, &c, init ? &st : nullptr, rows.data(), &n, lam.data(), fac.data(),
-                          nullptr, nullptr, cfg.q0_observer ? &ObserverBridge::call : nullptr,
-                          &bridge));
+    abi::check(cpdb_solve(ctx, &c, init_f ? &st : nullptr, rows.data(), &n, lam.data(),
+                          fac.data(), nullptr, nullptr,
+                          cfg.q0_observer ? &ObserverBridge::call : nullptr, &bridge));
 
     SolveResult out;
     for (uint64_t i = 0; i < n; ++i) {
@@ -205,12 +186,41 @@ inline SolveResult run_qr(const DenseTensor& x, const SolverConfig& cfg,
     }
     out.model.lambda = std::move(lam);
     std::size_t off = 0;
-    for (const std::size_t d : x.shape().dims()) {
+    for (const std::size_t d : dims) {
         out.model.factors.emplace_back(
             d, cfg.rank, std::vector<double>(fac.begin() + off, fac.begin() + off + d * cfg.rank));
         off += d * cfg.rank;
     }
     return out;
+}
+
+// One solve on a private device context (run_qr, solvers.hpp:215-309).
+inline SolveResult run_qr(const DenseTensor& x, const SolverConfig& cfg,
+                          const std::optional<KruskalModel>& init, bool extrapolate) {
+    cfg.validate();
+    const std::size_t order = x.order();
+    if (order < 2) throw std::invalid_argument("cp_als_qr: tensor order must be >= 2");
+    for (std::size_t k = 0; k < order; ++k)
+        if (cfg.rank > x.shape().extent(k))
+            throw std::invalid_argument(
+                "cp_als_qr: rank must not exceed any mode extent (compact QR)");
+    std::vector<double> init_f, init_l;
+    if (init) {
+        for (const Matrix& f : initial_factors(x, cfg, init))
+            init_f.insert(init_f.end(), f.values().begin(), f.values().end());
+        init_l = initial_lambda(init, cfg.rank);
+    }
+    cpdb_ctx* ctx = nullptr;
+    const char* env = std::getenv("CPD_DEVICE");
+    abi::check(cpdb_create(env ? std::atoi(env) : 0, &ctx));
+    struct Guard {
+        cpdb_ctx* c;
+        ~Guard() { cpdb_destroy(c); }
+    } guard{ctx};
+    const std::vector<uint64_t> dims = abi::u64(x.shape().dims());
+    abi::check(cpdb_tensor_set(ctx, x.data(), dims.data(), uint32_t(order)));
+    return run_on_context(ctx, x.shape().dims(), cfg, init ? &init_f : nullptr,
+                          init ? &init_l : nullptr, extrapolate);
 }
 
 }  // namespace detail

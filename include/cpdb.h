@@ -40,6 +40,8 @@ extern "C" {
 #define CPDB_CUDA_ERROR 5           /* device / driver failure (no fallback)        */
 #define CPDB_NCCL_ERROR 6
 #define CPDB_OUT_OF_MEMORY 7
+#define CPDB_FILE_ERROR 8           /* file_error   io.hpp:21-23 (open/read/write)  */
+#define CPDB_FORMAT_ERROR 9         /* format_error io.hpp:25-27 (malformed file)   */
 
 #define CPDB_MAX_ORDER 8
 #define CPDB_ROOT_KEY 0xFFFFFFFFu   /* "the input tensor X" as a step source       */
@@ -149,6 +151,16 @@ int cpdb_tensor_set_device(cpdb_ctx* ctx, const double* device_ptr, const uint64
 int cpdb_tensor_synth(cpdb_ctx* ctx, int32_t kind, const uint64_t* dims, uint32_t order,
                       uint64_t rank, double rho, uint64_t seed);
 int cpdb_tensor_get(cpdb_ctx* ctx, double* host);
+/* .cpdt tensor files (io.hpp:93-121: "CPDT", u8 version 1, u8 order, u64
+ * extents, f64 values little-endian, row-major).  load streams the payload
+ * straight into HBM through pinned double-buffered chunks (a sharded context
+ * reads only its mode-0 slab) and rejects what decode_tensor rejects (bad
+ * magic / version / extent, truncated or trailing bytes, non-finite values)
+ * with CPDB_FORMAT_ERROR; save writes an unsharded context's X. */
+int cpdb_tensor_load_cpdt(cpdb_ctx* ctx, const char* path);
+int cpdb_tensor_save_cpdt(cpdb_ctx* ctx, const char* path);
+/* Header only: order and extents (dims holds CPDB_MAX_ORDER entries). */
+int cpdb_cpdt_info(const char* path, uint32_t* order, uint64_t* dims);
 /* ||X||^2 (tensor.hpp:394-399 inner(x, x)), deterministic reduction */
 int cpdb_tensor_norm_sq(cpdb_ctx* ctx, double* out);
 

@@ -153,6 +153,38 @@ class Oracle:
         if rc != 0:
             raise OracleError(rc, self._f("last_error")().decode())
 
+    # ---- .cpdt files (reference codec; kind "reference" only) -------------
+    def write_tensor_file(self, path: str, x: np.ndarray) -> None:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        d = np.asarray(x.shape, dtype=np.uint64)
+        self._check(self._f("write_tensor_file")(os.fsencode(path), _dp(x),
+                                                  d.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                                  C.c_uint32(x.ndim)))
+
+    def read_tensor_file(self, path: str, cap: int = 1 << 26):
+        """-> (rc, array or None); rc 8 file_error, 9 format_error"""
+        order = C.c_uint32()
+        dims = np.zeros(8, dtype=np.uint64)
+        out = np.empty(cap)
+        rc = self._f("read_tensor_file")(os.fsencode(path), C.byref(order),
+                                         dims.ctypes.data_as(C.POINTER(C.c_uint64)), _dp(out),
+                                         C.c_uint64(cap))
+        if rc != 0:
+            return rc, None
+        shape = [int(v) for v in dims[: order.value]]
+        return 0, out[: int(np.prod(shape))].reshape(shape).copy()
+
+    def assemble_noisy(self, dims, rank, collinearity, l1, l2, seed) -> np.ndarray:
+        """reference synth.hpp:80-106 (kind "reference" only)"""
+        d = np.asarray(dims, dtype=np.uint64)
+        c = np.ascontiguousarray(collinearity, dtype=np.float64)
+        out = np.empty(int(np.prod(dims)))
+        self._check(self._f("assemble_noisy")(d.ctypes.data_as(C.POINTER(C.c_uint64)),
+                                              C.c_uint32(len(dims)), C.c_uint64(rank), _dp(c),
+                                              C.c_double(l1), C.c_double(l2),
+                                              C.c_uint64(seed), _dp(out)))
+        return out.reshape([int(v) for v in dims])
+
     # ---- primitives -------------------------------------------------------
     def rng_normals(self, seed: int, n: int) -> np.ndarray:
         out = np.empty(n)

@@ -39,6 +39,8 @@
 
 #include "cpd/dim_tree.hpp"
 #include "cpd/factor_state.hpp"
+#include "cpd/io.hpp"
+#include "cpd/synth.hpp"
 #include "cpd/kruskal.hpp"
 #include "cpd/linalg.hpp"
 #include "cpd/rng.hpp"
@@ -595,6 +597,59 @@ int cpdref_synth_baseline(int32_t kind, const uint64_t* dims, uint32_t order, ui
                 p += f.size();
             }
         }
+    });
+}
+
+// ---- .cpdt files through the reference's own codec (io.hpp:93-121, 176-209) ----
+// 8 = file_error, 9 = format_error (the CLI's exit codes 2 / 3 distinguish them)
+int cpdref_write_tensor_file(const char* path, const double* data, const uint64_t* dims,
+                             uint32_t order) {
+    try {
+        cpd::write_tensor_file(path, make_tensor(data, dims, order));
+        return kOk;
+    } catch (const cpd::file_error& e) {
+        g_error = e.what();
+        return 8;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return kOther;
+    }
+}
+
+int cpdref_read_tensor_file(const char* path, uint32_t* order, uint64_t* dims, double* out,
+                            uint64_t cap) {
+    try {
+        const cpd::DenseTensor t = cpd::read_tensor_file(path);
+        *order = uint32_t(t.order());
+        for (std::size_t k = 0; k < t.order() && k < 8; ++k) dims[k] = t.shape().extent(k);
+        if (out && t.size() <= cap) std::memcpy(out, t.data(), t.size() * sizeof(double));
+        return kOk;
+    } catch (const cpd::file_error& e) {
+        g_error = e.what();
+        return 8;
+    } catch (const cpd::format_error& e) {
+        g_error = e.what();
+        return 9;
+    } catch (const std::exception& e) {
+        g_error = e.what();
+        return kOther;
+    }
+}
+
+// ---- the reference's synthetic generator (synth.hpp:80-106, CLI `synth`) ----
+int cpdref_assemble_noisy(const uint64_t* dims, uint32_t order, uint64_t rank,
+                          const double* collinearity, double l1, double l2, uint64_t seed,
+                          double* out) {
+    return guarded([&] {
+        cpd::SynthSpec spec;
+        spec.dims = make_shape(dims, order);
+        spec.true_rank = rank;
+        spec.collinearity.assign(collinearity, collinearity + order);
+        spec.l1 = l1;
+        spec.l2 = l2;
+        spec.seed = seed;
+        const cpd::SynthResult r = cpd::assemble_noisy_tensor(spec);
+        std::memcpy(out, r.tensor.data(), r.tensor.size() * sizeof(double));
     });
 }
 

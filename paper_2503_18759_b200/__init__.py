@@ -9,6 +9,7 @@ and there is no CPU fallback: a missing library or GPU raises.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 from typing import Callable, Dict, List, Optional, Sequence, Tuple
 
@@ -58,6 +59,14 @@ class CudaError(CpdError):
     pass
 
 
+class FileError(CpdError, OSError):
+    """io.hpp:21-23 file_error (cannot open / read / write)"""
+
+
+class FormatError(CpdError):
+    """io.hpp:25-27 format_error (malformed .cpdt payload)"""
+
+
 def _lib():
     return _cpdb.load()
 
@@ -74,6 +83,10 @@ def _raise(rc: int, column: int = -1):
         raise SingularTriangularError(rc, msg, column)
     if rc == _cpdb.LOGIC_ERROR:
         raise CpdLogicError(rc, msg)
+    if rc == _cpdb.FILE_ERROR:
+        raise FileError(rc, msg)
+    if rc == _cpdb.FORMAT_ERROR:
+        raise FormatError(rc, msg)
     raise CudaError(rc, msg)
 
 
@@ -162,6 +175,15 @@ class Context:
         d = _u64(dims)
         _raise(_lib().cpdb_tensor_synth(self._h, kind, _up(d), len(d), rank, rho, seed))
         self.dims = [int(v) for v in d]
+
+    def load_tensor(self, path: str):
+        """Stream a .cpdt file (io.hpp:93-121) straight into HBM; a sharded
+        context reads only its mode-0 slab."""
+        _raise(_lib().cpdb_tensor_load_cpdt(self._h, os.fsencode(path)))
+        self.dims = cpdt_info(path)
+
+    def save_tensor(self, path: str):
+        _raise(_lib().cpdb_tensor_save_cpdt(self._h, os.fsencode(path)))
 
     def get_tensor(self, local_dims: Sequence[int]) -> np.ndarray:
         out = np.empty([int(v) for v in local_dims])
@@ -633,6 +655,14 @@ def retained_keys(s: Schedule, iteration: int, block: int) -> List[int]:
                                      s.num_iterations(), s.cycle_start, s.cycle_length, iteration,
                                      block, keys, 256, C.byref(n)))
     return [int(keys[i]) for i in range(n.value)]
+
+
+def cpdt_info(path: str) -> List[int]:
+    """Extents from a .cpdt header (host only, no device)."""
+    order = C.c_uint32()
+    dims = np.zeros(8, dtype=np.uint64)
+    _raise(_lib().cpdb_cpdt_info(os.fsencode(path), C.byref(order), _up(dims)))
+    return [int(v) for v in dims[: order.value]]
 
 
 def measured_cost(order: int, strategy, dims: Sequence[int], rank: int,

@@ -16,7 +16,7 @@ MAX_ORDER = 8
 ROOT_KEY = 0xFFFFFFFF
 
 OK, INVALID_ARGUMENT, STALE_INTERMEDIATE, SINGULAR_TRIANGULAR, LOGIC_ERROR, CUDA_ERROR, \
-    NCCL_ERROR, OUT_OF_MEMORY = range(8)
+    NCCL_ERROR, OUT_OF_MEMORY, FILE_ERROR, FORMAT_ERROR = range(10)
 
 
 class TraceRow(C.Structure):
@@ -106,6 +106,9 @@ SIGNATURES = {
     "cpdb_tensor_synth": (C.c_int, [CTX, C.c_int32, U64P, C.c_uint32, C.c_uint64, C.c_double,
                                     C.c_uint64]),
     "cpdb_tensor_get": (C.c_int, [CTX, P]),
+    "cpdb_tensor_load_cpdt": (C.c_int, [CTX, C.c_char_p]),
+    "cpdb_tensor_save_cpdt": (C.c_int, [CTX, C.c_char_p]),
+    "cpdb_cpdt_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint32), U64P]),
     "cpdb_tensor_norm_sq": (C.c_int, [CTX, P]),
     "cpdb_solve": (C.c_int, [CTX, C.POINTER(Config), C.POINTER(State), C.POINTER(TraceRow), U64P,
                              P, P, P, P, Q0Observer, C.c_void_p]),

@@ -11,6 +11,7 @@
 #include <vector>
 
 #include "comm.hpp"
+#include "cpdt.hpp"
 #include "cpdb.h"
 #include "kernels.hpp"
 #include "prims.hpp"
@@ -232,6 +233,45 @@ int cpdb_tensor_set(cpdb_ctx* c, const double* host, const uint64_t* dims, uint3
         upload(c, d, host, n);
         CPDB_CK(cudaStreamSynchronize(c->stream));
         c->x = d;
+    });
+}
+
+int cpdb_tensor_load_cpdt(cpdb_ctx* c, const char* path) {
+    return guarded([&] {
+        use_device(c);
+        if (!path) fail(CPDB_INVALID_ARGUMENT, "tensor_load: null path");
+        const cpdb::CpdtHeader h = cpdb::read_cpdt_header(path);
+        if (h.dims.size() > CPDB_MAX_ORDER)
+            fail(CPDB_INVALID_ARGUMENT, "tensor_load: order above 8 is not supported");
+        set_local_geometry(c, h.dims);
+        const uint64_t n = cpdb::numel(c->ldims);
+        double* d = c->xown.ensure(n);
+        // this rank's contiguous mode-0 slab: rows [row_begin, row_begin + rows)
+        const uint64_t inner = n / c->ldims[0];
+        cpdb::file_to_device(path, h.payload_offset + 8 * c->row_begin * inner, 8 * n, d,
+                             c->stream);
+        if (cpdb::count_nonfinite(d, n, c->stream) != 0)
+            fail(CPDB_FORMAT_ERROR, "tensor payload contains a non-finite value");
+        c->x = d;
+    });
+}
+
+int cpdb_tensor_save_cpdt(cpdb_ctx* c, const char* path) {
+    return guarded([&] {
+        use_device(c);
+        if (!path) fail(CPDB_INVALID_ARGUMENT, "tensor_save: null path");
+        if (!c->x) fail(CPDB_LOGIC_ERROR, "tensor_save: no tensor");
+        if (c->world > 1) fail(CPDB_INVALID_ARGUMENT, "tensor_save: sharded context");
+        cpdb::device_to_cpdt(path, c->dims, c->x, cpdb::numel(c->dims), c->stream);
+    });
+}
+
+int cpdb_cpdt_info(const char* path, uint32_t* order, uint64_t* dims) {
+    return guarded([&] {
+        if (!path || !order || !dims) fail(CPDB_INVALID_ARGUMENT, "cpdt_info: null argument");
+        const cpdb::CpdtHeader h = cpdb::read_cpdt_header(path);
+        *order = uint32_t(h.dims.size());
+        for (size_t k = 0; k < h.dims.size() && k < CPDB_MAX_ORDER; ++k) dims[k] = h.dims[k];
     });
 }
 

@@ -5,7 +5,9 @@
 #include <algorithm>
 
 #include "device.cuh"
+#include "cpdt.hpp"
 #include "prims.hpp"
+#include "runtime.hpp"
 
 namespace cpdb {
 namespace {
@@ -186,6 +188,30 @@ cudaError_t fitness_dev(double nx2, const double* v, const double* ah, uint64_t 
                         double* out4, cudaStream_t s) {
     fitness_kernel<<<1, 256, 0, s>>>(nx2, v, ah, rows, r0, rn, lam, r, out4);
     return cudaGetLastError();
+}
+
+namespace {
+__global__ void nonfinite_kernel(const double* x, uint64_t n, unsigned long long* out) {
+    unsigned long long c = 0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x)
+        c += isfinite(x[i]) ? 0ull : 1ull;
+    for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(out, c);  // integer: order-free
+}
+}  // namespace
+
+uint64_t count_nonfinite(const double* x, uint64_t n, cudaStream_t s) {
+    unsigned long long* d = nullptr;
+    unsigned long long h = 0;
+    CPDB_CK(cudaMallocAsync(&d, sizeof h, s));
+    CPDB_CK(cudaMemsetAsync(d, 0, sizeof h, s));
+    nonfinite_kernel<<<1184, 256, 0, s>>>(x, n, d);
+    CPDB_CK(cudaGetLastError());
+    CPDB_CK(cudaMemcpyAsync(&h, d, sizeof h, cudaMemcpyDeviceToHost, s));
+    CPDB_CK(cudaFreeAsync(d, s));
+    CPDB_CK(cudaStreamSynchronize(s));
+    return h;
 }
 
 }  // namespace cpdb
