@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
     Smem<RM> S(sm, R);
     double* scratch = S.w + per * ld;
     const int grp = threadIdx.x / T, q = threadIdx.x % T;
+    pdl_entry();
     CPDB_TS(0);
 
     double xk_part = 0.0;
@@ -312,6 +313,7 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
                                                                       : uint64_t(per))
                                       : 0);
     Smem<RM> S(sm, R);
+    pdl_entry();
     double* mats = S.w + per * ld;  // nm x R x R (after the R x R scratch)
     mats += R * R;
     const int grp = threadIdx.x / T, q = threadIdx.x % T;
@@ -393,7 +395,8 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
 }
 
 template <class Arg>
-cudaError_t launch_cluster(void (*kern)(Arg), size_t smem, cudaStream_t s, const Arg& arg) {
+cudaError_t launch_cluster(void (*kern)(Arg), size_t smem, cudaStream_t s, const Arg& arg,
+                           bool pdl) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          220 * 1024);
     if (e != cudaSuccess) return e;
@@ -402,13 +405,15 @@ cudaError_t launch_cluster(void (*kern)(Arg), size_t smem, cudaStream_t s, const
     c.blockDim = dim3(kNT, 1, 1);
     c.dynamicSmemBytes = smem;
     c.stream = s;
-    cudaLaunchAttribute attr[1];
+    cudaLaunchAttribute attr[2];
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = kCS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
     c.attrs = attr;
-    c.numAttrs = 1;
+    c.numAttrs = pdl ? 2 : 1;
     return cudaLaunchKernelEx(&c, kern, arg);
 }
 
@@ -440,10 +445,10 @@ cudaError_t launch_finish_cluster(const FinishArgs& a, cudaStream_t s) {
     const size_t smem = finish_cluster_smem(a.I, a.R);
     if (smem > 220 * 1024) return cudaErrorInvalidValue;
     switch (rm_of(a.R)) {
-        case 8: return launch_cluster<FinishArgs>(finish_cluster_kernel<8>, smem, s, a);
-        case 16: return launch_cluster<FinishArgs>(finish_cluster_kernel<16>, smem, s, a);
-        case 32: return launch_cluster<FinishArgs>(finish_cluster_kernel<32>, smem, s, a);
-        default: return launch_cluster<FinishArgs>(finish_cluster_kernel<64>, smem, s, a);
+        case 8: return launch_cluster<FinishArgs>(finish_cluster_kernel<8>, smem, s, a, true);
+        case 16: return launch_cluster<FinishArgs>(finish_cluster_kernel<16>, smem, s, a, true);
+        case 32: return launch_cluster<FinishArgs>(finish_cluster_kernel<32>, smem, s, a, true);
+        default: return launch_cluster<FinishArgs>(finish_cluster_kernel<64>, smem, s, a, true);
     }
 }
 
@@ -463,10 +468,10 @@ bool zqr_cluster_fits(uint64_t zrows, uint32_t R, uint32_t nm) {
 cudaError_t launch_zqr_cluster(const ZqrArgs& a, cudaStream_t s) {
     const size_t smem = zqr_cluster_smem(a.zrows, a.R, a.nm);
     switch (rm_of(a.R)) {
-        case 8: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<8>, smem, s, a);
-        case 16: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<16>, smem, s, a);
-        case 32: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<32>, smem, s, a);
-        default: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<64>, smem, s, a);
+        case 8: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<8>, smem, s, a, false);
+        case 16: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<16>, smem, s, a, false);
+        case 32: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<32>, smem, s, a, false);
+        default: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<64>, smem, s, a, false);
     }
 }
 

@@ -43,6 +43,21 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 __host__ __device__ inline uint32_t ttm_rpad_dev(uint32_t R) { return ((R + 7) / 8) * 8; }
 
+// Programmatic dependent launch (PDL).  Hot-path kernels are launched with
+// programmatic stream serialisation (launch_pdl / launch_cluster): the next
+// kernel on the stream is scheduled while this one runs, and every kernel
+// starts with pdl_wait() -- it returns once the previous grid has completed
+// and its writes are visible (immediately when launched without PDL) -- then
+// pdl_launch_dependents() lets the following kernel's launch overlap it.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_entry() {
+    pdl_wait();
+    pdl_launch_dependents();
+}
+
 __device__ __forceinline__ uint64_t globaltimer() {
     uint64_t t;
     asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -11,6 +11,7 @@
 #include <cmath>
 
 #include "kernels.hpp"
+#include "launch.hpp"
 #include "rowalg.cuh"
 
 namespace cpdb {
@@ -55,6 +56,7 @@ constexpr int kVBK = 16;  // k per smem tile
 template <int RM, bool DUAL>
 __global__ void __launch_bounds__(kVThreads)
 vgemm_kernel(VgemmArgs a, uint64_t kchunk) {
+    pdl_entry();
     __shared__ double yt[kVBI][kVBK + 1];
     __shared__ double pt[kVBK][RM];
     __shared__ double ft[DUAL ? kVBK : 1][RM];
@@ -232,6 +234,7 @@ householder_kernel(const double* a, uint64_t m, uint32_t n, double* work, double
 
 __global__ void reduce_splits_kernel(const double* part, uint32_t nsplit, uint64_t n,
                                      double* out) {
+    pdl_entry();
     for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < n;
          e += uint64_t(gridDim.x) * blockDim.x) {
         double s = 0.0;
@@ -259,6 +262,8 @@ cudaError_t vgemm_run(VgemmArgs& a, cudaStream_t s, int sms) {
     nsplit = (K + kchunk - 1) / kchunk;
     a.nsplit = uint32_t(nsplit);
     const dim3 grid{unsigned(iblocks), unsigned(nsplit), 1u};
+    // plain launch: V waits on the Z-QR's event (side stream), which
+    // programmatic serialisation must not relax
     vgemm_kernel<RM, DUAL><<<grid, kVThreads, 0, s>>>(a, kchunk);
     return cudaGetLastError();
 }
@@ -290,8 +295,8 @@ cudaError_t launch_vgemm(VgemmArgs& a, cudaStream_t s, int sms) {
 cudaError_t reduce_splits(const double* part, uint32_t nsplit, uint64_t n, double* out,
                           cudaStream_t s) {
     const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, 1024));
-    reduce_splits_kernel<<<std::max(grid, 1u), 256, 0, s>>>(part, nsplit, n, out);
-    return cudaGetLastError();
+    return launch_pdl(reduce_splits_kernel, dim3(std::max(grid, 1u)), dim3(256), 0, s, part,
+                      nsplit, n, out);
 }
 
 cudaError_t normalize_exact(double* a, uint64_t m, uint32_t n, double* weights, cudaStream_t s) {

@@ -25,6 +25,7 @@
 
 #include "device.cuh"
 #include "kernels.hpp"
+#include "launch.hpp"
 
 namespace cpdb {
 namespace {
@@ -50,6 +51,7 @@ __global__ void __launch_bounds__(kThreads)
 ttm_dmma_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qp,
                 uint64_t outer, uint64_t K, uint64_t inner, uint32_t R, uint64_t ntiles,
                 uint32_t nk) {
+    pdl_entry();
     using C = TtmCfg<RB, CB, BK, STAGES, LAYOUT>;
     extern __shared__ __align__(128) double smem[];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -199,6 +201,7 @@ ttm_dmma_kernel(const double* __restrict__ x, double* __restrict__ y, const doub
 __global__ void ttm_simple_kernel(const double* __restrict__ x, double* __restrict__ y,
                                   const double* __restrict__ q, uint64_t outer, uint64_t K,
                                   uint64_t inner, uint32_t R) {
+    pdl_entry();
     const uint64_t n = outer * R * inner;
     for (uint64_t idx = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; idx < n;
          idx += uint64_t(gridDim.x) * blockDim.x) {
@@ -213,6 +216,7 @@ __global__ void ttm_simple_kernel(const double* __restrict__ x, double* __restri
 // Q (K x R row-major) -> [Kpad/4][Rp][4] fragment order, zero padded.
 __global__ void pack_q_kernel(const double* __restrict__ q, double* __restrict__ qp, uint32_t K,
                               uint32_t R, uint32_t Kpad, uint32_t Rp) {
+    pdl_entry();
     const uint32_t n = Kpad * Rp;
     for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n;
          idx += gridDim.x * blockDim.x) {
@@ -241,9 +245,8 @@ cudaError_t launch_cfg(const TtmArgs& a, cudaStream_t s, int sms) {
     per_sm = std::max(per_sm, 1);
     const uint64_t grid = std::min<uint64_t>(ntiles, uint64_t(sms) * per_sm);
     if (grid == 0) return cudaSuccess;
-    kern<<<static_cast<unsigned>(grid), kThreads, C::SMEM, s>>>(a.x, a.y, a.qp, a.outer, a.K,
-                                                                a.inner, a.R, ntiles, nk);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(kThreads), C::SMEM, s, a.x,
+                      a.y, a.qp, a.outer, a.K, a.inner, a.R, ntiles, nk);
 }
 
 // Tile shapes per padded rank: RB*CB accumulator tiles per warp <= 16, and an
@@ -271,8 +274,8 @@ uint32_t ttm_rpad(uint32_t R) { return ((R + 7) / 8) * 8; }
 cudaError_t pack_q(const double* q, double* qp, uint32_t K, uint32_t R, cudaStream_t s) {
     const uint32_t Kpad = ttm_kpad(K), Rp = ttm_rpad(R);
     const uint32_t n = Kpad * Rp;
-    pack_q_kernel<<<(n + 255) / 256, 256, 0, s>>>(q, qp, K, R, Kpad, Rp);
-    return cudaGetLastError();
+    return launch_pdl(pack_q_kernel, dim3((n + 255) / 256), dim3(256), 0, s, q, qp, K, R, Kpad,
+                      Rp);
 }
 
 TtmPath ttm_path(const TtmArgs& a) {
@@ -297,9 +300,8 @@ cudaError_t launch_ttm(const TtmArgs& a, cudaStream_t s, int sms) {
         case TtmPath::simple: {
             const uint64_t n = a.outer * a.R * a.inner;
             const unsigned grid = static_cast<unsigned>(std::min<uint64_t>((n + 255) / 256, 4096));
-            ttm_simple_kernel<<<std::max(grid, 1u), 256, 0, s>>>(a.x, a.y, a.q, a.outer, a.K,
-                                                                 a.inner, a.R);
-            return cudaGetLastError();
+            return launch_pdl(ttm_simple_kernel, dim3(std::max(grid, 1u)), dim3(256), 0, s, a.x,
+                              a.y, a.q, a.outer, a.K, a.inner, a.R);
         }
     }
     return cudaErrorInvalidValue;

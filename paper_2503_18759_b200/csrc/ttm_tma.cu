@@ -26,6 +26,7 @@
 
 #include "device.cuh"
 #include "kernels.hpp"
+#include "launch.hpp"
 
 namespace cpdb {
 namespace {
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(Cfg<RB, CB, BK, STAGES, NC, LAYOUT>::NT, 1)
 ttm_tma_kernel(const __grid_constant__ CUtensorMap xmap, double* __restrict__ y,
                const double* __restrict__ qp, uint64_t outer, uint64_t K, uint64_t inner,
                uint32_t R, uint64_t ntiles, uint32_t nk) {
+    pdl_entry();
     using C = Cfg<RB, CB, BK, STAGES, NC, LAYOUT>;
     extern __shared__ __align__(128) double smem[];
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * C::STAGE);
@@ -310,9 +312,8 @@ cudaError_t launch_v2(const TtmArgs& a, cudaStream_t s, int sms) {
     const uint32_t nk = static_cast<uint32_t>((a.K + BK - 1) / BK);
     const uint64_t grid = std::min<uint64_t>(ntiles, uint64_t(sms));
     if (grid == 0) return cudaSuccess;
-    kern<<<unsigned(grid), C::NT, C::SMEM, s>>>(map, a.y, a.qp, a.outer, a.K, a.inner, a.R, ntiles,
-                                               nk);
-    return cudaGetLastError();
+    return launch_pdl(kern, dim3(unsigned(grid)), dim3(C::NT), C::SMEM, s, map, a.y, a.qp, a.outer,
+                      a.K, a.inner, a.R, ntiles, nk);
 }
 
 // Tiles a launch would have with CB column blocks per consumer warp.
