@@ -114,41 +114,51 @@ ttm_tma_kernel(const __grid_constant__ CUtensorMap xmap, double* __restrict__ y,
     __syncthreads();
 
     const uint64_t first = blockIdx.x;
-    const uint64_t my_tiles = first < ntiles ? (ntiles - 1 - first) / gridDim.x + 1 : 0;
-    const uint64_t total = my_tiles * nk;
     const uint64_t gpo = inner / 8;  // 8-column groups per o (kGroups)
+    // (tile, k-block) walk with a running ring slot and phase: no 64-bit
+    // division on the per-stage path
 
     if (warp == NC) {
         // ===================== producer: one elected lane issues TMA
         if (lane == 0) {
-            for (uint64_t t = 0; t < total; ++t) {
-                const int st = int(t % STAGES);
-                const uint32_t ph = uint32_t((t / STAGES) & 1);
-                mbar_wait(&empty[st], ph ^ 1);
-                const uint64_t tile = first + (t / nk) * gridDim.x;
-                const int k0 = int((t % nk) * BK);
-                double* sx = smem + st * C::STAGE;
-                double* sq = sx + C::XS;
-                mbar_expect_tx(&full[st], uint32_t(C::STAGE * sizeof(double)));
+            int st = 0;
+            uint32_t ph = 0;
+            for (uint64_t tile = first; tile < ntiles; tile += gridDim.x) {
+                uint64_t g0 = tile * C::G, go = 0, gi = 0;  // kGroups: (o, group-in-o)
                 if (LAYOUT == kGroups) {
-                    const uint64_t g0 = tile * C::G;  // first flat 8-group of the tile
-                    if (gpo >= uint64_t(C::G)) {
-                        tma_4d(sx, &xmap, &full[st], 0, k0, int(g0 % gpo), int(g0 / gpo));
-                    } else {
-                        tma_4d(sx, &xmap, &full[st], 0, k0, 0, int(g0 / gpo));
-                    }
-                } else if constexpr (C::BJ <= 256) {
-                    tma_3d(sx, &xmap, &full[st], 0, int(tile * C::BJ), k0 / 4);
-                } else {
-                    // box rows are capped at 256: one box per (k-quad, 256 rows)
-#pragma unroll
-                    for (int s = 0; s < BK / 4; ++s)
-#pragma unroll
-                        for (int h = 0; h < C::BJ / 256; ++h)
-                            tma_3d(sx + (s * C::BJ + h * 256) * 4, &xmap, &full[st], 0,
-                                   int(tile * C::BJ + h * 256), k0 / 4 + s);
+                    go = g0 / gpo;
+                    gi = g0 % gpo;
                 }
-                bulk_copy(sq, qp + size_t(k0) * C::Rp, uint32_t(C::QS * sizeof(double)), &full[st]);
+                for (uint32_t kb = 0; kb < nk; ++kb) {
+                    mbar_wait(&empty[st], ph ^ 1);
+                    const int k0 = int(kb * BK);
+                    double* sx = smem + st * C::STAGE;
+                    double* sq = sx + C::XS;
+                    mbar_expect_tx(&full[st], uint32_t(C::STAGE * sizeof(double)));
+                    if (LAYOUT == kGroups) {
+                        if (gpo >= uint64_t(C::G)) {
+                            tma_4d(sx, &xmap, &full[st], 0, k0, int(gi), int(go));
+                        } else {
+                            tma_4d(sx, &xmap, &full[st], 0, k0, 0, int(go));
+                        }
+                    } else if constexpr (C::BJ <= 256) {
+                        tma_3d(sx, &xmap, &full[st], 0, int(tile * C::BJ), k0 / 4);
+                    } else {
+                        // box rows are capped at 256: one box per (k-quad, 256 rows)
+#pragma unroll
+                        for (int s = 0; s < BK / 4; ++s)
+#pragma unroll
+                            for (int h = 0; h < C::BJ / 256; ++h)
+                                tma_3d(sx + (s * C::BJ + h * 256) * 4, &xmap, &full[st], 0,
+                                       int(tile * C::BJ + h * 256), k0 / 4 + s);
+                    }
+                    bulk_copy(sq, qp + size_t(k0) * C::Rp, uint32_t(C::QS * sizeof(double)),
+                              &full[st]);
+                    if (++st == STAGES) {
+                        st = 0;
+                        ph ^= 1;
+                    }
+                }
             }
         }
         return;
@@ -161,79 +171,84 @@ ttm_tma_kernel(const __grid_constant__ CUtensorMap xmap, double* __restrict__ y,
 #pragma unroll
         for (int b = 0; b < CB; ++b) acc[a][b][0] = acc[a][b][1] = 0.0;
 
-    for (uint64_t t = 0; t < total; ++t) {
-        const int st = int(t % STAGES);
-        mbar_wait(&full[st], uint32_t((t / STAGES) & 1));
-        const double* sx = smem + st * C::STAGE;
-        const double* sq = sx + C::XS;
-        double qf[2][RB], xf[2][CB];
-        auto load_frags = [&](int s, int buf) {
+    int st = 0;
+    uint32_t ph = 0;
+    for (uint64_t tile = first; tile < ntiles; tile += gridDim.x) {
+#pragma unroll 1
+        for (uint32_t kb = 0; kb < nk; ++kb) {
+            mbar_wait(&full[st], ph);
+            const double* sx = smem + st * C::STAGE;
+            const double* sq = sx + C::XS;
+            double qf[2][RB], xf[2][CB];
+            auto load_frags = [&](int s, int buf) {
 #pragma unroll
-            for (int rb = 0; rb < RB; ++rb) qf[buf][rb] = sq[(s * C::Rp + rb * 8) * 4 + lane];
-#pragma unroll
-            for (int cb = 0; cb < CB; ++cb) {
-                const int g = warp * CB + cb;
-                if (LAYOUT == kGroups)
-                    xf[buf][cb] = sx[(g * BK + 4 * s + (lane & 3)) * 8 + (lane >> 2)];
-                else
-                    xf[buf][cb] = sx[(s * C::BJ + g * 8) * 4 + lane];
-            }
-        };
-        load_frags(0, 0);
-#pragma unroll
-        for (int s = 0; s < BK / 4; ++s) {
-            const int cur = s & 1;
-            if (s + 1 < BK / 4) load_frags(s + 1, cur ^ 1);
-#pragma unroll
-            for (int rb = 0; rb < RB; ++rb)
+                for (int rb = 0; rb < RB; ++rb) qf[buf][rb] = sq[(s * C::Rp + rb * 8) * 4 + lane];
 #pragma unroll
                 for (int cb = 0; cb < CB; ++cb) {
+                    const int g = warp * CB + cb;
                     if (LAYOUT == kGroups)
-                        dmma(acc[rb][cb][0], acc[rb][cb][1], qf[cur][rb], xf[cur][cb]);
+                        xf[buf][cb] = sx[(g * BK + 4 * s + (lane & 3)) * 8 + (lane >> 2)];
                     else
-                        dmma(acc[rb][cb][0], acc[rb][cb][1], xf[cur][cb], qf[cur][rb]);
+                        xf[buf][cb] = sx[(s * C::BJ + g * 8) * 4 + lane];
                 }
-        }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[st]);
-
-        if (t % nk == nk - 1) {  // tile complete: epilogue straight to HBM
-            const uint64_t tile = first + (t / nk) * gridDim.x;
+            };
+            load_frags(0, 0);
 #pragma unroll
-            for (int cb = 0; cb < CB; ++cb) {
-                const int g = warp * CB + cb;
-                if (LAYOUT == kGroups) {
-                    const uint64_t gflat = tile * C::G + g;
-                    const uint64_t o = gflat / gpo, j = (gflat % gpo) * 8 + 2 * (lane & 3);
-                    if (o < outer) {
+            for (int s = 0; s < BK / 4; ++s) {
+                const int cur = s & 1;
+                if (s + 1 < BK / 4) load_frags(s + 1, cur ^ 1);
 #pragma unroll
-                        for (int rb = 0; rb < RB; ++rb) {
-                            const uint32_t r = rb * 8 + (lane >> 2);
-                            if (r < R)
-                                *reinterpret_cast<double2*>(y + (o * R + r) * inner + j) =
-                                    make_double2(acc[rb][cb][0], acc[rb][cb][1]);
-                        }
+                for (int rb = 0; rb < RB; ++rb)
+#pragma unroll
+                    for (int cb = 0; cb < CB; ++cb) {
+                        if (LAYOUT == kGroups)
+                            dmma(acc[rb][cb][0], acc[rb][cb][1], qf[cur][rb], xf[cur][cb]);
+                        else
+                            dmma(acc[rb][cb][0], acc[rb][cb][1], xf[cur][cb], qf[cur][rb]);
                     }
-                } else {
-                    const uint64_t m = tile * C::BJ + uint64_t(g) * 8 + (lane >> 2);
-                    if (m < outer) {
-#pragma unroll
-                        for (int rb = 0; rb < RB; ++rb) {
-                            const uint32_t r = rb * 8 + 2 * (lane & 3);
-                            double* dst = y + m * R + r;
-                            if (r + 1 < R && (R % 2 == 0)) {
-                                *reinterpret_cast<double2*>(dst) =
-                                    make_double2(acc[rb][cb][0], acc[rb][cb][1]);
-                            } else {
-                                if (r < R) dst[0] = acc[rb][cb][0];
-                                if (r + 1 < R) dst[1] = acc[rb][cb][1];
-                            }
-                        }
-                    }
-                }
-#pragma unroll
-                for (int rb = 0; rb < RB; ++rb) acc[rb][cb][0] = acc[rb][cb][1] = 0.0;
             }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[st]);
+            if (++st == STAGES) {
+                st = 0;
+                ph ^= 1;
+            }
+        }
+        // tile complete: epilogue straight to HBM
+#pragma unroll
+        for (int cb = 0; cb < CB; ++cb) {
+            const int g = warp * CB + cb;
+            if (LAYOUT == kGroups) {
+                const uint64_t gflat = tile * C::G + g;
+                const uint64_t o = gflat / gpo, j = (gflat % gpo) * 8 + 2 * (lane & 3);
+                if (o < outer) {
+#pragma unroll
+                    for (int rb = 0; rb < RB; ++rb) {
+                        const uint32_t r = rb * 8 + (lane >> 2);
+                        if (r < R)
+                            *reinterpret_cast<double2*>(y + (o * R + r) * inner + j) =
+                                make_double2(acc[rb][cb][0], acc[rb][cb][1]);
+                    }
+                }
+            } else {
+                const uint64_t m = tile * C::BJ + uint64_t(g) * 8 + (lane >> 2);
+                if (m < outer) {
+#pragma unroll
+                    for (int rb = 0; rb < RB; ++rb) {
+                        const uint32_t r = rb * 8 + 2 * (lane & 3);
+                        double* dst = y + m * R + r;
+                        if (r + 1 < R && (R % 2 == 0)) {
+                            *reinterpret_cast<double2*>(dst) =
+                                make_double2(acc[rb][cb][0], acc[rb][cb][1]);
+                        } else {
+                            if (r < R) dst[0] = acc[rb][cb][0];
+                            if (r + 1 < R) dst[1] = acc[rb][cb][1];
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int rb = 0; rb < RB; ++rb) acc[rb][cb][0] = acc[rb][cb][1] = 0.0;
         }
     }
 }
@@ -360,7 +375,7 @@ cudaError_t dispatch_v2(const TtmArgs& a, cudaStream_t s, int sms) {
         case 1: return launch_adaptive<1, 8, 8, 5, LAYOUT>(a, s, sms);
         case 2: return launch_adaptive<2, 8, 8, 5, LAYOUT>(a, s, sms);
         case 3: return launch_adaptive<3, 4, 16, 5, LAYOUT>(a, s, sms);
-        case 4: return launch_adaptive<4, 4, 16, 5, LAYOUT>(a, s, sms);
+        case 4: return launch_adaptive<4, 4, 16, 6, LAYOUT>(a, s, sms);
         case 5: return launch_adaptive<5, 2, 32, 4, LAYOUT>(a, s, sms);
         case 6: return launch_adaptive<6, 2, 32, 4, LAYOUT>(a, s, sms);
         case 7: return launch_adaptive<7, 2, 32, 4, LAYOUT>(a, s, sms);
