@@ -314,6 +314,7 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
                                       : 0);
     Smem<RM> S(sm, R);
     pdl_entry();
+    CPDB_TS(0);
     double* mats = S.w + per * ld;  // nm x R x R (after the R x R scratch)
     mats += R * R;
     const int grp = threadIdx.x / T, q = threadIdx.x % T;
@@ -321,42 +322,58 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
     for (int t = 0; t < nm; ++t)
         for (int e = threadIdx.x; e < R * R; e += kNT) mats[t * R * R + e] = a.rmats[t][e];
     __syncthreads();
-    // G1 = Hadamard_t (R_t^T R_t), computed redundantly by every rank (tiny)
+    // G1 = Hadamard_t (R_t^T R_t), computed redundantly by every rank (tiny);
+    // four independent accumulators break the FMA dependency chain
     for (int e = threadIdx.x; e < R * R; e += kNT) {
         const int i = e / R, j = e % R;
         const int lo = i < j ? i : j, hi = i < j ? j : i;
         double h = 1.0;
         for (int t = nm - 1; t >= 0; --t) {
             const double* m = mats + t * R * R;
-            double s = 0.0;
-            for (int k = 0; k <= lo; ++k) s = fma(m[k * R + lo], m[k * R + hi], s);
-            h = (t == nm - 1) ? s : h * s;
+            double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+            int k = 0;
+            for (; k + 3 <= lo; k += 4) {
+                s0 = fma(m[k * R + lo], m[k * R + hi], s0);
+                s1 = fma(m[(k + 1) * R + lo], m[(k + 1) * R + hi], s1);
+                s2 = fma(m[(k + 2) * R + lo], m[(k + 2) * R + hi], s2);
+                s3 = fma(m[(k + 3) * R + lo], m[(k + 3) * R + hi], s3);
+            }
+            for (; k <= lo; ++k) s0 = fma(m[k * R + lo], m[k * R + hi], s0);
+            const double sum = (s0 + s1) + (s2 + s3);
+            h = (t == nm - 1) ? sum : h * sum;
         }
         S.g[e] = h;
     }
     __syncthreads();
+    CPDB_TS(1);
     const bool ok1 = chol<kNT, RM>(S.g, R, R);
     if (!ok1 && rank == 0 && threadIdx.x == 0) *a.status = 2;
     stage_tri<RM>(S.g, R, R, S.u, S.dinv, kNT);  // U1 (kept in S.g too)
     __syncthreads();
+    CPDB_TS(2);
     // Q1 = Z U1^-1 on this rank's rows; Z rows are generated in registers
     // (product in descending mode order like the reference Khatri-Rao fold)
     for (int li = grp; li < rows + (G - rows % G) % G; li += G) {
         const bool act = li < rows;
         Row x;
-        uint64_t rem0 = r0 + (act ? li : 0);
+        // digits of the row index (32-bit: the cluster path has R^(N-1) rows
+        // in shared memory), shared by the lane group's columns
+        int digs[8];
+        {
+            uint32_t rem = uint32_t(r0) + uint32_t(act ? li : 0);
+            for (int k = nm - 1; k >= 0; --k) {
+                const uint32_t qt = rem / uint32_t(R);
+                digs[k] = int(rem - qt * uint32_t(R));
+                rem = qt;
+            }
+        }
 #pragma unroll
         for (int s = 0; s < Row::S; ++s) {
             const int c = s * T + q;
             double z = 0.0;
             if (c < R && act) {
-                uint64_t rem = rem0;
-                for (int k = nm - 1; k >= 0; --k) {
-                    const int dig = int(rem % R);
-                    rem /= R;
-                    const double v = mats[(k * R + dig) * R + c];
-                    z = (k == nm - 1) ? v : z * v;
-                }
+                z = mats[((nm - 1) * R + digs[nm - 1]) * R + c];
+                for (int k = nm - 2; k >= 0; --k) z *= mats[(k * R + digs[k]) * R + c];
             }
             x.t[s] = z;
         }
@@ -364,8 +381,11 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
         if (act) x.store(S.w + li * ld, R, q);
     }
     __syncthreads();
+    CPDB_TS(3);
     gram_dmma<kNT>(S.w, ld, rows, R, S.p, R);
+    CPDB_TS(4);
     cl.sync();
+    CPDB_TS(5);
     if (rank == 0) {
         double* u1 = S.w + per * ld;  // keep U1 (stride R) for R0 = U2 U1
         for (int e = threadIdx.x; e < R * R; e += kNT) u1[e] = S.g[e];
@@ -376,14 +396,22 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
         if (!ok2 && threadIdx.x == 0) *a.status = 2;
         for (int e = threadIdx.x; e < R * R; e += kNT) {  // R0 = U2 U1
             const int i = e / R, j = e % R;
-            double s = 0.0;
-            for (int k = i; k <= j; ++k) s = fma(S.g[i * R + k], u1[k * R + j], s);
-            a.r0[e] = i <= j ? s : 0.0;
+            double s0 = 0.0, s1 = 0.0;
+            int k = i;
+            for (; k + 1 <= j; k += 2) {
+                s0 = fma(S.g[i * R + k], u1[k * R + j], s0);
+                s1 = fma(S.g[i * R + k + 1], u1[(k + 1) * R + j], s1);
+            }
+            if (k <= j) s0 = fma(S.g[i * R + k], u1[k * R + j], s0);
+            a.r0[e] = i <= j ? s0 + s1 : 0.0;
         }
+        CPDB_TS(6);
     }
     cl.sync();
+    CPDB_TS(7);
     stage_tri<RM>(cl.map_shared_rank(S.g, 0), R, R, S.u, S.dinv, kNT);
     __syncthreads();
+    CPDB_TS(8);
     for (int li = grp; li < rows + (G - rows % G) % G; li += G) {
         const bool act = li < rows;
         Row x;
@@ -391,7 +419,9 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
         x.uinv(S.u, S.dinv, R, q);
         if (act) x.store(a.q0 + (r0 + li) * R, R, q);
     }
+    CPDB_TS(9);
     cl.sync();
+    CPDB_TS(10);
 }
 
 template <class Arg>

@@ -44,6 +44,7 @@ struct ZqrArgs {
     double* r0;              // R x R out
     double* work;            // zqr_work_doubles(R, grid)
     int* status;             // device flag: non-zero = Cholesky breakdown
+    unsigned long long* ts;  // optional phase timestamps (profiling)
 };
 size_t zqr_work_doubles(uint32_t R);
 cudaError_t launch_zqr(const ZqrArgs& a, cudaStream_t s, int sms);

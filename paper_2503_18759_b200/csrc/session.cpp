@@ -357,10 +357,24 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     z.status = c->dstatus;
     // Z-QR depends only on R_k (k != n), final since the previous update's
     // finisher: it runs on the side stream, overlapped with the TTM chain.
+    static const bool trace_phases = std::getenv("CPDB_PHASE_TRACE") != nullptr;
+    if (trace_phases) {
+        z.ts = reinterpret_cast<unsigned long long*>(zts.ensure(32));
+        CPDB_CK(cudaMemsetAsync(z.ts, 0, 32 * sizeof(double), c->side));
+    }
     CPDB_CK(cudaEventRecord(ev_ready, s));
     CPDB_CK(cudaStreamWaitEvent(c->side, ev_ready, 0));
     CPDB_CK(launch_zqr(z, c->side, c->sms));
     CPDB_CK(cudaEventRecord(ev_zqr, c->side));
+    if (trace_phases) {
+        unsigned long long ts[32];
+        CPDB_CK(cudaMemcpyAsync(ts, z.ts, sizeof ts, cudaMemcpyDeviceToHost, c->side));
+        CPDB_CK(cudaStreamSynchronize(c->side));
+        std::fprintf(stderr, "zqr mode %u phases(us):", n);
+        for (int k = 1; k < 11; ++k)
+            std::fprintf(stderr, " %d:%.2f", k, ts[k] ? (ts[k] - ts[0]) * 1e-3 : -1.0);
+        std::fprintf(stderr, "\n");
+    }
     c->launches += 5;
     if (observer) {
         std::vector<double> nat(zrows * R), ref(zrows * R);

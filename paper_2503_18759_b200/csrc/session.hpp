@@ -34,7 +34,7 @@ struct Session {
     uint64_t launches0 = 0;
 
     std::vector<FactorBufs> fb;
-    DevBuf lam, qp0_local, tsbuf;
+    DevBuf lam, qp0_local, tsbuf, zts;
     DevBuf fscratch, vpart, vfitpart, vfull, vfitfull, vout, fitbuf, q0buf, q1buf, r0buf, zwork;
     std::vector<DevBuf> hist, ybuf;
     std::vector<bool> has_hist;
