@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <cmath>
 
+#include "device.cuh"
 #include "kernels.hpp"
 #include "launch.hpp"
 #include "rowalg.cuh"
@@ -86,8 +87,11 @@ vgemm_kernel(VgemmArgs a, uint64_t kchunk) {
             const uint64_t k = k0 + c_, i = i0 + r_;
             double v = 0.0;
             if (k < ke && i < I) {
-                const uint64_t o = k / J, j = k % J;
-                v = a.y[(o * I + i) * J + j];
+                // K = R^(N-1) < 2^32: 32-bit index math (a 64-bit division per
+                // element dominated this loop)
+                const uint32_t k32 = uint32_t(k), J32 = uint32_t(J);
+                const uint32_t o = k32 / J32, j = k32 - o * J32;
+                v = a.y[(uint64_t(o) * I + i) * J + j];
             }
             yt[r_][c_] = v;
         }
@@ -125,6 +129,127 @@ vgemm_kernel(VgemmArgs a, uint64_t kchunk) {
             if (r < R) {
                 vp[r] = acc[u];
                 if (DUAL) fp[r] = accf[u];
+            }
+        }
+    }
+}
+
+// V-GEMM on the FP64 tensor cores.  CTA = 64 rows of V x all R columns over a
+// K-chunk (split-K, partials reduced in a fixed order by reduce_splits);
+// warp w owns rows 8w..8w+7 and the Rp/8 column blocks (DMMA m8n8k4).  Y and
+// P tiles (16 k) are staged in padded shared memory (conflict-free fragment
+// reads) with the next tile prefetched into registers; the extrapolation
+// P = Q0 + beta (Q0 - alpha H) is fused into the P tile load, and the DUAL
+// variant also accumulates Y Q0 for the fitness.
+constexpr int kDM = 64, kDK = 16, kDThreads = 256;
+
+template <int RM, bool DUAL>
+__global__ void __launch_bounds__(kDThreads)
+vgemm_dmma_kernel(VgemmArgs a, uint64_t kchunk) {
+    pdl_entry();
+    constexpr int RB = RM / 8 > 0 ? RM / 8 : 1;
+    constexpr int YLD = kDK + 4;   // (m*YLD) mod 16 spaced by 4: conflict-free A reads
+    constexpr int PLD = RM + 4;    // likewise for the B reads
+    constexpr int YPT = kDM * kDK / kDThreads;  // 4 Y elements per thread
+    constexpr int PPT = (kDK * RM + kDThreads - 1) / kDThreads;
+    __shared__ double ys[kDM * YLD];
+    __shared__ double ps[kDK * PLD];
+    __shared__ double fs[DUAL ? kDK * PLD : 1];
+    const int R = a.R;
+    const uint64_t I = a.I;
+    const uint32_t J = uint32_t(a.J), K = uint32_t(a.O * a.J);
+    const uint64_t i0 = uint64_t(blockIdx.x) * kDM;
+    const uint32_t kb = uint32_t(uint64_t(blockIdx.y) * kchunk);
+    const uint32_t ke = uint32_t(min(uint64_t(K), uint64_t(kb) + kchunk));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const bool jrun = (J % kDK) == 0;  // a 16-k tile is 16 consecutive j of one o
+
+    double yr[YPT], pr[PPT], fr[DUAL ? PPT : 1];
+    auto fetch = [&](uint32_t k0) {
+#pragma unroll
+        for (int u = 0; u < YPT; ++u) {
+            const int e = threadIdx.x + u * kDThreads;
+            const int m = jrun ? e / kDK : e % kDM, c = jrun ? e % kDK : e / kDM;
+            const uint32_t k = k0 + c;
+            const uint64_t i = i0 + m;
+            double v = 0.0;
+            if (k < ke && i < I) {
+                const uint32_t o = k / J, j = k - o * J;
+                v = a.y[(uint64_t(o) * I + i) * J + j];
+            }
+            yr[u] = v;
+        }
+#pragma unroll
+        for (int u = 0; u < PPT; ++u) {
+            const int e = threadIdx.x + u * kDThreads;
+            const int kk = e / RM, r = e % RM;
+            const uint32_t k = k0 + kk;
+            double q = 0.0, p = 0.0;
+            if (e < kDK * RM && k < ke && r < R) {
+                q = a.q0[uint64_t(k) * R + r];
+                p = a.extrap ? q + a.beta * (q - a.alpha * a.hist[uint64_t(k) * R + r]) : q;
+            }
+            pr[u] = p;
+            if (DUAL) fr[u] = q;
+        }
+    };
+    auto stash = [&]() {
+#pragma unroll
+        for (int u = 0; u < YPT; ++u) {
+            const int e = threadIdx.x + u * kDThreads;
+            const int m = jrun ? e / kDK : e % kDM, c = jrun ? e % kDK : e / kDM;
+            ys[m * YLD + c] = yr[u];
+        }
+#pragma unroll
+        for (int u = 0; u < PPT; ++u) {
+            const int e = threadIdx.x + u * kDThreads;
+            if (e < kDK * RM) {
+                ps[(e / RM) * PLD + e % RM] = pr[u];
+                if (DUAL) fs[(e / RM) * PLD + e % RM] = fr[u];
+            }
+        }
+    };
+
+    double acc[RB][2], accf[DUAL ? RB : 1][2];
+#pragma unroll
+    for (int b = 0; b < RB; ++b) acc[b][0] = acc[b][1] = 0.0;
+#pragma unroll
+    for (int b = 0; b < (DUAL ? RB : 1); ++b) accf[b][0] = accf[b][1] = 0.0;
+
+    if (kb < ke) fetch(kb);
+    for (uint32_t k0 = kb; k0 < ke; k0 += kDK) {
+        stash();
+        __syncthreads();
+        if (k0 + kDK < ke) fetch(k0 + kDK);  // next tile in flight during the MMAs
+#pragma unroll
+        for (int s4 = 0; s4 < kDK / 4; ++s4) {
+            const double av = ys[(warp * 8 + (lane >> 2)) * YLD + 4 * s4 + (lane & 3)];
+#pragma unroll
+            for (int b = 0; b < RB; ++b) {
+                const double bv = ps[(4 * s4 + (lane & 3)) * PLD + b * 8 + (lane >> 2)];
+                dmma(acc[b][0], acc[b][1], av, bv);
+                if (DUAL) {
+                    const double fv = fs[(4 * s4 + (lane & 3)) * PLD + b * 8 + (lane >> 2)];
+                    dmma(accf[b][0], accf[b][1], av, fv);
+                }
+            }
+        }
+        __syncthreads();
+    }
+    const uint64_t i = i0 + warp * 8 + (lane >> 2);
+    if (i < I) {
+        double* vp = a.vpart + (uint64_t(blockIdx.y) * I + i) * R;
+        double* fp = DUAL ? a.vfitpart + (uint64_t(blockIdx.y) * I + i) * R : nullptr;
+#pragma unroll
+        for (int b = 0; b < RB; ++b) {
+            const int r = b * 8 + 2 * (lane & 3);
+            if (r < R) {
+                vp[r] = acc[b][0];
+                if (DUAL) fp[r] = accf[b][0];
+            }
+            if (r + 1 < R) {
+                vp[r + 1] = acc[b][1];
+                if (DUAL) fp[r + 1] = accf[b][1];
             }
         }
     }
@@ -254,6 +379,20 @@ __global__ void permute_rows_kernel(const double* in, double* out, const uint64_
 template <int RM, bool DUAL>
 cudaError_t vgemm_run(VgemmArgs& a, cudaStream_t s, int sms) {
     const uint64_t K = a.O * a.J;
+    if (RM >= 8 && K < (1ull << 32)) {  // DMMA path
+        const uint64_t iblocks = (a.I + kDM - 1) / kDM;
+        const uint64_t ktiles = (K + kDK - 1) / kDK;
+        uint64_t nsplit = std::max<uint64_t>(1, (2 * uint64_t(sms)) / iblocks);
+        nsplit = std::min<uint64_t>({nsplit, ktiles, uint64_t(vgemm_max_split())});
+        const uint64_t kchunk = ((ktiles + nsplit - 1) / nsplit) * kDK;
+        nsplit = (K + kchunk - 1) / kchunk;
+        a.nsplit = uint32_t(nsplit);
+        const dim3 grid{unsigned(iblocks), unsigned(nsplit), 1u};
+        // plain launch: V waits on the Z-QR's event (side stream), which
+        // programmatic serialisation must not relax
+        vgemm_dmma_kernel<RM, DUAL><<<grid, kDThreads, 0, s>>>(a, kchunk);
+        return cudaGetLastError();
+    }
     const uint64_t iblocks = (a.I + kVBI - 1) / kVBI;
     const uint64_t ktiles = (K + kVBK - 1) / kVBK;
     uint64_t nsplit = std::max<uint64_t>(1, (2 * uint64_t(sms)) / iblocks);
