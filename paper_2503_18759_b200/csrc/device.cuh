@@ -43,6 +43,18 @@ __device__ __forceinline__ double warp_sum(double v) {
 
 __host__ __device__ inline uint32_t ttm_rpad_dev(uint32_t R) { return ((R + 7) / 8) * 8; }
 
+// Branch-free double reciprocal: MUFU approximation + two Newton steps
+// (error <= 1 ulp; __drcp_rn's IEEE path carries a slow-path branch that
+// keeps the scheduler from overlapping independent loads with it).
+__device__ __forceinline__ double rcp_nr(double d) {
+    double r;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+    double e = fma(-d, r, 1.0);
+    r = fma(r, e, r);
+    e = fma(-d, r, 1.0);
+    return fma(r, e, r);
+}
+
 // Programmatic dependent launch (PDL).  Hot-path kernels are launched with
 // programmatic stream serialisation (launch_pdl / launch_cluster): the next
 // kernel on the stream is scheduled while this one runs, and every kernel

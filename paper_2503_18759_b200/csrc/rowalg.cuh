@@ -222,12 +222,9 @@ __device__ bool block_chol(double* g, int ld, int R) {
     }
     bool ok = true;
     for (int j = 0; j < R; ++j) {
+        // every load of the step first (they only depend on the barrier),
+        // then the branch-free reciprocal of the pivot
         const double d = g[j * ld + j];
-        if (!(d > 0.0)) {
-            ok = false;  // uniform: every thread read the same d
-            break;
-        }
-        const double inv = __drcp_rn(d);
         double ga[KMAX], gb[KMAX], gab[KMAX];
 #pragma unroll
         for (int k = 0; k < KMAX; ++k) {
@@ -236,6 +233,11 @@ __device__ bool block_chol(double* g, int ld, int R) {
             gb[k] = act ? g[j * ld + pb[k]] : 0.0;
             gab[k] = act ? g[pa[k] * ld + pb[k]] : 0.0;
         }
+        if (!(d > 0.0)) {
+            ok = false;  // uniform: every thread read the same d
+            break;
+        }
+        const double inv = rcp_nr(d);
 #pragma unroll
         for (int k = 0; k < KMAX; ++k)
             if (pa[k] > j && pa[k] < R) g[pa[k] * ld + pb[k]] = fma(-ga[k] * inv, gb[k], gab[k]);
@@ -289,8 +291,8 @@ __device__ bool reg_chol(double* g, int ld, int R) {
                 if (t == 0) bad = 1;
                 break;
             }
-            const double inv = __drcp_rn(d);
             const double gb = b < R ? g[j * ld + b] : 0.0;  // G[j][b]
+            const double inv = rcp_nr(d);
 #pragma unroll
             for (int i = 0; i < E; ++i) {
                 const int a = 2 * i + par;
