@@ -132,6 +132,11 @@ int cpdb_create(int device, cpdb_ctx** out);
  * cpdb_nccl_unique_id on rank 0, broadcast by the caller. */
 int cpdb_create_sharded(int device, int rank, int world, const void* nccl_id, cpdb_ctx** out);
 int cpdb_nccl_unique_id(void* out128);
+/* `world` ranks of a mode-1 sharded run inside ONE process on ONE device,
+ * each to be driven by its own host thread; the collectives go through a
+ * shared device buffer and host barriers instead of NCCL.  For exercising the
+ * sharded path on a single GPU (tests); out holds `world` contexts. */
+int cpdb_create_local_group(int device, int world, cpdb_ctx** out);
 void cpdb_destroy(cpdb_ctx* ctx);
 /* Row range of the leading mode owned by `rank` (host-only, no device). */
 int cpdb_shard_rows(uint64_t extent0, int rank, int world, uint64_t* begin, uint64_t* count);

@@ -137,6 +137,21 @@ class Context:
         self._h = h
         self.device, self.rank, self.world = device, rank, world
 
+    @classmethod
+    def local_group(cls, device: int, world: int) -> List["Context"]:
+        """`world` mode-0 shard ranks inside this process on one device (each
+        must be driven from its own thread); collectives use a shared device
+        buffer instead of NCCL -- exercises the sharded path on one GPU."""
+        hs = (_cpdb.CTX * world)()
+        _raise(_lib().cpdb_create_local_group(device, world, hs))
+        out = []
+        for r in range(world):
+            ctx = cls.__new__(cls)
+            ctx._h = _cpdb.CTX(hs[r])
+            ctx.device, ctx.rank, ctx.world = device, r, world
+            out.append(ctx)
+        return out
+
     @staticmethod
     def nccl_unique_id() -> bytes:
         buf = C.create_string_buffer(128)

@@ -106,6 +106,7 @@ SIGNATURES = {
     "cpdb_tensor_synth": (C.c_int, [CTX, C.c_int32, U64P, C.c_uint32, C.c_uint64, C.c_double,
                                     C.c_uint64]),
     "cpdb_tensor_get": (C.c_int, [CTX, P]),
+    "cpdb_create_local_group": (C.c_int, [C.c_int, C.c_int, C.POINTER(CTX)]),
     "cpdb_tensor_load_cpdt": (C.c_int, [CTX, C.c_char_p]),
     "cpdb_tensor_save_cpdt": (C.c_int, [CTX, C.c_char_p]),
     "cpdb_cpdt_info": (C.c_int, [C.c_char_p, C.POINTER(C.c_uint32), U64P]),

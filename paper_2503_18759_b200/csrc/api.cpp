@@ -203,6 +203,31 @@ int cpdb_create_sharded(int device, int rank, int world, const void* nccl_id, cp
     return CPDB_OK;
 }
 
+int cpdb_create_local_group(int device, int world, cpdb_ctx** out) {
+    if (!out || world < 1) return CPDB_INVALID_ARGUMENT;
+    for (int r = 0; r < world; ++r) out[r] = nullptr;
+    auto group = std::make_shared<cpdb::LocalGroup>();
+    group->world = world;
+    for (int r = 0; r < world; ++r) {
+        cpdb_ctx* c = new (std::nothrow) cpdb_ctx();
+        if (!c) return CPDB_OUT_OF_MEMORY;
+        const int rc = guarded([&] {
+            init_ctx(c, device);
+            c->rank = r;
+            c->world = world;
+            c->group = group;
+        });
+        if (rc != CPDB_OK) {
+            delete c;
+            for (int q = 0; q < r; ++q) cpdb_destroy(out[q]);
+            return rc;
+        }
+        live_contexts(c->device, +1);
+        out[r] = c;
+    }
+    return CPDB_OK;
+}
+
 void cpdb_destroy(cpdb_ctx* ctx) {
     if (!ctx) return;
     const int dev = ctx->device;

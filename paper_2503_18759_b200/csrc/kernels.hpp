@@ -106,6 +106,9 @@ cudaError_t launch_zqr_multi(const ZqrArgs& a, cudaStream_t s, int sms);
 // out[e] = sum_{p < nsplit} part[p*n + e]  (fixed order)
 cudaError_t reduce_splits(const double* part, uint32_t nsplit, uint64_t n, double* out,
                           cudaStream_t s);
+// out[e] = sum_{r < world} slots[r*stride + e]  (fixed order; in-process rank groups)
+cudaError_t sum_slots(const double* slots, uint64_t stride, uint32_t world, uint64_t n,
+                      double* out, cudaStream_t s);
 
 // ---------------------------------------------------------------- misc
 // normalize_columns (linalg.hpp:225-242) with the reference's exact

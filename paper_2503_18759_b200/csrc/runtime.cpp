@@ -130,8 +130,54 @@ void require_tensor(cpdb_ctx* c) {
     if (!c->x) fail(CPDB_INVALID_ARGUMENT, "no tensor set on this context (cpdb_tensor_set)");
 }
 
+void LocalGroup::barrier(const std::function<void()>& last) {
+    std::unique_lock<std::mutex> lk(mu);
+    const uint64_t gen = generation;
+    if (++arrived == world) {
+        if (last) last();
+        arrived = 0;
+        ++generation;
+        cv.notify_all();
+    } else {
+        cv.wait(lk, [&] { return generation != gen; });
+    }
+}
+
+LocalGroup::~LocalGroup() {
+    if (slots) cudaFree(slots);
+}
+
+namespace {
+
+// rank r's n values -> slot r, then every rank reads all slots in rank order
+void group_publish(cpdb_ctx* c, const double* src, size_t n) {
+    LocalGroup& g = *c->group;
+    g.barrier([&] {  // grow the shared buffer while nobody uses it
+        if (g.cap < n) {
+            if (g.slots) cudaFree(g.slots);
+            g.slots = nullptr;
+            CPDB_CK(cudaMalloc(&g.slots, sizeof(double) * n * size_t(g.world)));
+            g.cap = n;
+        }
+    });
+    CPDB_CK(cudaMemcpyAsync(g.slots + size_t(c->rank) * g.cap, src, n * sizeof(double),
+                            cudaMemcpyDeviceToDevice, c->stream));
+    CPDB_CK(cudaStreamSynchronize(c->stream));
+    g.barrier();
+}
+
+}  // namespace
+
 void allreduce_sum(cpdb_ctx* c, double* dev, size_t n) {
     if (c->world <= 1) return;
+    if (c->group) {
+        LocalGroup& g = *c->group;
+        group_publish(c, dev, n);
+        CPDB_CK(sum_slots(g.slots, g.cap, uint32_t(g.world), n, dev, c->stream));
+        CPDB_CK(cudaStreamSynchronize(c->stream));
+        g.barrier();  // slots are reused by the next collective
+        return;
+    }
     const Nccl& N = nccl();
     const ncclResult_t r =
         N.AllReduce(dev, dev, n, ncclDouble, ncclSum, static_cast<ncclComm_t>(c->comm), c->stream);
@@ -140,6 +186,17 @@ void allreduce_sum(cpdb_ctx* c, double* dev, size_t n) {
 
 void allgather(cpdb_ctx* c, double* dev_full, size_t per_rank) {
     if (c->world <= 1) return;
+    if (c->group) {
+        LocalGroup& g = *c->group;
+        group_publish(c, dev_full + per_rank * size_t(c->rank), per_rank);
+        for (int r = 0; r < g.world; ++r)
+            CPDB_CK(cudaMemcpyAsync(dev_full + per_rank * size_t(r), g.slots + size_t(r) * g.cap,
+                                    per_rank * sizeof(double), cudaMemcpyDeviceToDevice,
+                                    c->stream));
+        CPDB_CK(cudaStreamSynchronize(c->stream));
+        g.barrier();
+        return;
+    }
     const Nccl& N = nccl();
     const ncclResult_t r = N.AllGather(dev_full + per_rank * c->rank, dev_full, per_rank,
                                        ncclDouble, static_cast<ncclComm_t>(c->comm), c->stream);

@@ -10,8 +10,12 @@
 
 #include <cuda_runtime.h>
 
+#include <condition_variable>
 #include <cstdint>
+#include <functional>
 #include <map>
+#include <memory>
+#include <mutex>
 #include <utility>
 #include <string>
 #include <vector>
@@ -79,6 +83,26 @@ struct Timer {
 
 }  // namespace cpdb
 
+namespace cpdb {
+// Ranks of one process on one device, each driven by its own host thread:
+// the collectives of the sharded path (all-reduce of partial sums, all-gather
+// of V) run through a shared device buffer and host barriers instead of
+// NCCL.  Exists so the sharded session is exercised on a single GPU
+// (cpdb_create_local_group); production multi-GPU runs use NCCL.
+struct LocalGroup {
+    int world = 1;
+    std::mutex mu;
+    std::condition_variable cv;
+    int arrived = 0;
+    uint64_t generation = 0;
+    double* slots = nullptr;  // world x cap doubles on the group's device
+    size_t cap = 0;
+    // every rank blocks until all arrived; the last one runs `last` first
+    void barrier(const std::function<void()>& last = {});
+    ~LocalGroup();
+};
+}  // namespace cpdb
+
 struct cpdb_ctx {
     int device = 0;
     int sms = 148;
@@ -88,6 +112,7 @@ struct cpdb_ctx {
     // sharding: leading mode split in contiguous slabs
     int rank = 0, world = 1;
     void* comm = nullptr;  // ncclComm_t
+    std::shared_ptr<cpdb::LocalGroup> group;  // in-process ranks (tests)
     uint64_t row_begin = 0, rows = 0;
 
     // X

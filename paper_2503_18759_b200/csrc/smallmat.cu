@@ -420,6 +420,25 @@ cudaError_t dot_dev(const double* a, const double* b, uint64_t n, double* partia
     return cudaGetLastError();
 }
 
+namespace {
+__global__ void sum_slots_kernel(const double* slots, uint64_t stride, uint32_t world, uint64_t n,
+                                 double* out) {
+    for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < n;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        double v = 0.0;
+        for (uint32_t r = 0; r < world; ++r) v += slots[r * stride + e];
+        out[e] = v;
+    }
+}
+}  // namespace
+
+cudaError_t sum_slots(const double* slots, uint64_t stride, uint32_t world, uint64_t n,
+                      double* out, cudaStream_t s) {
+    const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, 1024));
+    sum_slots_kernel<<<std::max(grid, 1u), 256, 0, s>>>(slots, stride, world, n, out);
+    return cudaGetLastError();
+}
+
 uint32_t vgemm_max_split() { return 1024; }
 
 cudaError_t launch_vgemm(VgemmArgs& a, cudaStream_t s, int sms) {

@@ -1,0 +1,94 @@
+"""The mode-0 sharded solver on ONE GPU: `world` ranks run in
+this process (one host thread each) through Context.local_group, whose
+collectives (all-reduce of the partial sums of mode-0 contractions, all-gather
+of V for the mode-0 update) use a shared device buffer instead of NCCL.  The
+session, slab geometry, shard plan and replicated tail are the production
+code; only the transport differs.  Results must match the unsharded run
+(summation order of the partials differs -> 1e-10 tolerance), integer costs
+exactly."""
+import threading
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def run_ranks(ctxs, fn):
+    out, errs = [None] * len(ctxs), []
+
+    def body(r):
+        try:
+            out[r] = fn(r, ctxs[r])
+        except Exception as e:  # pragma: no cover - surfaced below
+            errs.append(e)
+
+    ts = [threading.Thread(target=body, args=(r,)) for r in range(len(ctxs))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(600)
+    if errs:
+        raise errs[0]
+    return out
+
+
+@pytest.mark.parametrize("dims,rank,world,variant", [
+    ((16, 12, 10), 3, 2, "bre"),
+    ((24, 20, 16), 5, 4, "bre"),
+    ((12, 10, 8, 6), 3, 2, "bre"),
+    ((16, 12, 10), 3, 2, "naive"),
+    ((12, 10, 8, 6), 3, 2, "dim-tree"),
+    ((128, 96, 64), 16, 4, "bre"),
+    ((32, 24, 24, 20), 8, 8, "bre"),
+])
+def test_sharded_matches_unsharded(ctx, port, dims, rank, world, variant):
+    import paper_2503_18759_b200 as cpd
+    x = port.synth_baseline(0, dims, rank, 1e-2, 20250003)
+    strategy = "branch-reuse" if variant == "bre" else variant
+    cfg = cpd.SolverConfig(rank=rank, max_iterations=10, seed=7, strategy=strategy)
+    ext = variant == "bre"
+    ctx.set_tensor(x)
+    ref = ctx.solve(cfg, extrapolate=ext)
+    rows = dims[0] // world
+    group = cpd.Context.local_group(0, world)
+
+    def rank_run(r, c):
+        c.set_tensor(np.ascontiguousarray(x[r * rows:(r + 1) * rows]), dims)
+        return c.solve(cfg, extrapolate=ext)
+
+    res = run_ranks(group, rank_run)
+    for g in res:
+        assert len(g.trace) == len(ref.trace)
+        for a, b in zip(g.trace, ref.trace):
+            assert a.update_order == b.update_order and a.flops == b.flops
+            assert a.root_ttm_count == b.root_ttm_count and a.beta_used == b.beta_used
+            assert abs(a.fitness - b.fitness) <= 1e-10 * b.fitness
+        for fa, fb in zip(g.model.factors, ref.model.factors):
+            assert np.linalg.norm(fa - fb) <= 1e-10 * np.linalg.norm(fb)
+    # the replicated tail: every rank holds the same model
+    for g in res[1:]:
+        for fa, fb in zip(g.model.factors, res[0].model.factors):
+            assert np.array_equal(fa, fb)
+    for c in group:
+        c.close()
+
+
+def test_sharded_synth_matches_unsharded(ctx):
+    """Device generator on slabs: the counter-based values do not depend on
+    the shard layout; the noise scale is all-reduced."""
+    import paper_2503_18759_b200 as cpd
+    dims, world = [32, 24, 20], 4
+    ctx.synth_tensor(0, dims, 6, 1e-2, 99)
+    full = ctx.get_tensor(dims)
+    group = cpd.Context.local_group(0, world)
+
+    def rank_run(r, c):
+        c.synth_tensor(0, dims, 6, 1e-2, 99)
+        return c.get_tensor([dims[0] // world] + dims[1:])
+
+    slabs = run_ranks(group, rank_run)
+    got = np.concatenate(slabs, axis=0)
+    assert np.allclose(got, full, rtol=1e-13, atol=1e-13 * np.abs(full).max())
+    for c in group:
+        c.close()
