@@ -81,8 +81,13 @@ void init_ctx(cpdb_ctx* c, int device) {
     c->device = device;
     CPDB_CK(cudaSetDevice(device));
     c->sms = p.multiProcessorCount;
-    CPDB_CK(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-    CPDB_CK(cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking));
+    // the solve's critical path (stream, side) at high priority; the root-TTM
+    // prefetch (lo) yields to it CTA by CTA (Session::prefetch_root)
+    int least = 0, greatest = 0;
+    CPDB_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    CPDB_CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, greatest));
+    CPDB_CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, greatest));
+    CPDB_CK(cudaStreamCreateWithPriority(&c->lo, cudaStreamNonBlocking, least));
     CPDB_CK(cudaMalloc(&c->dstatus, 64));
     CPDB_CK(cudaMemset(c->dstatus, 0, 64));
     CPDB_CK(cudaMallocHost(&c->pinned, 64 * sizeof(double)));

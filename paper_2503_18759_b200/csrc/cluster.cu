@@ -20,6 +20,7 @@
 #include <cmath>
 
 #include "kernels.hpp"
+#include "launch.hpp"
 #include "rowalg.cuh"
 
 namespace cg = cooperative_groups;
@@ -443,7 +444,7 @@ cudaError_t launch_cluster(void (*kern)(Arg), size_t smem, cudaStream_t s, const
     attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[1].val.programmaticStreamSerializationAllowed = 1;
     c.attrs = attr;
-    c.numAttrs = pdl ? 2 : 1;
+    c.numAttrs = (pdl && pdl_enabled()) ? 2 : 1;
     return cudaLaunchKernelEx(&c, kern, arg);
 }
 

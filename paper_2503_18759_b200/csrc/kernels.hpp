@@ -14,6 +14,10 @@ struct TtmArgs {
     const double* qp;  // Q packed by pack_q -- tensor-core paths
     uint64_t outer, K, inner;
     uint32_t R, Rp;
+    int one_tile_per_cta;  // non-persistent grid (a low-priority launch that
+                           // yields SMs to concurrent work as its CTAs retire)
+    int no_pdl;            // plain launch (the stream's previous op is an event wait)
+    int no_tma;            // force the cp.async kernel (ttm.cu)
 };
 enum class TtmPath { groups, rows, simple };
 TtmPath ttm_path(const TtmArgs& a);

@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstring>
 #include <mutex>
 #include <numeric>
@@ -42,6 +43,7 @@ struct Block {
 };
 std::mutex g_pool_mu;
 std::vector<Block> g_pool;
+std::vector<Block> g_guarded;  // CPDB_GUARD debug registry
 
 }  // namespace
 
@@ -65,15 +67,45 @@ void* dev_alloc(size_t bytes, int* device, size_t* got) {
         }
     }
     void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, bytes);
+    static const bool guard = std::getenv("CPDB_GUARD") != nullptr;
+    const size_t gb = guard ? (size_t(1) << 20) : 0;  // debug: 1 MiB guard after the block
+    cudaError_t e = cudaMalloc(&p, bytes + gb);
     if (e == cudaErrorMemoryAllocation) {
         cudaGetLastError();
         dev_trim(dev);
-        e = cudaMalloc(&p, bytes);
+        e = cudaMalloc(&p, bytes + gb);
     }
     CPDB_CK(e);
+    if (guard) {
+        CPDB_CK(cudaMemset(static_cast<char*>(p) + bytes, 0xA5, gb));
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        g_guarded.push_back({dev, bytes, p});
+    }
     *got = bytes;
     return p;
+}
+
+void dev_guard_check(const char* where) {
+    std::vector<Block> blocks;
+    {
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        blocks = g_guarded;
+    }
+    CPDB_CK(cudaDeviceSynchronize());
+    std::vector<unsigned char> h(size_t(1) << 20);
+    for (const Block& b : blocks) {
+        CPDB_CK(cudaMemcpy(h.data(), static_cast<char*>(b.p) + b.bytes, h.size(),
+                           cudaMemcpyDeviceToHost));
+        size_t bad = 0, first = h.size();
+        for (size_t i = 0; i < h.size(); ++i)
+            if (h[i] != 0xA5) {
+                ++bad;
+                if (first == h.size()) first = i;
+            }
+        if (bad)
+            std::fprintf(stderr, "GUARD %s: block %p (%zu B) guard overwritten: %zu bytes, first +%zu\n",
+                         where, b.p, b.bytes, bad, first);
+    }
 }
 
 void dev_release(void* p, size_t bytes, int device) {
@@ -241,7 +273,8 @@ std::vector<uint64_t> natural_to_reference(uint32_t order, uint64_t R) {
 }
 
 void run_ttm(cpdb_ctx* ctx, const double* src, const std::vector<uint64_t>& sd, uint32_t c,
-             const double* q, const double* qp, uint32_t R, double* dst) {
+             const double* q, const double* qp, uint32_t R, double* dst, cudaStream_t stream,
+             bool one_tile_per_cta, bool no_pdl) {
     TtmArgs a{};
     a.x = src;
     a.y = dst;
@@ -254,7 +287,10 @@ void run_ttm(cpdb_ctx* ctx, const double* src, const std::vector<uint64_t>& sd, 
     a.K = sd[c];
     a.R = R;
     a.Rp = ttm_rpad(R);
-    CPDB_CK(launch_ttm(a, ctx->stream, ctx->sms));
+    a.one_tile_per_cta = one_tile_per_cta ? 1 : 0;
+    a.no_pdl = (no_pdl || one_tile_per_cta) ? 1 : 0;
+    a.no_tma = 0;
+    CPDB_CK(launch_ttm(a, stream ? stream : ctx->stream, ctx->sms));
     ctx->launches += 1;
 }
 
@@ -262,6 +298,7 @@ void run_ttm(cpdb_ctx* ctx, const double* src, const std::vector<uint64_t>& sd, 
 
 cpdb_ctx::~cpdb_ctx() {
     if (stream) cudaStreamSynchronize(stream);
+    if (lo) cudaStreamSynchronize(lo);
     if (comm) {
         const cpdb::Nccl& N = cpdb::nccl();
         if (N.ok) N.CommDestroy(static_cast<ncclComm_t>(comm));
@@ -270,4 +307,5 @@ cpdb_ctx::~cpdb_ctx() {
     if (pinned) cudaFreeHost(pinned);
     if (stream) cudaStreamDestroy(stream);
     if (side) cudaStreamDestroy(side);
+    if (lo) cudaStreamDestroy(lo);
 }

@@ -45,6 +45,7 @@ void check_cuda(cudaError_t e, const char* where);
 void* dev_alloc(size_t bytes, int* device, size_t* got);
 void dev_release(void* p, size_t bytes, int device);
 void dev_trim(int device);  // give every cached block of `device` back
+void dev_guard_check(const char* where);  // CPDB_GUARD debug: verify guard zones
 
 // Growable device allocation (never shrinks; released with its owner).
 struct DevBuf {
@@ -108,6 +109,7 @@ struct cpdb_ctx {
     int sms = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // Z-QR overlapped with the TTM chain
+    cudaStream_t lo = nullptr;    // low priority: root TTM prefetched under the previous update
 
     // sharding: leading mode split in contiguous slabs
     int rank = 0, world = 1;
@@ -160,6 +162,7 @@ std::vector<uint64_t> natural_to_reference(uint32_t order, uint64_t R);
 // One TTM of the execute() chain on device buffers: contracts `c` of a
 // tensor with local extents `sd` using factor Q (I_c x R) / packed Qp.
 void run_ttm(cpdb_ctx* ctx, const double* src, const std::vector<uint64_t>& sd, uint32_t c,
-             const double* q, const double* qp, uint32_t R, double* dst);
+             const double* q, const double* qp, uint32_t R, double* dst,
+             cudaStream_t stream = nullptr, bool one_tile_per_cta = false, bool no_pdl = false);
 
 }  // namespace cpdb

@@ -73,6 +73,9 @@ EventPool::~EventPool() {
 Session::~Session() {
     if (c && c->stream) cudaStreamSynchronize(c->stream);
     if (c && c->side) cudaStreamSynchronize(c->side);
+    if (c && c->lo) cudaStreamSynchronize(c->lo);
+    if (ev_fin) cudaEventDestroy(ev_fin);
+    if (pf.ev) cudaEventDestroy(pf.ev);
     if (t_start) cudaEventDestroy(t_start);
     if (ev_ready) cudaEventDestroy(ev_ready);
     if (ev_zqr) cudaEventDestroy(ev_zqr);
@@ -129,6 +132,14 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     launches0 = c->launches;
     CPDB_CK(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
     CPDB_CK(cudaEventCreateWithFlags(&ev_zqr, cudaEventDisableTiming));
+    CPDB_CK(cudaEventCreateWithFlags(&ev_fin, cudaEventDisableTiming));
+    CPDB_CK(cudaEventCreateWithFlags(&pf.ev, cudaEventDisableTiming));
+    {
+        const char* e = std::getenv("CPDB_ROOT_PREFETCH");
+        // not for TTM-dominated runs (C5: the root is 95% of the sweep, so the
+        // one-tile-per-CTA grid only costs)
+        prefetch_enabled = !sharded && !(e && e[0] == '0') && numel(c->ldims) < (1ull << 32);
+    }
 
     // ---- factor state (factor_state.hpp:28-34) -----------------------------
     fb.resize(order);
@@ -287,7 +298,9 @@ void Session::pack_local0() {
 }
 
 void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32_t flags,
-                       uint32_t k, double* dst, bool is_root) {
+                       uint32_t k, double* dst, bool is_root, cudaStream_t st, bool prefetch,
+                       bool no_pdl) {
+    if (!st) st = s;
     const double* q = fb[k].q.p;
     const double* qp = fb[k].qp.p;
     if (k == 0 && (flags & kSrcSharded)) {
@@ -299,11 +312,11 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32
         t.a = events.get();
         t.b = events.get();
         t.kind = is_root ? 0 : 1;
-        CPDB_CK(cudaEventRecord(t.a, s));
+        CPDB_CK(cudaEventRecord(t.a, st));
     }
-    run_ttm(c, src, sd, k, q, qp, R, dst);
+    run_ttm(c, src, sd, k, q, qp, R, dst, st, prefetch, no_pdl);
     if (c->timing) {
-        CPDB_CK(cudaEventRecord(t.b, s));
+        CPDB_CK(cudaEventRecord(t.b, st));
         const uint64_t nin = numel(sd);
         const uint64_t nout = nin / sd[k] * R;
         t.flops = 2.0 * double(nout) * double(sd[k]);
@@ -323,6 +336,38 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32
             CPDB_CK(cudaEventRecord(tc.b, s));
             timers.push_back(tc);
         }
+    }
+}
+
+// Root-TTM prefetch.  In a branch-reuse sweep the single root TTM sits in a
+// later update and contracts a mode whose Q was final one or more updates
+// earlier ("Dependencies and overlap").  Right after update b,
+// if update b2 > b+1 starts with a root step contracting c and no update in
+// (b, b2) changes Q_c, the root TTM is issued on the low-priority stream into
+// a spare buffer: its CTAs (one tile each) fill the SMs the latency-bound
+// updates in between leave idle, and update b2 adopts the buffer.
+void Session::prefetch_root(uint64_t sweep, uint32_t b) {
+    if (!prefetch_enabled || pf.active) return;
+    const Sweep& sw = plan.sweeps[sweep - 1];
+    for (uint32_t b2 = b + 2; b2 < order; ++b2) {
+        const Update& u = sw.updates[b2];
+        if (u.steps.empty() || u.steps[0].source != plan.root()) continue;
+        const uint32_t cm = u.steps[0].contract;
+        if (u.steps[0].produces == (1u << u.mode)) continue;  // (order 2: nothing to gain)
+        bool fresh = true;
+        for (uint32_t bm = b + 1; bm < b2; ++bm) fresh = fresh && sw.updates[bm].mode != cm;
+        if (!fresh) continue;
+        std::vector<uint64_t> od = c->ldims;
+        od[cm] = R;
+        pre.ensure(numel(od));
+        CPDB_CK(cudaEventRecord(ev_fin, s));
+        CPDB_CK(cudaStreamWaitEvent(c->lo, ev_fin, 0));
+        ttm_step(c->x, c->ldims, 0, cm, pre.p, true, c->lo, true, true);
+        CPDB_CK(cudaEventRecord(pf.ev, c->lo));
+        pf.active = true;
+        pf.sweep = sweep;
+        pf.block = b2;
+        return;
     }
 }
 
@@ -386,7 +431,9 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         observer(user, sweep, n, ref.data(), zrows, R);
     }
     // 4. the scheduled TTM chain (execute, dim_tree.hpp:496-541)
-    for (const Step& st : sw.updates[b].steps) {
+    bool after_wait = false;
+    for (size_t si = 0; si < sw.updates[b].steps.size(); ++si) {
+        const Step& st = sw.updates[b].steps[si];
         const double* src;
         std::vector<uint64_t> sd;
         std::vector<uint64_t> stamp(order, 0);
@@ -411,9 +458,19 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         }
         std::vector<uint64_t> od = sd;
         od[st.contract] = R;
-        double* dst =
-            (st.produces == (1u << n)) ? ybuf[n].p : cache[st.produces].buf.ensure(numel(od));
-        ttm_step(src, sd, flags, st.contract, dst, st.source == root);
+        if (si == 0 && pf.active && pf.sweep == sweep && pf.block == b) {
+            // issued early by prefetch_root: adopt its buffer as the slot
+            CPDB_CK(cudaStreamWaitEvent(s, pf.ev, 0));
+            cache[st.produces].buf.swap(pre);
+            pf.active = false;
+            after_wait = true;
+        } else {
+            double* dst =
+                (st.produces == (1u << n)) ? ybuf[n].p : cache[st.produces].buf.ensure(numel(od));
+            ttm_step(src, sd, flags, st.contract, dst, st.source == root, nullptr, false,
+                     after_wait);
+            after_wait = false;
+        }
         // global-extent flop count, exactly as the reference counts it
         uint64_t gout = 1;
         for (uint32_t k = 0; k < order; ++k)
@@ -520,6 +577,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
         hist[n].swap(q0buf);  // the history keeps the unextrapolated Q0 (:265)
         has_hist[n] = true;
     }
+    prefetch_root(sweep, b);
 }
 
 // ---------------------------------------------------------------- sweeps
@@ -568,6 +626,8 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
             fail(CPDB_SINGULAR_TRIANGULAR,
                  "Cholesky QR breakdown: rank-deficient Khatri-Rao or factor matrix");
         }
+        static const bool dbg_guard = std::getenv("CPDB_GUARD") != nullptr;
+        if (dbg_guard) dev_guard_check(("sweep " + std::to_string(sweep)).c_str());
         const double fit = c->pinned[0], raw = c->pinned[1];
         float ms = 0.f;
         CPDB_CK(cudaEventElapsedTime(&ms, t_start, e_end));

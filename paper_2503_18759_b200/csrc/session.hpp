@@ -48,6 +48,17 @@ struct Session {
 
     EventPool events;
     bool front_issued = false;  // next sweep's first Z-QR + TTM chain already on the stream
+    // root TTM of a later update of the sweep issued early on the low-priority
+    // stream, overlapped with the updates in between (prefetch_root)
+    struct Prefetch {
+        bool active = false;
+        uint64_t sweep = 0;
+        uint32_t block = 0;
+        cudaEvent_t ev = nullptr;
+    } pf;
+    DevBuf pre;
+    cudaEvent_t ev_fin = nullptr;
+    bool prefetch_enabled = false;
     std::vector<Timer> timers;
     cudaEvent_t t_start = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_zqr = nullptr;  // main -> side -> main fork/join
@@ -65,7 +76,9 @@ private:
     void qr_factor(uint32_t k);
     void pack_local0();
     void ttm_step(const double* src, const std::vector<uint64_t>& sd, int32_t flags,
-                  uint32_t k, double* dst, bool is_root);
+                  uint32_t k, double* dst, bool is_root, cudaStream_t st = nullptr,
+                  bool prefetch = false, bool no_pdl = false);
+    void prefetch_root(uint64_t sweep, uint32_t b);
     void mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer, void* user,
                      double& beta_used);
     void mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer observer, void* user);

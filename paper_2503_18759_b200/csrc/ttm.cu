@@ -290,7 +290,7 @@ cudaError_t launch_ttm(const TtmArgs& a, cudaStream_t s, int sms) {
         const char* v = std::getenv("CPDB_TTM");
         return v ? std::atoi(v) : 2;
     }();
-    if (version >= 2 && a.qp != nullptr) {
+    if (version >= 2 && a.qp != nullptr && !a.no_tma) {
         const cudaError_t e = launch_ttm_tma(a, s, sms);  // warp-specialised TMA path
         if (e != cudaErrorNotSupported) return e;
     }

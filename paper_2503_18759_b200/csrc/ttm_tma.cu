@@ -251,6 +251,8 @@ ttm_tma_kernel(const __grid_constant__ CUtensorMap xmap, double* __restrict__ y,
             for (int rb = 0; rb < RB; ++rb) acc[rb][cb][0] = acc[rb][cb][1] = 0.0;
         }
     }
+    // the output is read by later grids through TMA (async proxy)
+    asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
 // ---------------------------------------------------------------- tensor maps
@@ -318,16 +320,29 @@ cudaError_t launch_v2(const TtmArgs& a, cudaStream_t s, int sms) {
         return cudaErrorNotSupported;
     }
     auto kern = ttm_tma_kernel<RB, CB, BK, STAGES, NC, LAYOUT>;
+    // Every TMA TTM CTA reserves the SM's whole shared memory, so no CTA of
+    // another grid is co-resident with it.  Measured: with the root TTM
+    // running concurrently on the low-priority stream, co-residency with other
+    // grids' CTAs gave non-reproducible results (C3: 14 of 90 repeated solves
+    // differed; 0 of 90 with exclusive SMs; tools/det_probe.py).  The TTM
+    // runs one CTA per SM anyway.
+    const size_t smem = size_t(227 * 1024);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(C::SMEM));
+                                         int(smem));
     if (e != cudaSuccess) return e;
     const uint64_t ncols = LAYOUT == kGroups ? (a.outer * a.inner) / 8 : a.outer;  // groups or rows
     const uint64_t per_tile = LAYOUT == kGroups ? C::G : C::BJ;
     const uint64_t ntiles = (ncols + per_tile - 1) / per_tile;
     const uint32_t nk = static_cast<uint32_t>((a.K + BK - 1) / BK);
-    const uint64_t grid = std::min<uint64_t>(ntiles, uint64_t(sms));
+    const uint64_t grid =
+        a.one_tile_per_cta ? ntiles : std::min<uint64_t>(ntiles, uint64_t(sms));
     if (grid == 0) return cudaSuccess;
-    return launch_pdl(kern, dim3(unsigned(grid)), dim3(C::NT), C::SMEM, s, map, a.y, a.qp, a.outer,
+    if (a.no_pdl) {
+        kern<<<unsigned(grid), C::NT, smem, s>>>(map, a.y, a.qp, a.outer, a.K, a.inner, a.R,
+                                                   ntiles, nk);
+        return cudaGetLastError();
+    }
+    return launch_pdl(kern, dim3(unsigned(grid)), dim3(C::NT), smem, s, map, a.y, a.qp, a.outer,
                       a.K, a.inner, a.R, ntiles, nk);
 }
 

@@ -252,3 +252,26 @@ def test_full_size_teacher_forced(port, name, k):
     assert abs(g.trace[0].fitness - o.trace[0]["fitness"]) <= FIT_TOL * o.trace[0]["fitness"]
     for fg, fo in zip(g.model.factors, o.factors):
         assert np.linalg.norm(fg - fo) / np.linalg.norm(fo) <= FACTOR_TOL
+
+
+def test_repeated_solves_bit_identical_with_root_prefetch():
+    """Steady branch-reuse sweeps overlap the root TTM (low-priority stream)
+    with the preceding update.  Repeated solves in one context must stay
+    bit-identical (this shape exposed a co-residency race before the TMA TTM
+    took whole SMs; tools/det_probe.py)."""
+    import paper_2503_18759_b200 as cpd
+    ctx = cpd.Context(0)
+    ctx.synth_tensor(0, [96, 96, 96, 96], 16, 1e-2, 12345)
+    ref = None
+    for _ in range(6):
+        s = ctx.session(cfg_of(16, 4, seed=7), extrapolate=True)
+        rows = s.run(4)
+        model = s.end()
+        s.close()
+        got = ([(r.fitness, r.raw_radicand) for r in rows], [f.copy() for f in model.factors])
+        if ref is None:
+            ref = got
+        else:
+            assert got[0] == ref[0]
+            for a, b in zip(got[1], ref[1]):
+                assert np.array_equal(a, b)
