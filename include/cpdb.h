@@ -192,9 +192,11 @@ int cpdb_session_end(cpdb_session* s, cpdb_state* state, double* out_lambda,
 void cpdb_session_destroy(cpdb_session* s);
 int cpdb_profile_get(cpdb_ctx* ctx, cpdb_profile* out);
 /* Enable/disable per-kernel event timing inside cpdb_solve (default on; off
- * removes the events from the stream).  CUDA-graph capture of the sweeps is
- * used when `graphs` is 1 (default). */
-int cpdb_set_options(cpdb_ctx* ctx, int32_t timing, int32_t graphs);
+ * removes the events from the stream), and the root-TTM overlap (default on:
+ * a branch-reuse sweep's root TTM is issued on a low-priority stream under
+ * the preceding update; off runs every TTM in schedule order on the solve
+ * stream -- the kernel alone, e.g. for roofline measurements). */
+int cpdb_set_options(cpdb_ctx* ctx, int32_t timing, int32_t overlap);
 
 /* ---- dense primitives on host buffers (device compute) ------------------------ */
 int cpdb_ttm(cpdb_ctx* ctx, const double* t, const uint64_t* dims, uint32_t order,

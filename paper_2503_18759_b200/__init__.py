@@ -215,8 +215,10 @@ class Context:
         _raise(_lib().cpdb_profile_get(self._h, C.byref(p)))
         return {name: getattr(p, name) for name, _ in p._fields_}
 
-    def set_options(self, timing: bool = True, graphs: bool = True):
-        _raise(_lib().cpdb_set_options(self._h, int(timing), int(graphs)))
+    def set_options(self, timing: bool = True, overlap: bool = True):
+        """timing: per-kernel CUDA events; overlap: root-TTM prefetch on a
+        low-priority stream (off = every TTM in order, the kernel alone)."""
+        _raise(_lib().cpdb_set_options(self._h, int(timing), int(overlap)))
 
     # ---- solver
     def session(self, cfg: "SolverConfig", *, extrapolate: bool) -> "SolverSession":

@@ -423,10 +423,10 @@ int cpdb_profile_get(cpdb_ctx* c, cpdb_profile* out) {
     return CPDB_OK;
 }
 
-int cpdb_set_options(cpdb_ctx* c, int32_t timing, int32_t graphs) {
+int cpdb_set_options(cpdb_ctx* c, int32_t timing, int32_t overlap) {
     if (!c) return CPDB_INVALID_ARGUMENT;
     c->timing = timing != 0;
-    c->graphs = graphs != 0;
+    c->overlap = overlap != 0;
     return CPDB_OK;
 }
 

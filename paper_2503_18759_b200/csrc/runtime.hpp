@@ -135,7 +135,7 @@ struct cpdb_ctx {
 
     cpdb_profile prof{};
     bool timing = true;
-    bool graphs = true;
+    bool overlap = true;  // root-TTM prefetch (Session::prefetch_root)
     uint64_t launches = 0;
 
     ~cpdb_ctx();

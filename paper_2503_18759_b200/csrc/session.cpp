@@ -138,7 +138,8 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         const char* e = std::getenv("CPDB_ROOT_PREFETCH");
         // not for TTM-dominated runs (C5: the root is 95% of the sweep, so the
         // one-tile-per-CTA grid only costs)
-        prefetch_enabled = !sharded && !(e && e[0] == '0') && numel(c->ldims) < (1ull << 32);
+        prefetch_enabled = c->overlap && !sharded && !(e && e[0] == '0') &&
+                           numel(c->ldims) < (1ull << 32);
     }
 
     // ---- factor state (factor_state.hpp:28-34) -----------------------------
