@@ -275,3 +275,22 @@ def test_repeated_solves_bit_identical_with_root_prefetch():
             assert got[0] == ref[0]
             for a, b in zip(got[1], ref[1]):
                 assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("dims,rank", [((9, 8, 7), 1), ((20, 18, 16), 7), ((30, 28, 26), 13),
+                                       ((40, 38, 36), 33), ((70, 66, 65), 64),
+                                       ((12, 11, 10, 9), 9), ((10, 9, 8, 8, 7), 5)])
+def test_rank_edges_vs_oracle(ctx, port, dims, rank):
+    """Rank 1, ranks that are not multiples of 8 (padding of the DMMA
+    fragments and the packed Q), R = 33 (the RM = 64 templates with one
+    padding block), R = 64 (largest supported), 4th order with R = I_n, and a
+    5th-order tensor (naive plan only; the tree plans are orders 3-4)."""
+    import paper_2503_18759_b200 as cpd
+    x = port.rng_normals(4242 + rank, int(np.prod(dims))).reshape(dims)
+    if len(dims) == 5:
+        g = cpd.cp_als_qr(x, cfg_of(rank, 4, seed=5, strategy="naive"), ctx=ctx)
+        o = port.solve(x, rank, 4, extrapolate=False, strategy="naive", seed=5)
+    else:
+        g = cpd.als_qr_bre(x, cfg_of(rank, 6, seed=5), ctx=ctx)
+        o = port.solve(x, rank, 6, extrapolate=True, seed=5)
+    compare(g, o, fit_tol=1e-9, factor_tol=1e-8)
