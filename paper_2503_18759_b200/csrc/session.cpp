@@ -186,6 +186,10 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     zwork.ensure(zqr_work_doubles(R) + uint64_t(4 * c->sms) * R * R);
     vfull.ensure(maxI * R);
     vfitfull.ensure(maxI * R);
+    // V-GEMM partials up front (the dual ones are first needed when the beta
+    // gate opens, mid-run: no allocation inside the sweeps)
+    vpart.ensure(size_t(vgemm_max_split()) * maxI * R);
+    if (extrap) vfitpart.ensure(size_t(vgemm_max_split()) * maxI * R);
     versions.assign(order, 1);
     CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
     for (uint32_t k = 0; k < order; ++k) qr_factor(k);

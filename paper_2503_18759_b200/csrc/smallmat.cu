@@ -362,9 +362,16 @@ __global__ void reduce_splits_kernel(const double* part, uint32_t nsplit, uint64
     pdl_entry();
     for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < n;
          e += uint64_t(gridDim.x) * blockDim.x) {
-        double s = 0.0;
-        for (uint32_t p = 0; p < nsplit; ++p) s += part[p * n + e];
-        out[e] = s;
+        // eight loads in flight per step (the partials come from L2); fixed
+        // summation tree -> deterministic
+        double s[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        uint32_t p = 0;
+        for (; p + 8 <= nsplit; p += 8) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) s[u] += part[(p + u) * n + e];
+        }
+        for (; p < nsplit; ++p) s[0] += part[p * n + e];
+        out[e] = ((s[0] + s[1]) + (s[2] + s[3])) + ((s[4] + s[5]) + (s[6] + s[7]));
     }
 }
 
@@ -439,7 +446,7 @@ cudaError_t sum_slots(const double* slots, uint64_t stride, uint32_t world, uint
     return cudaGetLastError();
 }
 
-uint32_t vgemm_max_split() { return 1024; }
+uint32_t vgemm_max_split() { return 296; }  // 2 CTAs per SM on 148 SMs
 
 cudaError_t launch_vgemm(VgemmArgs& a, cudaStream_t s, int sms) {
     const bool d = a.dual != 0;
