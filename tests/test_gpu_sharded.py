@@ -92,3 +92,11 @@ def test_sharded_synth_matches_unsharded(ctx):
     assert np.allclose(got, full, rtol=1e-13, atol=1e-13 * np.abs(full).max())
     for c in group:
         c.close()
+
+
+def test_nccl_library_available():
+    """The multi-GPU transport: libnccl.so.2 resolves (dlopen, comm.cpp) and
+    hands out a unique id; one rank per GPU then calls cpdb_create_sharded."""
+    import paper_2503_18759_b200 as cpd
+    uid = cpd.Context.nccl_unique_id()
+    assert isinstance(uid, bytes) and len(uid) == 128 and any(uid)
