@@ -65,9 +65,9 @@ struct Smem {
     }
 };
 
-template <int RM>
+template <int RM, int SL>
 __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
-    using Row = LaneRow<RM>;
+    using Row = LaneRow<RM, SL>;
     constexpr int T = Row::T, G = kNT / T;
     cg::cluster_group cl = cg::this_cluster();
     const int rank = int(cl.block_rank());
@@ -300,9 +300,9 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
 }
 
 // ---------------------------------------------------------------- Z-QR (small Z)
-template <int RM>
+template <int RM, int SL>
 __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
-    using Row = LaneRow<RM>;
+    using Row = LaneRow<RM, SL>;
     constexpr int T = Row::T, G = kNT / T;
     cg::cluster_group cl = cg::this_cluster();
     const int rank = int(cl.block_rank());
@@ -471,16 +471,57 @@ size_t finish_cluster_smem(uint64_t I, uint32_t R) {
     }
 }
 
+namespace {
+
+// Slots per lane of the row solves: as few as possible (more lanes per row,
+// shorter solve steps) while every row of a CTA still gets a lane group.
+int slots_for(int rm, uint64_t rows_per_cta) {
+    int sl = 1;
+    while (sl < 8 && (uint64_t(kNT) / uint64_t(rm / sl)) < rows_per_cta) sl *= 2;
+    while (rm / sl > 32) sl *= 2;  // at most one warp per row
+    return sl;
+}
+
+template <int RM, int SL>
+cudaError_t finish_rs(const FinishArgs& a, size_t smem, cudaStream_t s) {
+    return launch_cluster<FinishArgs>(finish_cluster_kernel<RM, SL>, smem, s, a, true);
+}
+template <int RM, int SL>
+cudaError_t zqr_rs(const ZqrArgs& a, size_t smem, cudaStream_t s) {
+    return launch_cluster<ZqrArgs>(zqr_cluster_kernel<RM, SL>, smem, s, a, false);
+}
+
+template <int RM, class F8, class F4, class F2, class F1>
+cudaError_t by_slots(int sl, F8 f8, F4 f4, F2 f2, F1 f1) {
+    switch (sl) {
+        case 1: if constexpr (RM <= 32) return f1(); else return f2();
+        case 2: return f2();
+        case 4: return f4();
+        default: return f8();
+    }
+}
+
+}  // namespace
+
 cudaError_t launch_finish_cluster(const FinishArgs& a, cudaStream_t s) {
     if (a.R > 64) return cudaErrorInvalidValue;
     const size_t smem = finish_cluster_smem(a.I, a.R);
     if (smem > 220 * 1024) return cudaErrorInvalidValue;
-    switch (rm_of(a.R)) {
-        case 8: return launch_cluster<FinishArgs>(finish_cluster_kernel<8>, smem, s, a, true);
-        case 16: return launch_cluster<FinishArgs>(finish_cluster_kernel<16>, smem, s, a, true);
-        case 32: return launch_cluster<FinishArgs>(finish_cluster_kernel<32>, smem, s, a, true);
-        default: return launch_cluster<FinishArgs>(finish_cluster_kernel<64>, smem, s, a, true);
+    const uint64_t rows = (a.I + kCS - 1) / kCS;
+    const int rm = rm_of(a.R), sl = slots_for(rm, rows);
+#define CPDB_FIN(RM_)                                                                    \
+    return by_slots<RM_>(                                                                \
+        sl, [&] { return finish_rs<RM_, 8>(a, smem, s); },                               \
+        [&] { return finish_rs<RM_, 4>(a, smem, s); },                                   \
+        [&] { return finish_rs<RM_, 2>(a, smem, s); },                                   \
+        [&] { return finish_rs<RM_, (RM_ <= 32 ? 1 : 2)>(a, smem, s); })
+    switch (rm) {
+        case 8: CPDB_FIN(8);
+        case 16: CPDB_FIN(16);
+        case 32: CPDB_FIN(32);
+        default: CPDB_FIN(64);
     }
+#undef CPDB_FIN
 }
 
 static size_t zqr_cluster_smem(uint64_t zrows, uint32_t R, uint32_t nm) {
@@ -498,12 +539,21 @@ bool zqr_cluster_fits(uint64_t zrows, uint32_t R, uint32_t nm) {
 
 cudaError_t launch_zqr_cluster(const ZqrArgs& a, cudaStream_t s) {
     const size_t smem = zqr_cluster_smem(a.zrows, a.R, a.nm);
-    switch (rm_of(a.R)) {
-        case 8: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<8>, smem, s, a, false);
-        case 16: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<16>, smem, s, a, false);
-        case 32: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<32>, smem, s, a, false);
-        default: return launch_cluster<ZqrArgs>(zqr_cluster_kernel<64>, smem, s, a, false);
+    const uint64_t rows = (a.zrows + kCS - 1) / kCS;
+    const int rm = rm_of(a.R), sl = slots_for(rm, rows);
+#define CPDB_ZQR(RM_)                                                                    \
+    return by_slots<RM_>(                                                                \
+        sl, [&] { return zqr_rs<RM_, 8>(a, smem, s); },                                  \
+        [&] { return zqr_rs<RM_, 4>(a, smem, s); },                                      \
+        [&] { return zqr_rs<RM_, 2>(a, smem, s); },                                      \
+        [&] { return zqr_rs<RM_, (RM_ <= 32 ? 1 : 2)>(a, smem, s); })
+    switch (rm) {
+        case 8: CPDB_ZQR(8);
+        case 16: CPDB_ZQR(16);
+        case 32: CPDB_ZQR(32);
+        default: CPDB_ZQR(64);
     }
+#undef CPDB_ZQR
 }
 
 }  // namespace cpdb

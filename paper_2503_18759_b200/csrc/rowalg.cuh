@@ -35,10 +35,13 @@ __device__ double block_sum(double v, double* red) {
 // ---------------------------------------------------------------- lane rows
 // A row of length <= RM distributed over T = RM/8 lanes: lane q holds
 // x[8*i... ] as t[s] = x[s*T + q], s < 8.
-template <int RM>
+// SL = slots per lane: 8 by default; fewer slots (more lanes per row) when a
+// CTA has fewer rows than lane groups, which shortens every solve step.
+template <int RM, int SL = 8>
 struct LaneRow {
-    static constexpr int T = RM / 8 > 0 ? RM / 8 : 1;
-    static constexpr int S = RM / T;  // slots per lane (8)
+    static constexpr int T = RM / SL > 0 ? RM / SL : 1;  // lanes per row (<= 32)
+    static constexpr int S = RM / T;                    // slots per lane
+    static_assert(T <= 32, "LaneRow: at most one warp per row");
     double t[S];
 
     __device__ __forceinline__ void load(const double* src, int R, int q) {
