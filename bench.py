@@ -36,6 +36,8 @@ import sys
 import threading
 import time
 
+import numpy as np
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
@@ -47,6 +49,7 @@ CONFIGS = {
     "c4": dict(kind=1, dims=(256, 256, 256), rank=20, rho=1e-4, sweeps=500),
     "c5": dict(kind=0, dims=(256, 256, 256, 256), rank=64, rho=1e-3, sweeps=50),
 }
+CPU_BASELINE_MAX_ELEMS = 1 << 28  # 2 GB of f64: larger X has no bounded reference sample
 TRUTH_SEED = {"c1": 20250001, "c2": 20250002, "c3": 20250003, "c4": 20250004, "c5": 20250005}
 INIT_SEED = 7
 
@@ -192,6 +195,12 @@ def run_reference(args, c, rank, world):
         return 0
     from oracle.pyoracle import Oracle, available
     kind = "reference" if available("reference") else "port"
+    if int(np.prod(c["dims"])) > CPU_BASELINE_MAX_ELEMS:
+        print(json.dumps({"impl": "reference", "unavailable":
+                          f"one single-threaded reference sweep of {workload_name(args.config, c)} "
+                          "takes >= 10 min on a host core (SURVEY 8d): no bounded sample"}),
+              flush=True)
+        return 0
     o = Oracle(kind)
     t0 = time.perf_counter()
     x = o.synth_baseline(c["kind"], c["dims"], c["rank"], c["rho"], TRUTH_SEED[args.config])
@@ -237,8 +246,6 @@ def main():
     rank, world, local = init_dist()
     if args.impl == "reference":
         return run_reference(args, c, rank, world)
-
-    import numpy as np
 
     import paper_2503_18759_b200 as cpd
 
@@ -327,7 +334,9 @@ def main():
     e2e = None
     x_host = None
     local_dims = [dims[0] // world] + dims[1:]
-    if not args.no_e2e or (rank == 0 and world == 1 and not args.no_cpu_baseline):
+    need_cpu = (rank == 0 and world == 1 and not args.no_cpu_baseline
+                and np.prod(dims) <= CPU_BASELINE_MAX_ELEMS)
+    if not args.no_e2e or need_cpu:
         x_host = ctx.get_tensor(local_dims)
     if not args.no_e2e:
         try:
@@ -359,10 +368,17 @@ def main():
     # ---- CPU baseline: the reference itself, bounded sample ---------------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        rate, kind, n, wall = cpu_reference_rate(x_host, c, args.cpu_baseline_sweeps)
-        cpu = {"value": rate, "unit": "sweeps/s", "cores": 1, "kind": kind,
-               "sample": f"{n} steady ALS-QR-BRE sweeps (after the untimed dim-tree sweep) on "
-                         f"the same tensor, single-threaded reference, {wall:.1f}s wall"}
+        if np.prod(dims) > CPU_BASELINE_MAX_ELEMS:
+            # one reference sweep of C5's 34 GB tensor takes >= 10 min on a
+            # host core: no bounded sample of this workload exists
+            cpu = {"value": None, "unit": "sweeps/s", "cores": 1, "kind": "reference",
+                   "sample": "skipped: one single-threaded reference sweep of this tensor "
+                             "takes >= 10 min (SURVEY 8d)"}
+        else:
+            rate, kind, n, wall = cpu_reference_rate(x_host, c, args.cpu_baseline_sweeps)
+            cpu = {"value": rate, "unit": "sweeps/s", "cores": 1, "kind": kind,
+                   "sample": f"{n} steady ALS-QR-BRE sweeps (after the untimed dim-tree sweep) "
+                             f"on the same tensor, single-threaded reference, {wall:.1f}s wall"}
 
     if rank == 0:
         line = {

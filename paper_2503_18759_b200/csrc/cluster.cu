@@ -488,7 +488,7 @@ cudaError_t finish_rs(const FinishArgs& a, size_t smem, cudaStream_t s) {
 }
 template <int RM, int SL>
 cudaError_t zqr_rs(const ZqrArgs& a, size_t smem, cudaStream_t s) {
-    return launch_cluster<ZqrArgs>(zqr_cluster_kernel<RM, SL>, smem, s, a, false);
+    return launch_cluster<ZqrArgs>(zqr_cluster_kernel<RM, SL>, smem, s, a, a.pdl != 0);
 }
 
 template <int RM, class F8, class F4, class F2, class F1>

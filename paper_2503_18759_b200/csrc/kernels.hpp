@@ -49,6 +49,7 @@ struct ZqrArgs {
     double* work;            // zqr_work_doubles(R, grid)
     int* status;             // device flag: non-zero = Cholesky breakdown
     unsigned long long* ts;  // optional phase timestamps (profiling)
+    int pdl;                 // launch programmatically after the previous kernel
 };
 size_t zqr_work_doubles(uint32_t R);
 cudaError_t launch_zqr(const ZqrArgs& a, cudaStream_t s, int sms);
@@ -67,7 +68,10 @@ struct VgemmArgs {
     uint32_t R;
     double* vpart;       // nsplit x I x R
     double* vfitpart;    // nsplit x I x R (dual)
+    double* v_out;       // I x R: final V when the kernel reduces on chip (may be null)
+    double* vfit_out;    // I x R: final Vfit (dual)
     uint32_t nsplit;     // out: split count used
+    int reduced;         // out: 1 = V written to v_out (no reduce_splits needed)
 };
 cudaError_t launch_vgemm(VgemmArgs& a, cudaStream_t s, int sms);
 uint32_t vgemm_max_split();

@@ -323,6 +323,11 @@ __device__ bool reg_chol(double* g, int ld, int R) {
 
 // Measured (tools/probes/chol2_probe.cu, one 256-thread CTA): block_chol is
 // faster up to R = 32 (17.3k vs 23.4k cycles), reg_chol at R = 64 (76k vs 121k).
+// A one-warp register Cholesky (tools/probes/chol3_probe.cu: warp_chol) is
+// faster alone at R = 32 (14.5k vs 19.5k cycles) but 1.5-3.5x slower inside
+// the solver while TTM kernels run concurrently on the other SMs
+// (CPDB_PHASE_TRACE, C2: 5.2 us alone, 18.5 us beside the root TTM; block
+// form 7.0 / 10.2 us), so the block-wide form stays.
 template <int NT, int RM>
 __device__ bool chol(double* g, int ld, int R) {
     if constexpr (RM >= 64) {

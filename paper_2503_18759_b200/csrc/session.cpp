@@ -81,6 +81,42 @@ Session::~Session() {
     if (ev_zqr) cudaEventDestroy(ev_zqr);
 }
 
+// ---------------------------------------------------------------- timeline
+cudaEvent_t Session::tl_begin(cudaStream_t st) {
+    if (!timeline) return nullptr;
+    cudaEvent_t a;
+    CPDB_CK(cudaEventCreate(&a));
+    CPDB_CK(cudaEventRecord(a, st));
+    return a;
+}
+
+void Session::tl_end(cudaEvent_t a, cudaStream_t st, const char* label) {
+    if (!timeline) return;
+    cudaEvent_t b;
+    CPDB_CK(cudaEventCreate(&b));
+    CPDB_CK(cudaEventRecord(b, st));
+    const int sid = st == c->side ? 1 : st == c->lo ? 2 : 0;
+    marks.push_back(Mark{label, sid, tl_sweep, tl_mode, a, b});
+}
+
+void Session::tl_flush() {
+    if (!timeline || marks.empty()) return;
+    CPDB_CK(cudaDeviceSynchronize());
+    FILE* f = std::fopen(timeline, "a");
+    for (const Mark& m : marks) {
+        float t0 = 0.f, t1 = 0.f;
+        CPDB_CK(cudaEventElapsedTime(&t0, t_start, m.a));
+        CPDB_CK(cudaEventElapsedTime(&t1, t_start, m.b));
+        if (f)
+            std::fprintf(f, "%s,%d,%llu,%u,%.2f,%.2f\n", m.label, m.stream,
+                         (unsigned long long)m.sweep, m.mode, t0 * 1e3, t1 * 1e3);
+        cudaEventDestroy(m.a);
+        cudaEventDestroy(m.b);
+    }
+    if (f) std::fclose(f);
+    marks.clear();
+}
+
 // ---------------------------------------------------------------- setup
 void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* state) {
     c = ctx;
@@ -134,12 +170,15 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     CPDB_CK(cudaEventCreateWithFlags(&ev_zqr, cudaEventDisableTiming));
     CPDB_CK(cudaEventCreateWithFlags(&ev_fin, cudaEventDisableTiming));
     CPDB_CK(cudaEventCreateWithFlags(&pf.ev, cudaEventDisableTiming));
+    timeline = std::getenv("CPDB_TIMELINE");
     {
         const char* e = std::getenv("CPDB_ROOT_PREFETCH");
         // not for TTM-dominated runs (C5: the root is 95% of the sweep, so the
         // one-tile-per-CTA grid only costs)
         prefetch_enabled = c->overlap && !sharded && !(e && e[0] == '0') &&
                            numel(c->ldims) < (1ull << 32);
+        const char* cs = std::getenv("CPDB_CHAIN_SIDE");
+        chain_side = c->overlap && !sharded && !(cs && cs[0] == '0');
     }
 
     // ---- factor state (factor_state.hpp:28-34) -----------------------------
@@ -319,7 +358,9 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32
         t.kind = is_root ? 0 : 1;
         CPDB_CK(cudaEventRecord(t.a, st));
     }
+    cudaEvent_t tla = tl_begin(st);
     run_ttm(c, src, sd, k, q, qp, R, dst, st, prefetch, no_pdl);
+    tl_end(tla, st, prefetch ? "root_prefetch" : is_root ? "root" : "branch");
     if (c->timing) {
         CPDB_CK(cudaEventRecord(t.b, st));
         const uint64_t nin = numel(sd);
@@ -406,20 +447,30 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     z.work = zwork.p;
     z.status = c->dstatus;
     // Z-QR depends only on R_k (k != n), final since the previous update's
-    // finisher: it runs on the side stream, overlapped with the TTM chain.
+    // finisher, and overlaps the TTM chain on a second stream.  Unsharded, the
+    // Z-QR follows the finisher on the main stream (programmatic launch: its
+    // 8-CTA cluster is resident before the chain's CTAs arrive, which would
+    // otherwise leave no GPC with 8 free SMs) and the chain runs on the side
+    // stream; sharded runs keep the chain (and its collectives) on the main one.
+    cudaStream_t zs = chain_side ? s : c->side;
     static const bool trace_phases = std::getenv("CPDB_PHASE_TRACE") != nullptr;
     if (trace_phases) {
         z.ts = reinterpret_cast<unsigned long long*>(zts.ensure(32));
-        CPDB_CK(cudaMemsetAsync(z.ts, 0, 32 * sizeof(double), c->side));
+        CPDB_CK(cudaMemsetAsync(z.ts, 0, 32 * sizeof(double), zs));
     }
     CPDB_CK(cudaEventRecord(ev_ready, s));
     CPDB_CK(cudaStreamWaitEvent(c->side, ev_ready, 0));
-    CPDB_CK(launch_zqr(z, c->side, c->sms));
-    CPDB_CK(cudaEventRecord(ev_zqr, c->side));
+    z.pdl = chain_side && !trace_phases ? 1 : 0;
+    tl_sweep = sweep;
+    tl_mode = n;
+    cudaEvent_t tla = tl_begin(zs);
+    CPDB_CK(launch_zqr(z, zs, c->sms));
+    tl_end(tla, zs, "zqr");
+    if (!chain_side) CPDB_CK(cudaEventRecord(ev_zqr, c->side));
     if (trace_phases) {
         unsigned long long ts[32];
-        CPDB_CK(cudaMemcpyAsync(ts, z.ts, sizeof ts, cudaMemcpyDeviceToHost, c->side));
-        CPDB_CK(cudaStreamSynchronize(c->side));
+        CPDB_CK(cudaMemcpyAsync(ts, z.ts, sizeof ts, cudaMemcpyDeviceToHost, zs));
+        CPDB_CK(cudaStreamSynchronize(zs));
         std::fprintf(stderr, "zqr mode %u phases(us):", n);
         for (int k = 1; k < 11; ++k)
             std::fprintf(stderr, " %d:%.2f", k, ts[k] ? (ts[k] - ts[0]) * 1e-3 : -1.0);
@@ -429,14 +480,15 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     if (observer) {
         std::vector<double> nat(zrows * R), ref(zrows * R);
         CPDB_CK(cudaMemcpyAsync(nat.data(), q0buf.p, zrows * R * sizeof(double),
-                                cudaMemcpyDeviceToHost, c->side));
-        CPDB_CK(cudaStreamSynchronize(c->side));
+                                cudaMemcpyDeviceToHost, zs));
+        CPDB_CK(cudaStreamSynchronize(zs));
         for (uint64_t i = 0; i < zrows; ++i)
             std::memcpy(&ref[perm[i] * R], &nat[i * R], R * sizeof(double));
         observer(user, sweep, n, ref.data(), zrows, R);
     }
     // 4. the scheduled TTM chain (execute, dim_tree.hpp:496-541)
-    bool after_wait = false;
+    const cudaStream_t ts = chain_side ? c->side : s;
+    bool after_wait = chain_side;  // the side stream's first kernel follows an event wait
     for (size_t si = 0; si < sw.updates[b].steps.size(); ++si) {
         const Step& st = sw.updates[b].steps[si];
         const double* src;
@@ -465,14 +517,16 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         od[st.contract] = R;
         if (si == 0 && pf.active && pf.sweep == sweep && pf.block == b) {
             // issued early by prefetch_root: adopt its buffer as the slot
-            CPDB_CK(cudaStreamWaitEvent(s, pf.ev, 0));
+            cudaEvent_t tlw = tl_begin(ts);
+            CPDB_CK(cudaStreamWaitEvent(ts, pf.ev, 0));
+            tl_end(tlw, ts, "adopt_wait");
             cache[st.produces].buf.swap(pre);
             pf.active = false;
             after_wait = true;
         } else {
             double* dst =
                 (st.produces == (1u << n)) ? ybuf[n].p : cache[st.produces].buf.ensure(numel(od));
-            ttm_step(src, sd, flags, st.contract, dst, st.source == root, nullptr, false,
+            ttm_step(src, sd, flags, st.contract, dst, st.source == root, ts, false,
                      after_wait);
             after_wait = false;
         }
@@ -494,6 +548,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     const std::vector<ModeSet> keep = retained_keys(plan, sweep - 1, b);
     for (auto& kv : cache)
         if (std::find(keep.begin(), keep.end(), kv.first) == keep.end()) kv.second.valid = false;
+    if (chain_side) CPDB_CK(cudaEventRecord(ev_zqr, c->side));  // join: V needs Y_(n)
 
 }
 
@@ -525,16 +580,26 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     const size_t part = size_t(vgemm_max_split()) * v.I * R;
     v.vpart = vpart.ensure(part);
     v.vfitpart = v.dual ? vfitpart.ensure(part) : nullptr;
-    CPDB_CK(cudaStreamWaitEvent(s, ev_zqr, 0));
-    CPDB_CK(launch_vgemm(v, s, c->sms));
-    c->launches += 1;
     // split-K partials -> V (this rank's rows; sharded mode-0 updates gather
     // the full V on every rank)
     const bool gather = (shard_flags(0, 0, 1u << n, n, sharded) & kGatherV) != 0;
     const uint64_t off = gather ? c->row_begin * R : 0;
-    CPDB_CK(reduce_splits(v.vpart, v.nsplit, v.I * R, vfull.p + off, s));
-    if (v.dual) CPDB_CK(reduce_splits(v.vfitpart, v.nsplit, v.I * R, vfitfull.p + off, s));
-    c->launches += v.dual ? 2 : 1;
+    v.v_out = vfull.p + off;
+    v.vfit_out = v.dual ? vfitfull.p + off : nullptr;
+    CPDB_CK(cudaStreamWaitEvent(s, ev_zqr, 0));
+    tl_sweep = sweep;
+    tl_mode = n;
+    cudaEvent_t tla = tl_begin(s);
+    CPDB_CK(launch_vgemm(v, s, c->sms));
+    tl_end(tla, s, "vgemm");
+    c->launches += 1;
+    if (!v.reduced) {
+        tla = tl_begin(s);
+        CPDB_CK(reduce_splits(v.vpart, v.nsplit, v.I * R, vfull.p + off, s));
+        if (v.dual) CPDB_CK(reduce_splits(v.vfitpart, v.nsplit, v.I * R, vfitfull.p + off, s));
+        tl_end(tla, s, "reduce");
+        c->launches += v.dual ? 2 : 1;
+    }
     if (gather) {
         allgather(c, vfull.p, v.I * R);
         if (v.dual) allgather(c, vfitfull.p, v.I * R);
@@ -565,7 +630,9 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
         f.ts = reinterpret_cast<unsigned long long*>(tsbuf.ensure(32));
         CPDB_CK(cudaMemsetAsync(f.ts, 0, 32 * sizeof(double), s));
     }
+    tla = tl_begin(s);
     CPDB_CK(launch_finish(f, s));
+    tl_end(tla, s, "finish");
     c->launches += 1;
     if (trace_phases) {
         unsigned long long ts[32];
@@ -692,6 +759,7 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         has_prev = true;
         if (fit >= cfg.fitness_threshold) converged = true;  // :301
     }
+    tl_flush();
     c->prof.sweeps = done - first_sweep;
     c->prof.mode_update_ms =
         c->prof.solve_ms - c->prof.root_ttm_ms - c->prof.branch_ttm_ms - c->prof.comm_ms;

@@ -59,9 +59,26 @@ struct Session {
     DevBuf pre;
     cudaEvent_t ev_fin = nullptr;
     bool prefetch_enabled = false;
+    bool chain_side = false;  // TTM chain on the side stream, Z-QR on the main one
     std::vector<Timer> timers;
     cudaEvent_t t_start = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_zqr = nullptr;  // main -> side -> main fork/join
+    // CPDB_TIMELINE=<csv>: an event pair around every launch site, written
+    // at the end of run() (diagnostic: the events cost PDL overlap)
+    struct Mark {
+        const char* label;
+        int stream;  // 0 main, 1 side, 2 low priority
+        uint64_t sweep;
+        uint32_t mode;
+        cudaEvent_t a, b;
+    };
+    const char* timeline = nullptr;
+    std::vector<Mark> marks;
+    uint64_t tl_sweep = 0;
+    uint32_t tl_mode = 0;
+    cudaEvent_t tl_begin(cudaStream_t st);
+    void tl_end(cudaEvent_t a, cudaStream_t st, const char* label);
+    void tl_flush();
 
     ~Session();
     void begin(cpdb_ctx* ctx, const cpdb_config& cfg, const cpdb_state* state);

@@ -9,6 +9,9 @@
 // bit-identical (solver_test.cpp:272-282 requires it).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "device.cuh"
 #include "kernels.hpp"
@@ -17,6 +20,8 @@
 
 namespace cpdb {
 namespace {
+
+namespace cg = cooperative_groups;
 
 // ------------------------------------------------------------------ norms
 constexpr int kNormThreads = 256;
@@ -135,19 +140,34 @@ vgemm_kernel(VgemmArgs a, uint64_t kchunk) {
 }
 
 // V-GEMM on the FP64 tensor cores.  CTA = 64 rows of V x all R columns over a
-// K-chunk (split-K, partials reduced in a fixed order by reduce_splits);
-// warp w owns rows 8w..8w+7 and the Rp/8 column blocks (DMMA m8n8k4).  Y and
-// P tiles (16 k) are staged in padded shared memory (conflict-free fragment
-// reads) with the next tile prefetched into registers; the extrapolation
-// P = Q0 + beta (Q0 - alpha H) is fused into the P tile load, and the DUAL
-// variant also accumulates Y Q0 for the fitness.
-constexpr int kDM = 64, kDK = 16, kDThreads = 256;
+// K-chunk; warp w owns rows 8w..8w+7 and the Rp/8 column blocks (DMMA
+// m8n8k4).  Y and P tiles (16 k) are staged in padded shared memory
+// (conflict-free fragment reads) with the next tile prefetched into
+// registers; the extrapolation P = Q0 + beta (Q0 - alpha H) is fused into the
+// P tile load, and the DUAL variant also accumulates Y Q0 for the fitness.
+// Two ways to combine the K-chunks, both in a fixed order (deterministic):
+//  * vgemm_cluster_kernel (very short K, C1): the 8 K-chunks of a
+//    row block are one thread-block cluster and are summed through
+//    distributed shared memory straight into V -- one launch, no partials;
+//  * vgemm_dmma_kernel (longer K, C2-C5): split-K partials in HBM, summed by
+//    reduce_splits.
+constexpr int kDM = 64, kDK = 16, kDThreads = 256, kVCluster = 8;
+// K-tiles per CTA up to which the cluster form is used: measured, it wins at
+// C1 (K = 100: 1 tile per CTA, 6020 -> 6310 sweeps/s) and loses at C4 / C2
+// (4 / 8 tiles per CTA run in sequence: -4% / -2% against 1-tile split-K
+// CTAs plus the reduction kernel)
+constexpr int kVClusterTiles = 2;
 
 template <int RM, bool DUAL>
-__global__ void __launch_bounds__(kDThreads)
-vgemm_dmma_kernel(VgemmArgs a, uint64_t kchunk) {
-    pdl_entry();
-    constexpr int RB = RM / 8 > 0 ? RM / 8 : 1;
+struct VAcc {
+    static constexpr int RB = RM / 8 > 0 ? RM / 8 : 1;
+    double v[RB][2], f[DUAL ? RB : 1][2];
+};
+
+template <int RM, bool DUAL>
+__device__ __forceinline__ void vgemm_tile(const VgemmArgs& a, uint64_t i0, uint32_t kb,
+                                           uint32_t ke, VAcc<RM, DUAL>& acc) {
+    constexpr int RB = VAcc<RM, DUAL>::RB;
     constexpr int YLD = kDK + 4;   // (m*YLD) mod 16 spaced by 4: conflict-free A reads
     constexpr int PLD = RM + 4;    // likewise for the B reads
     constexpr int YPT = kDM * kDK / kDThreads;  // 4 Y elements per thread
@@ -157,15 +177,15 @@ vgemm_dmma_kernel(VgemmArgs a, uint64_t kchunk) {
     __shared__ double fs[DUAL ? kDK * PLD : 1];
     const int R = a.R;
     const uint64_t I = a.I;
-    const uint32_t J = uint32_t(a.J), K = uint32_t(a.O * a.J);
-    const uint64_t i0 = uint64_t(blockIdx.x) * kDM;
-    const uint32_t kb = uint32_t(uint64_t(blockIdx.y) * kchunk);
-    const uint32_t ke = uint32_t(min(uint64_t(K), uint64_t(kb) + kchunk));
+    const uint32_t J = uint32_t(a.J);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool jrun = (J % kDK) == 0;  // a 16-k tile is 16 consecutive j of one o
 
-    double yr[YPT], pr[PPT], fr[DUAL ? PPT : 1];
-    auto fetch = [&](uint32_t k0) {
+    // two register sets: tiles t+1 and t+2 are in flight during tile t's MMAs
+    struct Regs {
+        double y[YPT], p[PPT], f[DUAL ? PPT : 1];
+    };
+    auto fetch = [&](Regs& rg, uint32_t k0) {
 #pragma unroll
         for (int u = 0; u < YPT; ++u) {
             const int e = threadIdx.x + u * kDThreads;
@@ -177,7 +197,7 @@ vgemm_dmma_kernel(VgemmArgs a, uint64_t kchunk) {
                 const uint32_t o = k / J, j = k - o * J;
                 v = a.y[(uint64_t(o) * I + i) * J + j];
             }
-            yr[u] = v;
+            rg.y[u] = v;
         }
 #pragma unroll
         for (int u = 0; u < PPT; ++u) {
@@ -189,53 +209,80 @@ vgemm_dmma_kernel(VgemmArgs a, uint64_t kchunk) {
                 q = a.q0[uint64_t(k) * R + r];
                 p = a.extrap ? q + a.beta * (q - a.alpha * a.hist[uint64_t(k) * R + r]) : q;
             }
-            pr[u] = p;
-            if (DUAL) fr[u] = q;
+            rg.p[u] = p;
+            if (DUAL) rg.f[u] = q;
         }
     };
-    auto stash = [&]() {
+    auto stash = [&](const Regs& rg) {
 #pragma unroll
         for (int u = 0; u < YPT; ++u) {
             const int e = threadIdx.x + u * kDThreads;
             const int m = jrun ? e / kDK : e % kDM, c = jrun ? e % kDK : e / kDM;
-            ys[m * YLD + c] = yr[u];
+            ys[m * YLD + c] = rg.y[u];
         }
 #pragma unroll
         for (int u = 0; u < PPT; ++u) {
             const int e = threadIdx.x + u * kDThreads;
             if (e < kDK * RM) {
-                ps[(e / RM) * PLD + e % RM] = pr[u];
-                if (DUAL) fs[(e / RM) * PLD + e % RM] = fr[u];
+                ps[(e / RM) * PLD + e % RM] = rg.p[u];
+                if (DUAL) fs[(e / RM) * PLD + e % RM] = rg.f[u];
             }
         }
     };
-
-    double acc[RB][2], accf[DUAL ? RB : 1][2];
-#pragma unroll
-    for (int b = 0; b < RB; ++b) acc[b][0] = acc[b][1] = 0.0;
-#pragma unroll
-    for (int b = 0; b < (DUAL ? RB : 1); ++b) accf[b][0] = accf[b][1] = 0.0;
-
-    if (kb < ke) fetch(kb);
-    for (uint32_t k0 = kb; k0 < ke; k0 += kDK) {
-        stash();
-        __syncthreads();
-        if (k0 + kDK < ke) fetch(k0 + kDK);  // next tile in flight during the MMAs
+    auto mma = [&]() {
 #pragma unroll
         for (int s4 = 0; s4 < kDK / 4; ++s4) {
             const double av = ys[(warp * 8 + (lane >> 2)) * YLD + 4 * s4 + (lane & 3)];
 #pragma unroll
             for (int b = 0; b < RB; ++b) {
                 const double bv = ps[(4 * s4 + (lane & 3)) * PLD + b * 8 + (lane >> 2)];
-                dmma(acc[b][0], acc[b][1], av, bv);
+                dmma(acc.v[b][0], acc.v[b][1], av, bv);
                 if (DUAL) {
                     const double fv = fs[(4 * s4 + (lane & 3)) * PLD + b * 8 + (lane >> 2)];
-                    dmma(accf[b][0], accf[b][1], av, fv);
+                    dmma(acc.f[b][0], acc.f[b][1], av, fv);
                 }
             }
         }
+    };
+
+#pragma unroll
+    for (int b = 0; b < RB; ++b) acc.v[b][0] = acc.v[b][1] = 0.0;
+#pragma unroll
+    for (int b = 0; b < (DUAL ? RB : 1); ++b) acc.f[b][0] = acc.f[b][1] = 0.0;
+
+    Regs ra, rb;
+    if (kb < ke) fetch(ra, kb);
+    if (kb + kDK < ke) fetch(rb, kb + kDK);
+    for (uint32_t k0 = kb; k0 < ke; k0 += 2 * kDK) {
+        stash(ra);
         __syncthreads();
+        if (k0 + 2 * kDK < ke) fetch(ra, k0 + 2 * kDK);
+        mma();
+        __syncthreads();
+        if (k0 + kDK < ke) {
+            stash(rb);
+            __syncthreads();
+            if (k0 + 3 * kDK < ke) fetch(rb, k0 + 3 * kDK);
+            mma();
+            __syncthreads();
+        }
     }
+}
+
+template <int RM, bool DUAL>
+__global__ void __launch_bounds__(kDThreads)
+vgemm_dmma_kernel(VgemmArgs a, uint64_t kchunk) {
+    pdl_entry();
+    constexpr int RB = VAcc<RM, DUAL>::RB;
+    const int R = a.R;
+    const uint64_t I = a.I;
+    const uint32_t K = uint32_t(a.O * a.J);
+    const uint64_t i0 = uint64_t(blockIdx.x) * kDM;
+    const uint32_t kb = uint32_t(uint64_t(blockIdx.y) * kchunk);
+    const uint32_t ke = uint32_t(min(uint64_t(K), uint64_t(kb) + kchunk));
+    VAcc<RM, DUAL> acc;
+    vgemm_tile<RM, DUAL>(a, i0, kb, ke, acc);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint64_t i = i0 + warp * 8 + (lane >> 2);
     if (i < I) {
         double* vp = a.vpart + (uint64_t(blockIdx.y) * I + i) * R;
@@ -244,15 +291,60 @@ vgemm_dmma_kernel(VgemmArgs a, uint64_t kchunk) {
         for (int b = 0; b < RB; ++b) {
             const int r = b * 8 + 2 * (lane & 3);
             if (r < R) {
-                vp[r] = acc[b][0];
-                if (DUAL) fp[r] = accf[b][0];
+                vp[r] = acc.v[b][0];
+                if (DUAL) fp[r] = acc.f[b][0];
             }
             if (r + 1 < R) {
-                vp[r + 1] = acc[b][1];
-                if (DUAL) fp[r + 1] = accf[b][1];
+                vp[r + 1] = acc.v[b][1];
+                if (DUAL) fp[r + 1] = acc.f[b][1];
             }
         }
     }
+}
+
+// grid (row blocks, 8), cluster (1, 8): CTA y sums K-chunk y; the chunks'
+// 64 x RM accumulators meet in shared memory and CTA y reduces rows
+// 8y..8y+7 of the block over the cluster in rank order.
+template <int RM, bool DUAL>
+__global__ void __launch_bounds__(kDThreads)
+vgemm_cluster_kernel(VgemmArgs a, uint32_t kchunk) {
+    constexpr int RB = VAcc<RM, DUAL>::RB, NV = DUAL ? 2 : 1;
+    extern __shared__ double red[];  // NV x kDM x RM
+    cg::cluster_group cl = cg::this_cluster();
+    const int R = a.R;
+    const uint64_t I = a.I;
+    const uint32_t K = uint32_t(a.O * a.J);
+    const uint64_t i0 = uint64_t(blockIdx.x) * kDM;
+    const uint32_t kb = min(K, uint32_t(blockIdx.y) * kchunk);
+    const uint32_t ke = min(K, kb + kchunk);
+    VAcc<RM, DUAL> acc;
+    vgemm_tile<RM, DUAL>(a, i0, kb, ke, acc);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int row = warp * 8 + (lane >> 2);
+#pragma unroll
+    for (int b = 0; b < RB; ++b) {
+        const int c = b * 8 + 2 * (lane & 3);
+        red[row * RM + c] = acc.v[b][0];
+        red[row * RM + c + 1] = acc.v[b][1];
+        if (DUAL) {
+            red[kDM * RM + row * RM + c] = acc.f[b][0];
+            red[kDM * RM + row * RM + c + 1] = acc.f[b][1];
+        }
+    }
+    cl.sync();
+    const int rank = int(cl.block_rank());
+    constexpr int kRows = kDM / kVCluster;
+    for (int e = threadIdx.x; e < NV * kRows * RM; e += kDThreads) {
+        const int v = e / (kRows * RM), rr = (e / RM) % kRows, c = e % RM;
+        const int off = v * kDM * RM + (rank * kRows + rr) * RM + c;
+        double t[kVCluster];
+#pragma unroll
+        for (int q = 0; q < kVCluster; ++q) t[q] = cl.map_shared_rank(red, q)[off];
+        const double sum = ((t[0] + t[1]) + (t[2] + t[3])) + ((t[4] + t[5]) + (t[6] + t[7]));
+        const uint64_t i = i0 + rank * kRows + rr;
+        if (i < I && c < R) (v ? a.vfit_out : a.v_out)[i * R + c] = sum;
+    }
+    cl.sync();  // keep every CTA's shared memory alive until all ranks have read it
 }
 
 // ------------------------------------------------------------------ misc kernels
@@ -386,6 +478,38 @@ __global__ void permute_rows_kernel(const double* in, double* out, const uint64_
 template <int RM, bool DUAL>
 cudaError_t vgemm_run(VgemmArgs& a, cudaStream_t s, int sms) {
     const uint64_t K = a.O * a.J;
+    a.reduced = 0;
+    // short K: one cluster per 64-row block, chunks summed on chip
+    static const bool cluster_ok = [] {
+        const char* e = std::getenv("CPDB_VGEMM_CLUSTER");
+        return !(e && e[0] == '0');
+    }();
+    if (RM >= 8 && cluster_ok && a.v_out && (!DUAL || a.vfit_out) &&
+        (K + kDK - 1) / kDK <= uint64_t(kVCluster) * kVClusterTiles) {
+        const uint64_t iblocks = (a.I + kDM - 1) / kDM;
+        const uint64_t ktiles = (K + kDK - 1) / kDK;
+        const uint32_t kchunk = uint32_t((ktiles + kVCluster - 1) / kVCluster) * kDK;
+        const size_t smem = size_t(DUAL ? 2 : 1) * kDM * RM * sizeof(double);
+        cudaError_t e = cudaFuncSetAttribute(vgemm_cluster_kernel<RM, DUAL>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(smem));
+        if (e != cudaSuccess) return e;
+        cudaLaunchConfig_t c{};
+        c.gridDim = dim3(unsigned(iblocks), kVCluster, 1);
+        c.blockDim = dim3(kDThreads, 1, 1);
+        c.dynamicSmemBytes = smem;
+        c.stream = s;
+        cudaLaunchAttribute attr[1];
+        attr[0].id = cudaLaunchAttributeClusterDimension;
+        attr[0].val.clusterDim.x = 1;
+        attr[0].val.clusterDim.y = kVCluster;
+        attr[0].val.clusterDim.z = 1;
+        c.attrs = attr;
+        c.numAttrs = 1;  // plain launch: V waits on the Z-QR / chain event
+        a.nsplit = 1;
+        a.reduced = 1;
+        return cudaLaunchKernelEx(&c, vgemm_cluster_kernel<RM, DUAL>, a, kchunk);
+    }
     if (RM >= 8 && K < (1ull << 32)) {  // DMMA path
         const uint64_t iblocks = (a.I + kDM - 1) / kDM;
         const uint64_t ktiles = (K + kDK - 1) / kDK;
