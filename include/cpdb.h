@@ -42,6 +42,7 @@ extern "C" {
 #define CPDB_OUT_OF_MEMORY 7
 #define CPDB_FILE_ERROR 8           /* file_error   io.hpp:21-23 (open/read/write)  */
 #define CPDB_FORMAT_ERROR 9         /* format_error io.hpp:25-27 (malformed file)   */
+#define CPDB_SINGULAR_SYSTEM 10     /* singular_system_error linalg.hpp (solve_spd) */
 
 #define CPDB_MAX_ORDER 8
 #define CPDB_ROOT_KEY 0xFFFFFFFFu   /* "the input tensor X" as a step source       */
@@ -197,6 +198,34 @@ int cpdb_profile_get(cpdb_ctx* ctx, cpdb_profile* out);
  * the preceding update; off runs every TTM in schedule order on the solve
  * stream -- the kernel alone, e.g. for roofline measurements). */
 int cpdb_set_options(cpdb_ctx* ctx, int32_t timing, int32_t overlap);
+
+/* ---- CP-ALS through the normal equations ---------- */
+/* reference: solvers.hpp:149-208 cp_als.  Device-resident run on the
+ * context's tensor: per mode MTTKRP (TTM + Khatri-Rao contraction), Gamma =
+ * Hadamard of the other Grams, solve_spd, normalize_columns, Gram; fitness
+ * (fitness_fast_als) once per sweep.  init_factors (sum I_k x R, mode after
+ * mode) / init_lambda (R) are the optional KruskalModel init; trace has
+ * max_iterations rows (root_ttm_count 0, beta_used 0, regularized = a ridge
+ * retry happened in the sweep).  CPDB_SINGULAR_SYSTEM when the ridge fails. */
+int cpdb_als_solve(cpdb_ctx* ctx, const cpdb_config* cfg, const double* init_lambda,
+                   const double* init_factors, cpdb_trace_row* trace, uint64_t* trace_len,
+                   double* out_lambda, double* out_factors);
+/* reference: tensor.hpp:453-488 mttkrp (and :494-518 mttkrp_materialized,
+ * the same product).  t: host tensor; factors[k]: host I_k x R (factors[mode]
+ * unused, may be NULL) with their shapes; out: dims[mode] x R. */
+int cpdb_mttkrp(cpdb_ctx* ctx, const double* t, const uint64_t* dims, uint32_t order,
+                const double* const* factors, const uint64_t* factor_rows,
+                const uint64_t* factor_cols, uint32_t mode, double* out);
+/* reference: linalg.hpp:132-187 solve_spd: x G = rhs (x, rhs: rows x n),
+ * Cholesky with one 1e-12 trace/n ridge retry (*regularized = 1). */
+int cpdb_solve_spd(cpdb_ctx* ctx, const double* g, uint64_t g_rows, uint64_t g_cols,
+                   const double* rhs, uint64_t rows, uint64_t cols, double* x,
+                   int32_t* regularized);
+/* reference: kruskal.hpp:88-104 fitness_fast_als. */
+int cpdb_fitness_fast_als(cpdb_ctx* ctx, double norm_x_sq, const double* m, const double* a_hat,
+                          uint64_t rows, uint64_t cols, const double* gamma,
+                          const double* lambda, uint64_t r, const double* s_last,
+                          double* fitness, double* raw);
 
 /* ---- dense primitives on host buffers (device compute) ------------------------ */
 int cpdb_ttm(cpdb_ctx* ctx, const double* t, const uint64_t* dims, uint32_t order,

@@ -413,6 +413,61 @@ class Oracle:
                              prev_fitness=float(st.prev_fitness) if st.has_prev_fitness else None)
         return res
 
+    # ---- CP-ALS, normal equations (solvers.hpp:149-208) --------------------
+    def cp_als(self, x: np.ndarray, rank: int, iterations: int, *, seed: int = 0,
+               fitness_threshold: float = 1.0, init_lam=None, init_factors=None) -> SolveOut:
+        x = np.ascontiguousarray(x, dtype=np.float64)
+        dims = list(x.shape)
+        cfg = Config(rank=rank, max_iterations=iterations, fitness_threshold=fitness_threshold,
+                     strategy=0, extrapolate=0, alpha=0.1, has_beta_override=0, beta_override=0.0,
+                     activation_gap=0.03, seed=seed)
+        trace = (TraceRow * iterations)()
+        tlen = C.c_uint64()
+        lam = np.empty(rank)
+        fac = np.empty(sum(d * rank for d in dims))
+        il = None if init_lam is None else np.ascontiguousarray(init_lam, dtype=np.float64)
+        ifa = None if init_factors is None else np.concatenate(
+            [np.ascontiguousarray(f, dtype=np.float64).ravel() for f in init_factors])
+        self._check(self._f("cp_als")(_dp(x), _u64(dims).ctypes.data_as(_U64P), C.c_uint32(len(dims)),
+                                      C.byref(cfg), None if il is None else _dp(il),
+                                      None if ifa is None else _dp(ifa), trace, C.byref(tlen),
+                                      _dp(lam), _dp(fac)))
+        out, off = [], 0
+        for d in dims:
+            out.append(fac[off:off + d * rank].reshape(d, rank).copy())
+            off += d * rank
+        return SolveOut(trace=trace_to_dicts(trace, tlen.value), lam=lam, factors=out)
+
+    def mttkrp(self, t: np.ndarray, factors, mode: int) -> np.ndarray:
+        t = np.ascontiguousarray(t, dtype=np.float64)
+        ms = [None if f is None else np.ascontiguousarray(f, dtype=np.float64) for f in factors]
+        rank = next(m.shape[1] for k, m in enumerate(ms) if k != mode and m is not None)
+        ptrs = (_P * len(ms))(*[None if m is None else _dp(m) for m in ms])
+        out = np.empty((t.shape[mode], rank))
+        self._check(self._f("mttkrp")(_dp(t), _u64(t.shape).ctypes.data_as(_U64P),
+                                      C.c_uint32(t.ndim), ptrs, C.c_uint64(rank),
+                                      C.c_uint32(mode), _dp(out)))
+        return out
+
+    def solve_spd(self, g: np.ndarray, rhs: np.ndarray):
+        g = np.ascontiguousarray(g, dtype=np.float64)
+        rhs = np.ascontiguousarray(rhs, dtype=np.float64)
+        x = np.empty_like(rhs)
+        reg = C.c_int32()
+        self._check(self._f("solve_spd")(_dp(g), C.c_uint64(g.shape[0]), _dp(rhs),
+                                         C.c_uint64(rhs.shape[0]), _dp(x), C.byref(reg)))
+        return x, bool(reg.value)
+
+    def fitness_fast_als(self, nx2, m, a_hat, gamma, lam, s_last):
+        m, a_hat, gamma, lam, s_last = (np.ascontiguousarray(z, dtype=np.float64)
+                                        for z in (m, a_hat, gamma, lam, s_last))
+        fit, raw = C.c_double(), C.c_double()
+        self._check(self._f("fitness_fast_als")(C.c_double(nx2), _dp(m), _dp(a_hat),
+                                                C.c_uint64(m.shape[0]), C.c_uint64(m.shape[1]),
+                                                _dp(gamma), _dp(lam), C.c_uint64(lam.size),
+                                                _dp(s_last), C.byref(fit), C.byref(raw)))
+        return fit.value, raw.value
+
     def synth_baseline(self, kind: int, dims, rank: int, rho: float, seed: int,
                        want_truth: bool = False):
         d = _u64(dims)

@@ -27,12 +27,17 @@
 //   cpdref_solve            solvers.hpp:317-336  cp_als_qr / als_qr_bre, or a
 //                           loop-for-loop mirror of run_qr (solvers.hpp:215-309)
 //                           when a resume state or per-sweep dumps are requested
+//   cpdref_cp_als           solvers.hpp:149-208  cp_als (normal equations)
+//   cpdref_mttkrp           tensor.hpp:453-488   mttkrp (streaming path)
+//   cpdref_solve_spd        linalg.hpp:132-187   solve_spd
+//   cpdref_fitness_fast_als kruskal.hpp:88-104   fitness_fast_als
 //   cpdref_synth_baseline   BASELINE.json configs built from rng.hpp +
 //                           kruskal.hpp:54-67 reconstruct
 #include <cmath>
 #include <cstdint>
 #include <cstring>
 #include <optional>
+#include <span>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -61,6 +66,7 @@ enum : int {
     kSingularTriangular = 3,
     kLogic = 4,
     kOther = 5,
+    kSingularSystem = 10,
 };
 
 template <class F>
@@ -74,6 +80,9 @@ int guarded(F&& body) {
     } catch (const cpd::singular_triangular_error& e) {
         g_error = e.what();
         return kSingularTriangular;
+    } catch (const cpd::singular_system_error& e) {
+        g_error = e.what();
+        return kSingularSystem;
     } catch (const std::invalid_argument& e) {
         g_error = e.what();
         return kInvalidArgument;
@@ -650,6 +659,78 @@ int cpdref_assemble_noisy(const uint64_t* dims, uint32_t order, uint64_t rank,
         spec.seed = seed;
         const cpd::SynthResult r = cpd::assemble_noisy_tensor(spec);
         std::memcpy(out, r.tensor.data(), r.tensor.size() * sizeof(double));
+    });
+}
+
+int cpdref_cp_als(const double* x, const uint64_t* dims, uint32_t order, const cpdo_config* cfg,
+                  const double* init_lambda, const double* init_factors, cpdo_trace_row* trace,
+                  uint64_t* trace_len, double* out_lambda, double* out_factors) {
+    return guarded([&] {
+        const cpd::DenseTensor t = make_tensor(x, dims, order);
+        cpd::SolverConfig c = config_of(*cfg);
+        c.algorithm = cpd::Algorithm::als;
+        std::optional<cpd::KruskalModel> init;
+        if (init_factors) {
+            cpd::KruskalModel m;
+            m.lambda.assign(init_lambda, init_lambda + cfg->rank);
+            const double* p = init_factors;
+            for (uint32_t k = 0; k < order; ++k) {
+                m.factors.push_back(make_matrix(p, dims[k], cfg->rank));
+                p += dims[k] * cfg->rank;
+            }
+            init = std::move(m);
+        }
+        const cpd::SolveResult r = cpd::cp_als(t, c, init);
+        for (std::size_t i = 0; i < r.trace.size(); ++i)
+            if (trace) put_row(r.trace[i], trace + i);
+        if (trace_len) *trace_len = r.trace.size();
+        if (out_lambda)
+            std::memcpy(out_lambda, r.model.lambda.data(), r.model.lambda.size() * sizeof(double));
+        if (out_factors) {
+            double* p = out_factors;
+            for (const auto& f : r.model.factors) {
+                put(f, p);
+                p += f.size();
+            }
+        }
+    });
+}
+
+int cpdref_mttkrp(const double* t, const uint64_t* dims, uint32_t order,
+                  const double* const* factors, uint64_t rank, uint32_t mode, double* out) {
+    return guarded([&] {
+        const cpd::DenseTensor x = make_tensor(t, dims, order);
+        std::vector<cpd::Matrix> mats(order);
+        std::vector<const cpd::Matrix*> ptrs(order, nullptr);
+        for (uint32_t k = 0; k < order; ++k) {
+            if (k == mode || !factors[k]) continue;
+            mats[k] = make_matrix(factors[k], dims[k], rank);
+            ptrs[k] = &mats[k];
+        }
+        put(cpd::mttkrp(x, std::span<const cpd::Matrix* const>(ptrs.data(), ptrs.size()), mode),
+            out);
+    });
+}
+
+int cpdref_solve_spd(const double* g, uint64_t n, const double* rhs, uint64_t rows, double* x,
+                     int32_t* regularized) {
+    return guarded([&] {
+        const auto r = cpd::solve_spd(make_matrix(g, n, n), make_matrix(rhs, rows, n));
+        put(r.x, x);
+        if (regularized) *regularized = r.regularized ? 1 : 0;
+    });
+}
+
+int cpdref_fitness_fast_als(double nx2, const double* m, const double* a_hat, uint64_t rows,
+                            uint64_t cols, const double* gamma, const double* lambda, uint64_t r,
+                            const double* s_last, double* fitness, double* raw) {
+    return guarded([&] {
+        const cpd::FitnessResult f = cpd::fitness_fast_als(
+            nx2, make_matrix(m, rows, cols), make_matrix(a_hat, rows, cols),
+            make_matrix(gamma, r, r), std::vector<double>(lambda, lambda + r),
+            make_matrix(s_last, r, r));
+        *fitness = f.fitness;
+        *raw = f.raw_radicand;
     });
 }
 

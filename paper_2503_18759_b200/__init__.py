@@ -67,6 +67,10 @@ class FormatError(CpdError):
     """io.hpp:25-27 format_error (malformed .cpdt payload)"""
 
 
+class SingularSystemError(CpdError):
+    """linalg.hpp:15-17 singular_system_error (solve_spd failed after the ridge)"""
+
+
 def _lib():
     return _cpdb.load()
 
@@ -87,6 +91,8 @@ def _raise(rc: int, column: int = -1):
         raise FileError(rc, msg)
     if rc == _cpdb.FORMAT_ERROR:
         raise FormatError(rc, msg)
+    if rc == _cpdb.SINGULAR_SYSTEM:
+        raise SingularSystemError(rc, msg)
     raise CudaError(rc, msg)
 
 
@@ -304,6 +310,38 @@ class Context:
         return res
 
 
+    def solve_als(self, cfg: "SolverConfig", init: Optional["KruskalModel"] = None) -> "SolveResult":
+        """cp_als (solvers.hpp:149-208) on this context's tensor (cpdb_als_solve)."""
+        dims = self.dims
+        R = int(cfg.rank)
+        c = _config(cfg, False)
+        iters = int(cfg.max_iterations)
+        trace = (_cpdb.TraceRow * iters)()
+        tlen = C.c_uint64()
+        lam = np.empty(R)
+        fac = np.empty(sum(d * R for d in dims))
+        il = if_ = None
+        if init is not None:
+            if len(init.factors) != len(dims) or init.rank() != R:
+                raise CpdInvalidArgument(_cpdb.INVALID_ARGUMENT,
+                                         "solver: init model does not match tensor/config")
+            for f, d in zip(init.factors, dims):
+                if np.asarray(f).shape[0] != d:
+                    raise CpdInvalidArgument(_cpdb.INVALID_ARGUMENT,
+                                             "solver: init factor rows do not match tensor")
+            il = _f64(init.lam).copy()
+            if_ = np.concatenate([_f64(f).ravel() for f in init.factors])
+        _raise(_lib().cpdb_als_solve(self._h, C.byref(c), None if il is None else _p(il),
+                                     None if if_ is None else _p(if_), trace, C.byref(tlen),
+                                     _p(lam), _p(fac)))
+        out, off = [], 0
+        for d in dims:
+            out.append(fac[off:off + d * R].reshape(d, R).copy())
+            off += d * R
+        rows = [TraceRow.from_c(trace[i]) for i in range(tlen.value)]
+        return SolveResult(model=KruskalModel(lam.copy(), out), trace=rows)
+
+
 def _config(cfg: "SolverConfig", extrapolate: bool) -> _cpdb.Config:
     return _cpdb.Config(rank=int(cfg.rank), max_iterations=int(cfg.max_iterations),
                         fitness_threshold=float(cfg.fitness_threshold),
@@ -463,7 +501,66 @@ def als_qr_bre(x, cfg: SolverConfig, init: Optional[KruskalModel] = None,
     return _solve(x, cfg, init, True, ctx, **kw)
 
 
+def cp_als(x, cfg: SolverConfig, init: Optional[KruskalModel] = None,
+           ctx: Optional[Context] = None) -> SolveResult:
+    """solvers.hpp:149-208 (normal equations + MTTKRP)"""
+    if cfg.algorithm not in ("als",):
+        raise CpdInvalidArgument(_cpdb.INVALID_ARGUMENT, "cp_als: config algorithm must be als")
+    ctx = ctx or default_context()
+    ctx.set_tensor(_f64(x))
+    return ctx.solve_als(cfg, init)
+
+
 # ---------------------------------------------------------------- primitives
+def mttkrp(t, factors: Sequence[Optional[np.ndarray]], mode: int,
+           ctx: Optional[Context] = None) -> np.ndarray:
+    """tensor.hpp:453-488 (factors[mode] is not read)"""
+    ctx = ctx or default_context()
+    t = _f64(t)
+    order = t.ndim
+    if len(factors) != order:
+        raise CpdInvalidArgument(_cpdb.INVALID_ARGUMENT, "mttkrp: need one factor per mode")
+    mats = [None if f is None else _f64(f) for f in factors]
+    ptrs = (_cpdb.P * order)(*[None if m is None else _p(m) for m in mats])
+    rows = _u64([0 if m is None else m.shape[0] for m in mats])
+    cols = _u64([0 if m is None else (m.shape[1] if m.ndim == 2 else 1) for m in mats])
+    rank = next((int(c) for k, c in enumerate(cols) if k != mode and mats[k] is not None), 0)
+    out = np.empty((t.shape[mode] if 0 <= mode < order else 0, max(rank, 1)))
+    _raise(_lib().cpdb_mttkrp(ctx.handle, _p(t.ravel()), _up(_u64(t.shape)), order, ptrs,
+                              _up(rows), _up(cols), mode, _p(out)))
+    return out
+
+
+def solve_spd(g, rhs, ctx: Optional[Context] = None) -> Tuple[np.ndarray, bool]:
+    """linalg.hpp:132-187 -> (x, regularized) with x G = rhs"""
+    ctx = ctx or default_context()
+    g, rhs = _f64(g), _f64(rhs)
+    x = np.empty_like(rhs)
+    reg = C.c_int32()
+    _raise(_lib().cpdb_solve_spd(ctx.handle, _p(g), g.shape[0], g.shape[1], _p(rhs), rhs.shape[0],
+                                 rhs.shape[1], _p(x), C.byref(reg)))
+    return x, bool(reg.value)
+
+
+def fitness_fast_als(norm_x_sq, m_last, a_hat_last, gamma_last, lam, s_last,
+                     ctx: Optional[Context] = None):
+    """kruskal.hpp:88-104 -> (fitness, raw_radicand)"""
+    ctx = ctx or default_context()
+    m, a, g, lam, s = (_f64(z) for z in (m_last, a_hat_last, gamma_last, lam, s_last))
+    if not norm_x_sq > 0.0:
+        raise CpdInvalidArgument(_cpdb.INVALID_ARGUMENT, "fitness_fast_als: zero-norm tensor")
+    if m.shape != a.shape:
+        raise CpdInvalidArgument(_cpdb.INVALID_ARGUMENT, "dot: dimension mismatch")
+    r = lam.size
+    if g.shape[0] != r or s.shape[0] != r:
+        raise CpdInvalidArgument(_cpdb.INVALID_ARGUMENT, "fitness_fast_als: dimension mismatch")
+    fit, raw = C.c_double(), C.c_double()
+    _raise(_lib().cpdb_fitness_fast_als(ctx.handle, float(norm_x_sq), _p(m), _p(a), m.shape[0],
+                                        m.shape[1], _p(g), _p(lam), r, _p(s), C.byref(fit),
+                                        C.byref(raw)))
+    return fit.value, raw.value
+
+
 def ttm(t, b, mode: int, ctx: Optional[Context] = None) -> np.ndarray:
     """tensor.hpp:288-315: Y = t x_mode b, b is (rows x I_mode)."""
     ctx = ctx or default_context()

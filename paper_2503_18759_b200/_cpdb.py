@@ -16,7 +16,7 @@ MAX_ORDER = 8
 ROOT_KEY = 0xFFFFFFFF
 
 OK, INVALID_ARGUMENT, STALE_INTERMEDIATE, SINGULAR_TRIANGULAR, LOGIC_ERROR, CUDA_ERROR, \
-    NCCL_ERROR, OUT_OF_MEMORY, FILE_ERROR, FORMAT_ERROR = range(10)
+    NCCL_ERROR, OUT_OF_MEMORY, FILE_ERROR, FORMAT_ERROR, SINGULAR_SYSTEM = range(11)
 
 
 class TraceRow(C.Structure):
@@ -131,6 +131,12 @@ SIGNATURES = {
     "cpdb_fitness_fast_qr": (C.c_int, [CTX, C.c_double, P, P, C.c_uint64, P, P, P, C.c_uint64, P,
                                        P]),
     "cpdb_inner": (C.c_int, [CTX, P, P, C.c_uint64, P]),
+    "cpdb_als_solve": (C.c_int, [CTX, C.POINTER(Config), P, P, C.POINTER(TraceRow), U64P, P, P]),
+    "cpdb_mttkrp": (C.c_int, [CTX, P, U64P, C.c_uint32, C.POINTER(P), U64P, U64P, C.c_uint32, P]),
+    "cpdb_solve_spd": (C.c_int, [CTX, P, C.c_uint64, C.c_uint64, P, C.c_uint64, C.c_uint64, P,
+                                 C.POINTER(C.c_int32)]),
+    "cpdb_fitness_fast_als": (C.c_int, [CTX, C.c_double, P, P, C.c_uint64, C.c_uint64, P, P,
+                                        C.c_uint64, P, P, P]),
     "cpdb_select_beta": (C.c_int, [C.c_double, C.c_double, C.c_double, P]),
     "cpdb_schedule_build": (C.c_int, [C.c_uint32, C.c_int32, C.c_uint64, I64P, C.c_uint64, U64P,
                                       U64P]),

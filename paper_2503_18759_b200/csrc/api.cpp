@@ -609,6 +609,117 @@ int cpdb_fitness_fast_qr(cpdb_ctx* c, double nx2, const double* v, const double*
     });
 }
 
+int cpdb_als_solve(cpdb_ctx* c, const cpdb_config* cfg, const double* init_lambda,
+                   const double* init_factors, cpdb_trace_row* trace, uint64_t* trace_len,
+                   double* out_lambda, double* out_factors) {
+    return guarded([&] {
+        use_device(c);
+        if (!cfg) fail(CPDB_INVALID_ARGUMENT, "null config");
+        cpdb::als_solve(c, *cfg, init_lambda, init_factors, trace, trace_len, out_lambda,
+                        out_factors);
+    });
+}
+
+int cpdb_mttkrp(cpdb_ctx* c, const double* t, const uint64_t* dims, uint32_t order,
+                const double* const* factors, const uint64_t* factor_rows,
+                const uint64_t* factor_cols, uint32_t mode, double* out) {
+    return guarded([&] {
+        use_device(c);
+        const std::vector<uint64_t> d = dims_of(dims, order);
+        // check_mttkrp_args (tensor.hpp:415-431)
+        if (mode >= order) fail(CPDB_INVALID_ARGUMENT, "mttkrp: mode out of range");
+        if (!factors || !factor_rows || !factor_cols)
+            fail(CPDB_INVALID_ARGUMENT, "mttkrp: need one factor per mode");
+        uint64_t rank = 0;
+        for (uint32_t k = 0; k < order; ++k) {
+            if (k == mode) continue;
+            if (!factors[k]) fail(CPDB_INVALID_ARGUMENT, "mttkrp: missing factor");
+            if (rank == 0) rank = factor_cols[k];
+            if (factor_cols[k] != rank) fail(CPDB_INVALID_ARGUMENT, "mttkrp: mismatched ranks");
+            if (factor_rows[k] != d[k])
+                fail(CPDB_INVALID_ARGUMENT, "mttkrp: factor rows do not match mode extent");
+        }
+        if (rank == 0) fail(CPDB_INVALID_ARGUMENT, "mttkrp: order must be >= 2");
+        if (rank > 64) fail(CPDB_INVALID_ARGUMENT, "mttkrp: ranks above 64 are not supported");
+        const uint32_t R = uint32_t(rank);
+        const uint64_t nx = cpdb::numel(d);
+        uint64_t nf = 0;
+        for (uint32_t k = 0; k < order; ++k)
+            if (k != mode) nf += d[k] * R;
+        double* dx = c->scratch_a.ensure(nx);
+        double* df = c->scratch_b.ensure(nf + d[mode] * R);
+        upload(c, dx, t, nx);
+        std::vector<const double*> fac(order, nullptr);
+        uint64_t off = 0;
+        for (uint32_t k = 0; k < order; ++k) {
+            if (k == mode) continue;
+            upload(c, df + off, factors[k], d[k] * R);
+            fac[k] = df + off;
+            off += d[k] * R;
+        }
+        double* dm = df + nf;
+        cpdb::mttkrp_primitive(c, dx, d, fac, R, mode, dm);
+        download(c, out, dm, d[mode] * R);
+    });
+}
+
+int cpdb_solve_spd(cpdb_ctx* c, const double* g, uint64_t g_rows, uint64_t g_cols,
+                   const double* rhs, uint64_t rows, uint64_t cols, double* x,
+                   int32_t* regularized) {
+    return guarded([&] {
+        use_device(c);
+        // linalg.hpp:133-135
+        if (g_cols != g_rows) fail(CPDB_INVALID_ARGUMENT, "solve_spd: G must be square");
+        if (cols != g_rows) fail(CPDB_INVALID_ARGUMENT, "solve_spd: RHS columns must match G");
+        if (g_rows == 0) fail(CPDB_INVALID_ARGUMENT, "Matrix: zero dimension");
+        if (g_rows > 64) fail(CPDB_INVALID_ARGUMENT, "solve_spd: n above 64 is not supported");
+        const uint32_t n = uint32_t(g_rows);
+        double* dg = c->scratch_a.ensure(2 * uint64_t(n) * n + 8);
+        double* dx = c->scratch_b.ensure(std::max<uint64_t>(rows * n, 1));
+        upload(c, dg, g, uint64_t(n) * n);
+        if (rows) upload(c, dx, rhs, rows * n);
+        int* flags = reinterpret_cast<int*>(dg + 2 * uint64_t(n) * n);
+        CPDB_CK(cudaMemsetAsync(flags, 0, 2 * sizeof(int), c->stream));
+        CPDB_CK(cpdb::launch_spd_solve(dg, n, dg + uint64_t(n) * n, dx, rows, flags, flags + 1,
+                                       c->stream, c->sms));
+        int h[2];
+        CPDB_CK(cudaMemcpyAsync(h, flags, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+        CPDB_CK(cudaStreamSynchronize(c->stream));
+        if (h[0] == 5) fail(CPDB_INVALID_ARGUMENT, "solve_spd: G is not symmetric");
+        if (h[0] == 4)
+            fail(CPDB_SINGULAR_SYSTEM, "solve_spd: factorization failed after ridge");
+        if (rows) download(c, x, dx, rows * n);
+        if (regularized) *regularized = h[1];
+    });
+}
+
+int cpdb_fitness_fast_als(cpdb_ctx* c, double nx2, const double* m, const double* a_hat,
+                          uint64_t rows, uint64_t cols, const double* gamma,
+                          const double* lambda, uint64_t r, const double* s_last,
+                          double* fitness, double* raw) {
+    return guarded([&] {
+        use_device(c);
+        if (!(nx2 > 0.0)) fail(CPDB_INVALID_ARGUMENT, "fitness_fast_als: zero-norm tensor");
+        if (r == 0) fail(CPDB_INVALID_ARGUMENT, "fitness_fast_als: dimension mismatch");
+        double* dv = c->scratch_a.ensure(std::max<uint64_t>(2 * rows * cols, 1));
+        double* dm = c->scratch_b.ensure(2 * r * r + r + 8);
+        if (rows * cols) {
+            upload(c, dv, m, rows * cols);
+            upload(c, dv + rows * cols, a_hat, rows * cols);
+        }
+        upload(c, dm, gamma, r * r);
+        upload(c, dm + r * r, s_last, r * r);
+        upload(c, dm + 2 * r * r, lambda, r);
+        double* o = dm + 2 * r * r + r;
+        CPDB_CK(cpdb::launch_fitness_als(nx2, dv, dv + rows * cols, rows * cols, dm,
+                                         dm + 2 * r * r, dm + r * r, uint32_t(r), o, c->stream));
+        double h[2];
+        download(c, h, o, 2);
+        *fitness = h[0];
+        *raw = h[1];
+    });
+}
+
 int cpdb_inner(cpdb_ctx* c, const double* a, const double* b, uint64_t n, double* out) {
     return guarded([&] {
         use_device(c);

@@ -425,6 +425,164 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
     CPDB_TS(10);
 }
 
+// ---------------------------------------------------------------- CP-ALS mode tail
+// solvers.hpp:177-197 for mode n: Gamma = Hadamard_k G_k (k != n, ascending,
+// from a ones matrix), A_hat = solve_spd(Gamma, M) (linalg.hpp:132-187),
+// (A_n, lambda) = normalize_columns(A_hat) (linalg.hpp:225-242), G_n =
+// gram(A_n), and on the last mode fitness_fast_als (kruskal.hpp:88-104).
+// Rank 0 factors Gamma (U^T U = Gamma, i.e. U = L^T); every rank solves its
+// rows, x = m U^-1 U^-T, and the two Grams are reduced over DSMEM.
+template <int RM, int SL>
+__global__ void __launch_bounds__(kNT) als_finish_cluster_kernel(AlsFinishArgs a) {
+    using Row = LaneRow<RM, SL>;
+    constexpr int T = Row::T, G = kNT / T;
+    cg::cluster_group cl = cg::this_cluster();
+    const int rank = int(cl.block_rank());
+    extern __shared__ double sm[];
+    __shared__ double red[32];
+    __shared__ int flag;
+    const int R = a.R, ld = R + 1;
+    const uint64_t I = a.I;
+    const int per = int((I + kCS - 1) / kCS);
+    const uint64_t r0 = uint64_t(per) * rank;
+    const int rows = int(r0 < I ? (I - r0 < uint64_t(per) ? I - r0 : uint64_t(per)) : 0);
+    Smem<RM> S(sm, R);
+    double* gam = S.w + per * ld;  // R x R: Gamma (rank 0)
+    const int grp = threadIdx.x / T, q = threadIdx.x % T;
+    pdl_entry();
+    CPDB_TS(0);
+
+    if (rank == 0) {
+        double mabs = 0.0, masym = 0.0;
+        for (int e = threadIdx.x; e < R * R; e += kNT) {
+            double h = 1.0;
+            for (uint32_t t = 0; t < a.ng; ++t) h = h * a.grams[t][e];
+            gam[e] = h;
+            S.g[e] = h;
+        }
+        __syncthreads();
+        for (int e = threadIdx.x; e < R * R; e += kNT) {
+            const int i = e / R, j = e % R;
+            mabs = fmax(mabs, fabs(gam[e]));
+            masym = fmax(masym, fabs(gam[e] - gam[j * R + i]));
+        }
+        mabs = block_max<kNT>(mabs, red);
+        masym = block_max<kNT>(masym, red);
+        int code = 0, used = 0;
+        if (masym > 1e-10 * mabs) {
+            code = 5;
+        } else {
+            bool ok = chol<kNT, RM>(S.g, R, R);
+            if (!ok) {  // ridge retry, delta = 1e-12 trace / n (linalg.hpp:147-154)
+                double tr = 0.0;
+                for (int i = 0; i < R; ++i) tr += gam[i * R + i];
+                const double delta = 1e-12 * tr / double(R);
+                for (int e = threadIdx.x; e < R * R; e += kNT)
+                    S.g[e] = gam[e] + ((e / R == e % R) ? delta : 0.0);
+                __syncthreads();
+                ok = chol<kNT, RM>(S.g, R, R);
+                used = 1;
+            }
+            code = ok ? 0 : 4;
+        }
+        if (threadIdx.x == 0) {
+            S.misc[2] = double(code);
+            if (used) *a.regularized = 1;
+        }
+        CPDB_TS(1);
+    }
+    cl.sync();  // ---- 1: U (rank 0's g) published
+    {
+        const double* g0 = cl.map_shared_rank(S.g, 0);
+        stage_tri<RM>(g0, R, R, S.u, S.dinv, kNT);
+        stage_tri_t<RM>(g0, R, R, S.ut, S.dinv, kNT);
+        if (threadIdx.x == 0) flag = int(cl.map_shared_rank(S.misc, 0)[2]);
+    }
+    cl.sync();  // rank 0 may reuse g only after every rank copied U
+    if (flag) {
+        if (rank == 0 && threadIdx.x == 0) *a.status = flag;
+        return;  // uniform across the cluster
+    }
+    // rows: A_hat = M U^-1 U^-T (+ this rank's share of <M, A_hat>)
+    double xk_part = 0.0;
+    for (int li = grp; li < rows + (G - rows % G) % G; li += G) {
+        const bool act = li < rows;
+        Row x;
+        x.load(a.m + (act ? (r0 + li) : r0) * R, act ? R : 0, q);
+        Row m = x;
+        x.uinv(S.u, S.dinv, R, q);
+        x.utinv(S.ut, S.dinv, R, q);
+        if (a.fitness) {
+#pragma unroll
+            for (int s = 0; s < Row::S; ++s) xk_part = fma(m.t[s], x.t[s], xk_part);
+        }
+        if (act) x.store(S.w + li * ld, R, q);
+    }
+    __syncthreads();
+    CPDB_TS(2);
+    gram_dmma<kNT>(S.w, ld, rows, R, S.p, R);
+    if (a.fitness) {
+        const double x = block_sum<kNT>(xk_part, red);
+        if (threadIdx.x == 0) S.misc[0] = x;
+    }
+    cl.sync();  // ---- 2: Gram partials of A_hat
+    if (rank == 0) {
+        cluster_reduce(cl, S.p, R * R, S.g);
+        if (a.fitness && threadIdx.x == 0) {
+            double x = 0.0;
+            for (int r = 0; r < kCS; ++r) x += cl.map_shared_rank(S.misc, r)[0];
+            S.misc[1] = x;  // <M, A_hat>
+        }
+        __syncthreads();
+        for (int c = threadIdx.x; c < R; c += kNT) S.vec[c] = sqrt(S.g[c * R + c]);  // lambda
+    }
+    cl.sync();  // ---- 3: lambda published (rank 0's vec)
+    {
+        const double* l0 = cl.map_shared_rank(S.vec, 0);
+        for (int c = threadIdx.x; c < RM; c += kNT) {
+            const double l = c < R ? l0[c] : 0.0;
+            S.dinv[c] = l < 1e-300 ? 0.0 : __drcp_rn(l);  // 1/lambda (U is no longer needed)
+            if (rank == 0 && c < R) a.lambda[c] = l < 1e-300 ? 0.0 : l;
+        }
+    }
+    __syncthreads();
+    // A_n = A_hat / lambda (vanishing column -> e1, weight 0)
+    for (int e = threadIdx.x; e < rows * R; e += kNT) {
+        const int li = e / R, c = e % R;
+        const double il = S.dinv[c];
+        const double v = il == 0.0 ? ((r0 + li) == 0 ? 1.0 : 0.0) : S.w[li * ld + c] * il;
+        S.w[li * ld + c] = v;
+        a.a_out[(r0 + li) * R + c] = v;
+    }
+    __syncthreads();
+    gram_dmma<kNT>(S.w, ld, rows, R, S.p, R);
+    cl.sync();  // ---- 4: Gram partials of A_n
+    if (rank == 0) {
+        cluster_reduce(cl, S.p, R * R, S.g);
+        __syncthreads();
+        for (int e = threadIdx.x; e < R * R; e += kNT) a.g_out[e] = S.g[e];
+        if (a.fitness) {
+            // ||K||^2 = sum_ij Gamma_ij l_i G_ij l_j  (kruskal.hpp:97-100)
+            double kk = 0.0;
+            for (int e = threadIdx.x; e < R * R; e += kNT) {
+                const int i = e / R, j = e % R;
+                const double li = S.vec[i] < 1e-300 ? 0.0 : S.vec[i];
+                const double lj = S.vec[j] < 1e-300 ? 0.0 : S.vec[j];
+                kk += gam[e] * li * S.g[e] * lj;
+            }
+            kk = block_sum<kNT>(kk, red);
+            if (threadIdx.x == 0) {
+                const double raw = a.norm_x_sq - 2.0 * S.misc[1] + kk;
+                const double rad = raw < 0.0 ? 0.0 : raw;
+                a.fit_out[0] = 1.0 - sqrt(rad) / sqrt(a.norm_x_sq);
+                a.fit_out[1] = raw;
+            }
+        }
+        CPDB_TS(3);
+    }
+    cl.sync();  // the other ranks' smem must outlive rank 0's DSMEM reads
+}
+
 template <class Arg>
 cudaError_t launch_cluster(void (*kern)(Arg), size_t smem, cudaStream_t s, const Arg& arg,
                            bool pdl) {
@@ -522,6 +680,46 @@ cudaError_t launch_finish_cluster(const FinishArgs& a, cudaStream_t s) {
         default: CPDB_FIN(64);
     }
 #undef CPDB_FIN
+}
+
+static size_t als_smem(uint64_t I, uint32_t R) {
+    // Smem plan + Gamma (R x R) after the rows
+    const uint64_t per = (I + kCS - 1) / kCS;
+    switch (rm_of(R)) {
+        case 8: return (Smem<8>::doubles(R, per) + size_t(R) * R) * sizeof(double);
+        case 16: return (Smem<16>::doubles(R, per) + size_t(R) * R) * sizeof(double);
+        case 32: return (Smem<32>::doubles(R, per) + size_t(R) * R) * sizeof(double);
+        default: return (Smem<64>::doubles(R, per) + size_t(R) * R) * sizeof(double);
+    }
+}
+
+bool als_finish_fits(uint64_t I, uint32_t R) { return R <= 64 && als_smem(I, R) <= 220 * 1024; }
+
+namespace {
+template <int RM, int SL>
+cudaError_t als_rs(const AlsFinishArgs& a, size_t smem, cudaStream_t s) {
+    return launch_cluster<AlsFinishArgs>(als_finish_cluster_kernel<RM, SL>, smem, s, a, true);
+}
+}  // namespace
+
+cudaError_t launch_als_finish(const AlsFinishArgs& a, cudaStream_t s) {
+    if (!als_finish_fits(a.I, a.R)) return cudaErrorInvalidValue;
+    const size_t smem = als_smem(a.I, a.R);
+    const uint64_t rows = (a.I + kCS - 1) / kCS;
+    const int rm = rm_of(a.R), sl = slots_for(rm, rows);
+#define CPDB_ALS(RM_)                                                                    \
+    return by_slots<RM_>(                                                                \
+        sl, [&] { return als_rs<RM_, 8>(a, smem, s); },                                  \
+        [&] { return als_rs<RM_, 4>(a, smem, s); },                                      \
+        [&] { return als_rs<RM_, 2>(a, smem, s); },                                      \
+        [&] { return als_rs<RM_, (RM_ <= 32 ? 1 : 2)>(a, smem, s); })
+    switch (rm) {
+        case 8: CPDB_ALS(8);
+        case 16: CPDB_ALS(16);
+        case 32: CPDB_ALS(32);
+        default: CPDB_ALS(64);
+    }
+#undef CPDB_ALS
 }
 
 static size_t zqr_cluster_smem(uint64_t zrows, uint32_t R, uint32_t nm) {

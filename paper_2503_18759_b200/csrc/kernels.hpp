@@ -76,6 +76,59 @@ struct VgemmArgs {
 cudaError_t launch_vgemm(VgemmArgs& a, cudaStream_t s, int sms);
 uint32_t vgemm_max_split();
 
+// ---------------------------------------------------------------- CP-ALS (als.cu)
+// MTTKRP = TTM(X, A_c) + Khatri-Rao contraction of the other modes.
+struct KrcArgs {
+    const double* t;       // TTM output T
+    const double* fac[8];  // A_k (I_k x R) of every mode
+    uint64_t dims[8];
+    uint32_t km[8];        // modes of the W table, ascending (not n, not c)
+    uint32_t nkm;
+    uint64_t rows_w;       // prod of dims[km]
+    uint32_t R;
+    int router;            // 0: T = [P, In, Q, R] (c = N-1); 1: T = [R, Q, In] (c = 0)
+    uint64_t P, In, Q;
+};
+cudaError_t launch_kr_table(const KrcArgs& a, double* w, cudaStream_t s);
+uint64_t krc_split(const KrcArgs& a, int sms);
+// out: split x In x R partials (split == 1: M itself)
+cudaError_t launch_krc(const KrcArgs& a, const double* w, double* out, uint64_t split,
+                       cudaStream_t s);
+cudaError_t launch_spd_solve(const double* g, uint32_t n, double* u_work, double* x, uint64_t rows,
+                             int* status, int* reg, cudaStream_t s, int sms);
+struct GramList {
+    const double* g[8];
+    uint32_t n;
+};
+cudaError_t launch_or_flag(const int* src, int* dst, cudaStream_t s);  // *dst |= *src != 0
+cudaError_t gram_dev(const double* a, uint64_t m, uint32_t n, double* g, cudaStream_t s);
+cudaError_t hadamard_dev(const GramList& l, uint32_t r, double* out, cudaStream_t s);
+cudaError_t launch_fitness_als(double nx2, const double* m, const double* ah, uint64_t n_mr,
+                               const double* gamma, const double* lam, const double* s_last,
+                               uint32_t r, double* out, cudaStream_t s);
+
+// Per-mode tail of cp_als (solvers.hpp:177-197) as one 8-CTA cluster kernel:
+// Gamma = Hadamard(G_k, k != n), solve_spd(Gamma, M) (Cholesky + ridge retry),
+// normalize_columns -> A_n, lambda, G_n = gram(A_n), fitness_fast_als.
+struct AlsFinishArgs {
+    const double* m;           // I x R (MTTKRP)
+    const double* grams[8];    // G_k, k != n (ascending)
+    uint32_t ng;
+    uint64_t I;
+    uint32_t R;
+    double* a_out;             // I x R normalised factor
+    double* g_out;             // R x R Gram of a_out
+    double* lambda;            // R
+    int fitness;
+    double norm_x_sq;
+    double* fit_out;           // [fitness, raw]
+    int* status;               // 4 singular after the ridge, 5 Gamma not symmetric
+    int* regularized;          // set to 1 when the ridge retry was used
+    unsigned long long* ts;
+};
+bool als_finish_fits(uint64_t I, uint32_t R);
+cudaError_t launch_als_finish(const AlsFinishArgs& a, cudaStream_t s);
+
 // ---------------------------------------------------------------- finisher
 // Per-mode tail: reduce V partials, A_hat = V R0^-T, normalise (lambda),
 // CholQR2 of the factor -> Q_n, R_n, packed Q_n, and (last mode) the

@@ -32,6 +32,20 @@ __device__ double block_sum(double v, double* red) {
     return s;  // valid in warp 0
 }
 
+// max over the block, returned to every thread
+template <int NT>
+__device__ double block_max(double v, double* red) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();
+    if (lane == 0) red[warp] = v;
+    __syncthreads();
+    double m = red[0];
+    for (int w = 1; w < NT / 32; ++w) m = fmax(m, red[w]);
+    return m;
+}
+
 // ---------------------------------------------------------------- lane rows
 // A row of length <= RM distributed over T = RM/8 lanes: lane q holds
 // x[8*i... ] as t[s] = x[s*T + q], s < 8.

@@ -157,6 +157,14 @@ void solve(cpdb_ctx* c, const cpdb_config& cfg, cpdb_state* state, cpdb_trace_ro
 
 // Natural (Y row-major) <-> reference (Khatri-Rao, descending fold) row order
 // of Z / Q0 for mode n: digit reversal over the N-1 other modes.
+// CP-ALS through the normal equations (als.cpp, solvers.hpp:149-208)
+void als_solve(cpdb_ctx* c, const cpdb_config& cfg, const double* init_lambda,
+               const double* init_factors, cpdb_trace_row* trace, uint64_t* trace_len,
+               double* out_lambda, double* out_factors);
+void mttkrp_primitive(cpdb_ctx* c, const double* x, const std::vector<uint64_t>& dims,
+                      const std::vector<const double*>& fac_dev, uint32_t R, uint32_t n,
+                      double* m_out);
+
 std::vector<uint64_t> natural_to_reference(uint32_t order, uint64_t R);
 
 // One TTM of the execute() chain on device buffers: contracts `c` of a

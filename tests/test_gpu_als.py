@@ -1,0 +1,232 @@
+"""GPU: CP-ALS through the normal equations (SURVEY.md 8f row 4,
+solvers.hpp:149-208) and its primitives against the CPU oracle.
+
+Same bar as the QR path: per-sweep relative fitness <= 1e-10 (looser on
+random, non-low-rank tensors, where the normal equations square the
+conditioning), identical trace length, update order, integer flops and
+ridge flags; factors <= 1e-10.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+FIT_TOL = 1e-10
+
+
+def als_cfg(rank, iters, seed=0, **kw):
+    import paper_2503_18759_b200 as cpd
+    return cpd.SolverConfig(rank=rank, max_iterations=iters, seed=seed, algorithm="als", **kw)
+
+
+def compare(g, o, fit_tol=FIT_TOL, factor_tol=1e-10):
+    assert len(g.trace) == len(o.trace)
+    for a, b in zip(g.trace, o.trace):
+        assert a.iteration == b["iteration"]
+        assert a.update_order == b["update_order"]
+        assert a.flops == b["flops"] and a.root_ttm_count == 0 == b["root_ttm_count"]
+        assert a.regularized == b["regularized"]
+        assert abs(a.fitness - b["fitness"]) <= fit_tol * max(abs(b["fitness"]), 1e-300), \
+            (a.iteration, a.fitness, b["fitness"])
+    for k, (fg, fo) in enumerate(zip(g.model.factors, o.factors)):
+        err = np.linalg.norm(fg - fo) / np.linalg.norm(fo)
+        assert err <= factor_tol, (k, err)
+    assert np.linalg.norm(g.model.lam - o.lam) / np.linalg.norm(o.lam) <= factor_tol
+
+
+# ---------------------------------------------------------------- MTTKRP
+@pytest.mark.parametrize("dims", [(9, 8, 7), (7, 6, 5, 4), (5, 11), (3, 4, 2, 3, 2), (100, 30, 64)])
+@pytest.mark.parametrize("rank", [1, 3, 10, 32, 64])
+def test_mttkrp_every_mode(ctx, ref, dims, rank):
+    import paper_2503_18759_b200 as cpd
+    rng = np.random.default_rng(sum(dims) * 7 + rank)
+    x = rng.standard_normal(dims)
+    fs = [rng.standard_normal((d, rank)) for d in dims]
+    for mode in range(len(dims)):
+        f2 = list(fs)
+        f2[mode] = None  # factors[mode] is never read (tensor.hpp:415-431)
+        g = cpd.mttkrp(x, f2, mode, ctx=ctx)
+        o = ref.mttkrp(x, fs, mode)
+        scale = np.abs(o).max()
+        assert np.abs(g - o).max() <= 1e-12 * max(scale, 1.0) * np.sqrt(x.size / dims[mode]), \
+            (dims, rank, mode)
+
+
+def test_mttkrp_argument_errors(ctx):
+    import paper_2503_18759_b200 as cpd
+    x = np.ones((3, 4, 5))
+    fs = [np.ones((3, 2)), np.ones((4, 2)), np.ones((5, 2))]
+    with pytest.raises(cpd.CpdInvalidArgument, match="mode out of range"):
+        cpd.mttkrp(x, fs, 3, ctx=ctx)
+    with pytest.raises(cpd.CpdInvalidArgument, match="mismatched ranks"):
+        cpd.mttkrp(x, [fs[0], fs[1], np.ones((5, 3))], 0, ctx=ctx)
+    with pytest.raises(cpd.CpdInvalidArgument, match="rows do not match"):
+        cpd.mttkrp(x, [fs[0], np.ones((5, 2)), fs[2]], 0, ctx=ctx)
+    with pytest.raises(cpd.CpdInvalidArgument, match="missing factor"):
+        cpd.mttkrp(x, [fs[0], None, fs[2]], 0, ctx=ctx)
+
+
+# ---------------------------------------------------------------- solve_spd
+def test_solve_spd_reference_cases(ctx):
+    """linalg_test.cpp:111-156 restated."""
+    import paper_2503_18759_b200 as cpd
+    rhs = np.random.default_rng(113).standard_normal((4, 3))
+    x, reg = cpd.solve_spd(np.eye(3), rhs, ctx=ctx)
+    assert np.array_equal(x, rhs) and not reg
+    x, _ = cpd.solve_spd(np.diag([2.0, 4.0]), np.array([[2.0, 4.0]]), ctx=ctx)
+    assert np.abs(x - 1.0).max() <= 1e-15
+    _, reg = cpd.solve_spd(np.ones((2, 2)), np.ones((1, 2)), ctx=ctx)
+    assert reg
+    with pytest.raises(cpd.SingularSystemError):
+        cpd.solve_spd(np.zeros((2, 2)), np.zeros((1, 2)), ctx=ctx)
+    with pytest.raises(cpd.CpdInvalidArgument, match="not symmetric"):
+        cpd.solve_spd(np.array([[1.0, 0.5], [0.0, 1.0]]), np.zeros((1, 2)), ctx=ctx)
+    with pytest.raises(cpd.CpdInvalidArgument, match="square"):
+        cpd.solve_spd(np.ones((2, 3)), np.zeros((1, 3)), ctx=ctx)
+
+
+@pytest.mark.parametrize("n,rows", [(1, 5), (5, 7), (16, 300), (20, 33), (32, 1000), (64, 129)])
+def test_solve_spd_vs_oracle(ctx, ref, n, rows):
+    import paper_2503_18759_b200 as cpd
+    rng = np.random.default_rng(n * 131 + rows)
+    f = rng.standard_normal((3 * n + 2, n))
+    g = f.T @ f
+    rhs = rng.standard_normal((rows, n))
+    x, reg = cpd.solve_spd(g, rhs, ctx=ctx)
+    xo, rego = ref.solve_spd(g, rhs)
+    assert reg == rego
+    assert np.abs(x - xo).max() <= 1e-10 * np.abs(xo).max()
+    assert np.linalg.norm(x @ g - rhs) <= 1e-10 * np.linalg.norm(rhs)
+
+
+def test_fitness_fast_als_vs_oracle(ctx, ref):
+    import paper_2503_18759_b200 as cpd
+    rng = np.random.default_rng(5)
+    m, a = rng.standard_normal((40, 6)), rng.standard_normal((40, 6))
+    f1, f2 = rng.standard_normal((9, 6)), rng.standard_normal((11, 6))
+    gam, s = f1.T @ f1, f2.T @ f2
+    lam = rng.uniform(0.5, 2.0, 6)
+    nx2 = 1e3
+    g = cpd.fitness_fast_als(nx2, m, a, gam, lam, s, ctx=ctx)
+    o = ref.fitness_fast_als(nx2, m, a, gam, lam, s)
+    assert abs(g[1] - o[1]) <= 1e-12 * abs(o[1]) and abs(g[0] - o[0]) <= 1e-12
+    with pytest.raises(cpd.CpdInvalidArgument):
+        cpd.fitness_fast_als(0.0, m, a, gam, lam, s, ctx=ctx)
+
+
+# ---------------------------------------------------------------- cp_als
+@pytest.mark.parametrize("dims,rank,kind", [((12, 11, 10), 4, 0), ((9, 8, 7), 3, 0),
+                                            ((8, 7, 6, 5), 3, 0), ((40, 30, 20), 8, 0),
+                                            ((16, 12, 10, 8), 5, 0), ((30, 2, 20), 2, 0),
+                                            ((50, 60), 7, 0), ((64, 64, 64), 20, 1)])
+def test_cp_als_trajectories(ctx, ref, dims, rank, kind):
+    """Low-rank + 1e-2 noise tensors (the BASELINE construction)."""
+    import paper_2503_18759_b200 as cpd
+    x = ref.synth_baseline(kind, dims, rank, 1e-2, 777 + rank)
+    g = cpd.cp_als(x, als_cfg(rank, 25, seed=9), ctx=ctx)
+    o = ref.cp_als(x, rank, 25, seed=9)
+    compare(g, o, fit_tol=1e-10 if kind == 0 else 1e-9, factor_tol=1e-9 if kind == 0 else 1e-7)
+
+
+@pytest.mark.parametrize("dims,rank", [((12, 11, 10), 4), ((7, 6, 5, 4), 3)])
+def test_cp_als_random_tensors(ctx, ref, dims, rank):
+    """solver_test.cpp:127-137 shapes: random tensors, slow convergence."""
+    import paper_2503_18759_b200 as cpd
+    x = np.random.default_rng(sum(dims)).standard_normal(dims)
+    g = cpd.cp_als(x, als_cfg(rank, 15, seed=31), ctx=ctx)
+    o = ref.cp_als(x, rank, 15, seed=31)
+    compare(g, o, fit_tol=1e-8, factor_tol=1e-6)
+    for i in range(1, len(g.trace)):  # solver_test.cpp:131-136
+        assert g.trace[i].fitness >= g.trace[i - 1].fitness - 1e-9
+
+
+def test_cp_als_c1_full(ctx, ref):
+    """BASELINE C1 (100^3 R10, 1e-2 noise), 50 sweeps of CP-ALS."""
+    import paper_2503_18759_b200 as cpd
+    x = ref.synth_baseline(0, (100, 100, 100), 10, 1e-2, 20250001)
+    g = cpd.cp_als(x, als_cfg(10, 50, seed=7), ctx=ctx)
+    o = ref.cp_als(x, 10, 50, seed=7)
+    compare(g, o)
+
+
+def test_cp_als_init_and_threshold(ctx, ref):
+    """solver_test.cpp:100-112: the truth as init is a fixed point (one sweep)."""
+    import paper_2503_18759_b200 as cpd
+    rng = np.random.default_rng(521)
+    dims, R = (6, 5, 4), 3
+    fs = [rng.standard_normal((d, R)) for d in dims]
+    fs = [f / np.linalg.norm(f, axis=0) for f in fs]
+    lam = np.array([3.0, 2.0, 1.0])
+    x = np.einsum("r,ir,jr,kr->ijk", lam, *fs)
+    cfg = als_cfg(R, 10, fitness_threshold=1.0 - 1e-6)
+    g = cpd.cp_als(x, cfg, init=cpd.KruskalModel(lam, fs), ctx=ctx)
+    o = ref.cp_als(x, R, 10, fitness_threshold=1.0 - 1e-6, init_lam=lam, init_factors=fs)
+    assert len(g.trace) == len(o.trace) == 1
+    assert g.trace[0].fitness > 1.0 - 1e-6
+
+
+def test_cp_als_ridge_on_rank_deficient_gram(ctx, ref):
+    """A zero factor column makes Gamma singular: the ridge retry fires
+    (solve_spd regularized) on both sides."""
+    import paper_2503_18759_b200 as cpd
+    rng = np.random.default_rng(3)
+    dims, R = (6, 5, 4), 3
+    x = rng.standard_normal(dims)
+    fs = [rng.standard_normal((d, R)) for d in dims]
+    fs[1][:, 2] = fs[1][:, 1]  # two equal columns: Gamma rank-deficient for mode 0
+    fs[2][:, 2] = fs[2][:, 1]
+    lam = np.ones(R)
+    g = cpd.cp_als(x, als_cfg(R, 3), init=cpd.KruskalModel(lam, fs), ctx=ctx)
+    o = ref.cp_als(x, R, 3, init_lam=lam, init_factors=fs)
+    assert [t.regularized for t in g.trace] == [t["regularized"] for t in o.trace]
+    assert g.trace[0].regularized
+
+
+def test_cp_als_rejections(ctx):
+    import paper_2503_18759_b200 as cpd
+    with pytest.raises(cpd.CpdInvalidArgument, match="zero-norm"):
+        cpd.cp_als(np.zeros((3, 3)), als_cfg(2, 5), ctx=ctx)
+    with pytest.raises(cpd.CpdInvalidArgument, match="algorithm must be als"):
+        cpd.cp_als(np.ones((3, 3)), cpd.SolverConfig(rank=2, max_iterations=5), ctx=ctx)
+    with pytest.raises(cpd.CpdInvalidArgument, match="ranks above 64"):
+        cpd.cp_als(np.ones((70, 70)), als_cfg(65, 1), ctx=ctx)
+
+
+def test_cp_als_deterministic(ctx, ref):
+    """solver_test.cpp:272-282: repeated runs are bit-identical."""
+    import paper_2503_18759_b200 as cpd
+    x = ref.synth_baseline(0, (40, 50, 30), 6, 1e-2, 4242)
+    a = cpd.cp_als(x, als_cfg(6, 8, seed=77), ctx=ctx)
+    b = cpd.cp_als(x, als_cfg(6, 8, seed=77), ctx=ctx)
+    assert [t.fitness for t in a.trace] == [t.fitness for t in b.trace]
+    for fa, fb in zip(a.model.factors, b.model.factors):
+        assert np.array_equal(fa, fb)
+
+
+@pytest.mark.parametrize("world", [2, 4])
+@pytest.mark.parametrize("dims,rank", [((64, 20, 24), 5), ((32, 9, 10, 11), 4)])
+def test_cp_als_sharded_matches_unsharded(ctx, ref, world, dims, rank):
+    """Mode-0 shards inside one process: MTTKRP partials
+    all-reduced (n != 0) or all-gathered (n = 0); the tail is replicated."""
+    import paper_2503_18759_b200 as cpd
+    from test_gpu_sharded import run_ranks
+    x = ref.synth_baseline(0, dims, rank, 1e-2, 99)
+    base = cpd.cp_als(x, als_cfg(rank, 10, seed=5), ctx=ctx)
+    rows = dims[0] // world
+    group = cpd.Context.local_group(0, world)
+
+    def rank_run(r, c):
+        c.set_tensor(np.ascontiguousarray(x[r * rows:(r + 1) * rows]), dims)
+        return c.solve_als(als_cfg(rank, 10, seed=5))
+
+    res = run_ranks(group, rank_run)
+    for g in res:
+        assert [t.flops for t in g.trace] == [t.flops for t in base.trace]
+        for a, b in zip(g.trace, base.trace):
+            assert abs(a.fitness - b.fitness) <= 1e-10 * abs(b.fitness)
+        for fa, fb in zip(g.model.factors, base.model.factors):
+            assert np.linalg.norm(fa - fb) <= 1e-10 * np.linalg.norm(fb)
+    for g in res[1:]:
+        for fa, fb in zip(g.model.factors, res[0].model.factors):
+            assert np.array_equal(fa, fb)
+    for c in group:
+        c.close()
