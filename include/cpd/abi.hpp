@@ -11,6 +11,7 @@
 //   CPDB_STALE_INTERMEDIATE   cpd::stale_intermediate_error  (dim_tree.hpp:20-22)
 //   CPDB_SINGULAR_TRIANGULAR  cpd::singular_triangular_error (linalg.hpp:18-25)
 //   CPDB_LOGIC_ERROR          std::logic_error
+//   CPDB_SINGULAR_SYSTEM      cpd::singular_system_error     (linalg.hpp:15-17)
 //   anything else             cpd::device_error (CUDA / NCCL / OOM)
 #pragma once
 
@@ -57,6 +58,7 @@ namespace abi {
         case CPDB_STALE_INTERMEDIATE: throw stale_intermediate_error(msg);
         case CPDB_SINGULAR_TRIANGULAR: throw singular_triangular_error(0, 0.0);
         case CPDB_LOGIC_ERROR: throw std::logic_error(msg);
+        case CPDB_SINGULAR_SYSTEM: throw singular_system_error(msg);
         default: throw device_error("cpdb: " + msg);
     }
 }

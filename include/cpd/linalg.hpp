@@ -7,8 +7,9 @@
 //                                                   1e-14 relative singularity test
 //   normalize_columns            linalg.hpp:225-242 device, the reference's exact
 //                                                   summation order
-// The SPD solve (solve_spd, linalg.hpp:114-171) serves the CP-ALS normal
-// equations, outside this library's scope.
+//   solve_spd                    linalg.hpp:132-187 device Cholesky (+ the
+//                                                   1e-12 trace/n ridge retry) and
+//                                                   row solves (CP-ALS normal equations)
 #pragma once
 
 #include <cstddef>
@@ -61,6 +62,22 @@ inline NormalizedColumns normalize_columns(const Matrix& a) {
     NormalizedColumns out{Matrix(a.rows(), a.cols()), std::vector<double>(a.cols(), 0.0)};
     abi::check(cpdb_normalize_columns(abi::ctx(), a.data(), a.rows(), a.cols(),
                                       out.matrix.data(), out.weights.data()));
+    return out;
+}
+
+struct SpdSolveResult {
+    Matrix x;
+    bool regularized = false;
+};
+
+// X G = RHS with G symmetric positive (semi)definite (linalg.hpp:132-187):
+// symmetric check, Cholesky, one ridge retry, singular_system_error.
+inline SpdSolveResult solve_spd(const Matrix& g, const Matrix& rhs) {
+    SpdSolveResult out{Matrix(rhs.rows(), rhs.cols()), false};
+    int32_t reg = 0;
+    abi::check(cpdb_solve_spd(abi::ctx(), g.data(), g.rows(), g.cols(), rhs.data(), rhs.rows(),
+                              rhs.cols(), out.x.data(), &reg));
+    out.regularized = reg != 0;
     return out;
 }
 

@@ -9,8 +9,9 @@
 // SolverConfig / TraceRow / SolveResult keep the reference's fields, including
 // q0_observer (called with Q0 in the reference's Khatri-Rao row order).
 //
-// cp_als (normal equations + MTTKRP, solvers.hpp:149-208) is the comparison
-// solver of the paper and outside this library's scope.
+//   cp_als      solvers.hpp:149-208  device-resident normal-equation ALS (the
+//                                    paper's comparison solver): per mode
+//                                    MTTKRP, Gamma, solve_spd, normalisation
 #pragma once
 
 #include <cmath>
@@ -224,6 +225,67 @@ inline SolveResult run_qr(const DenseTensor& x, const SolverConfig& cfg,
 }
 
 }  // namespace detail
+
+inline SolveResult cp_als(const DenseTensor& x, const SolverConfig& cfg,
+                          const std::optional<KruskalModel>& init = {}) {
+    cfg.validate();
+    if (cfg.algorithm != Algorithm::als)
+        throw std::invalid_argument("cp_als: config algorithm must be als");
+    if (x.order() < 2) throw std::invalid_argument("cp_als: tensor order must be >= 2");
+    std::vector<double> init_f, init_l;
+    if (init) {
+        for (const Matrix& f : detail::initial_factors(x, cfg, init))
+            init_f.insert(init_f.end(), f.values().begin(), f.values().end());
+        init_l = detail::initial_lambda(init, cfg.rank);
+    }
+    cpdb_ctx* ctx = nullptr;
+    const char* env = std::getenv("CPD_DEVICE");
+    abi::check(cpdb_create(env ? std::atoi(env) : 0, &ctx));
+    struct Guard {
+        cpdb_ctx* c;
+        ~Guard() { cpdb_destroy(c); }
+    } guard{ctx};
+    const std::vector<uint64_t> dims = abi::u64(x.shape().dims());
+    abi::check(cpdb_tensor_set(ctx, x.data(), dims.data(), uint32_t(x.order())));
+    cpdb_config c{};
+    c.rank = cfg.rank;
+    c.max_iterations = cfg.max_iterations;
+    c.fitness_threshold = cfg.fitness_threshold;
+    c.alpha = cfg.alpha;
+    c.activation_gap = cfg.activation_gap;
+    c.seed = cfg.seed;
+    std::size_t nfac = 0;
+    for (const std::size_t d : x.shape().dims()) nfac += d * cfg.rank;
+    std::vector<cpdb_trace_row> rows(cfg.max_iterations);
+    std::vector<double> lam(cfg.rank), fac(nfac);
+    uint64_t n = 0;
+    abi::check(cpdb_als_solve(ctx, &c, init ? init_l.data() : nullptr,
+                              init ? init_f.data() : nullptr, rows.data(), &n, lam.data(),
+                              fac.data()));
+    SolveResult out;
+    for (uint64_t i = 0; i < n; ++i) {
+        const cpdb_trace_row& r = rows[i];
+        TraceRow t;
+        t.iteration = std::size_t(r.iteration);
+        t.update_order.assign(r.update_order, r.update_order + r.order);
+        t.fitness = r.fitness;
+        t.raw_radicand = r.raw_radicand;
+        t.wall_seconds = r.wall_seconds;
+        t.root_ttm_count = r.root_ttm_count;
+        t.flops = r.flops;
+        t.beta_used = r.beta_used;
+        t.regularized = r.regularized != 0;
+        out.trace.push_back(std::move(t));
+    }
+    out.model.lambda = std::move(lam);
+    std::size_t off = 0;
+    for (const std::size_t d : x.shape().dims()) {
+        out.model.factors.emplace_back(
+            d, cfg.rank, std::vector<double>(fac.begin() + off, fac.begin() + off + d * cfg.rank));
+        off += d * cfg.rank;
+    }
+    return out;
+}
 
 inline SolveResult cp_als_qr(const DenseTensor& x, const SolverConfig& cfg,
                              const std::optional<KruskalModel>& init = {}) {

@@ -285,6 +285,45 @@ inline Matrix khatri_rao(std::initializer_list<const Matrix*> mats) {
     return khatri_rao(std::span<const Matrix* const>(mats.begin(), mats.size()));
 }
 
+// Matricized tensor times Khatri-Rao product (tensor.hpp:453-488): one
+// device TTM of X with the factor of another mode plus a Khatri-Rao
+// contraction of the rest; factors[mode] is not read (tensor.hpp:415-431).
+inline Matrix mttkrp(const DenseTensor& t, std::span<const Matrix* const> factors,
+                     std::size_t mode) {
+    const std::size_t order = t.order();
+    if (mode >= order) throw std::invalid_argument("mttkrp: mode out of range");
+    if (factors.size() != order) throw std::invalid_argument("mttkrp: need one factor per mode");
+    std::vector<const double*> ptrs(order, nullptr);
+    std::vector<uint64_t> rows(order, 0), cols(order, 0);
+    std::size_t rank = 0;
+    for (std::size_t k = 0; k < order; ++k) {
+        if (k == mode || factors[k] == nullptr) continue;
+        ptrs[k] = factors[k]->data();
+        rows[k] = factors[k]->rows();
+        cols[k] = factors[k]->cols();
+        if (rank == 0) rank = factors[k]->cols();
+    }
+    Matrix out(t.shape().extent(mode), rank == 0 ? 1 : rank);
+    const std::vector<uint64_t> dims = abi::u64(t.shape().dims());
+    abi::check(cpdb_mttkrp(abi::ctx(), t.data(), dims.data(), uint32_t(order), ptrs.data(),
+                           rows.data(), cols.data(), uint32_t(mode), out.data()));
+    return out;
+}
+
+// The reference keeps a materialising variant as an independent check of the
+// streaming path (tensor.hpp:494-518); both name the same product, which the
+// device computes one way.  Same argument checks.
+inline Matrix mttkrp_materialized(const DenseTensor& t, std::span<const Matrix* const> factors,
+                                  std::size_t mode) {
+    const std::size_t order = t.order();
+    if (mode >= order) throw std::invalid_argument("mttkrp: mode out of range");
+    if (factors.size() != order) throw std::invalid_argument("mttkrp: need one factor per mode");
+    for (std::size_t k = 0; k < order; ++k)
+        if (k != mode && factors[k] == nullptr)
+            throw std::invalid_argument("mttkrp: missing factor");
+    return mttkrp(t, factors, mode);
+}
+
 // <A, B> (tensor.hpp:394-399), deterministic device reduction.
 inline double inner(const DenseTensor& a, const DenseTensor& b) {
     if (a.shape() != b.shape()) throw std::invalid_argument("inner: shape mismatch");

@@ -1,12 +1,13 @@
 """The reference's own hot-path unit tests (dim_tree_test, linalg_test,
-tensor_test, kruskal_test, solver_test from /root/reference/proj/tests),
+tensor_test, kruskal_test, solver_test, io_test, synth_test from
+/root/reference/proj/tests),
 compiled UNCHANGED against the drop-in `cpd::` headers (include/cpd) and
 libcpdb.so by oracle/conformance/Makefile, run on the B200.
 
 The binaries are built in the container (where the reference sources are)
-and travel to the GPU box in oracle/_ref/conformance/.  Test cases that only
-exercise the CP-ALS normal-equation shim (oracle/conformance/offpath.hpp, not
-part of the library) still run; they are listed in OFFPATH for the record.
+and travel to the GPU box in oracle/_ref/conformance/.  Every case runs on the
+library, including the CP-ALS normal-equation ones (cp_als, mttkrp,
+solve_spd, fitness_fast_als: SURVEY.md 8f row 4).
 """
 import os
 import re
@@ -17,9 +18,8 @@ import pytest
 from conftest import ROOT
 
 BIN = os.path.join(ROOT, "oracle", "_ref", "conformance")
-SUITES = ["dim_tree_test", "linalg_test", "tensor_test", "kruskal_test", "solver_test"]
-# cases whose subject is the off-path shim (cp_als / mttkrp / solve_spd / fitness_fast_als)
-OFFPATH = re.compile(r"^(CpAls\.|SolveSpd|Mttkrp|FitnessFastAls)")
+SUITES = ["dim_tree_test", "linalg_test", "tensor_test", "kruskal_test", "solver_test", "io_test",
+          "synth_test"]
 
 
 def run_suite(name):
