@@ -113,14 +113,16 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
         // phase A: A_hat = V R0^-T (+ this row's share of <V_fit, A_hat R0^T>)
         for (int li = grp; li < rows + (G - rows % G) % G; li += G) {
             const bool act = li < rows;
-            Row x;
-            x.load(a.vpart + (act ? (r0 + li) : r0) * R, act ? R : 0, q);
+            // V row = sum of the V-GEMM's split-K partials (nsplit x I x R)
+            const uint64_t roff = (act ? (r0 + li) : r0) * R;
+            Row v;
+            v.load_sum(a.vpart + roff, I * R, a.nsplit, act ? R : 0, q);
+            Row x = v;
             x.utinv(S.ut, S.dinv, R, q);
             if (a.fitness) {  // uniform branch: the lane groups shuffle inside
                 // <vf, a_hat R0^T> = sum_k a_hat[k] * (vf R0)[k]
-                Row vf, w;
-                vf.load((a.dual ? a.vfitpart : a.vpart) + (act ? (r0 + li) : r0) * R,
-                        act ? R : 0, q);
+                Row vf = v, w;
+                if (a.dual) vf.load_sum(a.vfitpart + roff, I * R, a.nsplit, act ? R : 0, q);
                 w.set_times_upper(vf, S.u, R, q);
 #pragma unroll
                 for (int s = 0; s < Row::S; ++s) xk_part = fma(x.t[s], w.t[s], xk_part);
@@ -220,7 +222,12 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
     if (rank == 0) {
         cluster_reduce(cl, S.p, R * R, S.g);
         __syncthreads();
-        const bool ok = chol<kNT, RM>(S.g, R, R);
+        CPDB_TS(19);
+        // A1 is orthonormal to working accuracy: its Gram is I + O(kappa^2 eps)
+        // (rank 0's own partial S.p and the lambda scratch are free again)
+        const int steps = near_identity_chol<kNT>(S.g, R, S.p, scratch, red);
+        if (a.ts && threadIdx.x == 0) a.ts[20] = a.ts[0] + 1000ull * steps;
+        const bool ok = steps > 0 || chol<kNT, RM>(S.g, R, R);
         if (threadIdx.x == 0) S.misc[2] = ok ? 0.0 : 1.0;
         CPDB_TS(11);
         if (ok) {
@@ -234,17 +241,28 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
             }
             __syncthreads();
             if (!a.init && a.fitness) {
+                // R0 into rank 0's free Gram partial (conflict-free reads below)
+                for (int e = threadIdx.x; e < R * R; e += kNT) S.p[e] = a.r0[e];
+                __syncthreads();
                 // ||K||^2 = sum_ij (R0^T R0)_ij l_i (Rn^T Rn)_ij l_j  (kruskal.hpp:457-462)
                 double s = 0.0;
                 for (int e = threadIdx.x; e < R * R; e += kNT) {
                     const int i = e / R, j = e % R;
-                    double p0 = 0.0, pn = 0.0;
+                    const double li = a.lambda[i], lj = a.lambda[j];
+                    double p0 = 0.0, pn = 0.0, p1 = 0.0, pm = 0.0;
                     const int top = i < j ? i : j;
-                    for (int p = 0; p <= top; ++p) {
-                        p0 = fma(a.r0[p * R + i], a.r0[p * R + j], p0);
+                    int p = 0;
+                    for (; p + 1 <= top; p += 2) {
+                        p0 = fma(S.p[p * R + i], S.p[p * R + j], p0);
+                        pn = fma(scratch[p * R + i], scratch[p * R + j], pn);
+                        p1 = fma(S.p[(p + 1) * R + i], S.p[(p + 1) * R + j], p1);
+                        pm = fma(scratch[(p + 1) * R + i], scratch[(p + 1) * R + j], pm);
+                    }
+                    if (p <= top) {
+                        p0 = fma(S.p[p * R + i], S.p[p * R + j], p0);
                         pn = fma(scratch[p * R + i], scratch[p * R + j], pn);
                     }
-                    s += p0 * a.lambda[i] * pn * a.lambda[j];
+                    s += (p0 + p1) * li * (pn + pm) * lj;
                 }
                 const double kk = block_sum<kNT>(s, red);
                 if (threadIdx.x == 0) {
@@ -313,6 +331,7 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
     const int rows = int(r0 < a.zrows ? (a.zrows - r0 < uint64_t(per) ? a.zrows - r0
                                                                       : uint64_t(per))
                                       : 0);
+    __shared__ double red[32];
     Smem<RM> S(sm, R);
     pdl_entry();
     CPDB_TS(0);
@@ -393,7 +412,12 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
         __syncthreads();
         cluster_reduce(cl, S.p, R * R, S.g);
         __syncthreads();
-        const bool ok2 = chol<kNT, RM>(S.g, R, R);
+        CPDB_TS(11);
+        // Q1 = Z U1^-1 is orthonormal to working accuracy (S.p and the
+        // Khatri-Rao inputs are free again)
+        const int steps = near_identity_chol<kNT>(S.g, R, S.p, mats, red);
+        if (a.ts && threadIdx.x == 0) a.ts[12] = a.ts[0] + 1000ull * steps;
+        const bool ok2 = steps > 0 || chol<kNT, RM>(S.g, R, R);
         if (!ok2 && threadIdx.x == 0) *a.status = 2;
         for (int e = threadIdx.x; e < R * R; e += kNT) {  // R0 = U2 U1
             const int i = e / R, j = e % R;

@@ -72,6 +72,7 @@ struct VgemmArgs {
     double* vfit_out;    // I x R: final Vfit (dual)
     uint32_t nsplit;     // out: split count used
     int reduced;         // out: 1 = V written to v_out (no reduce_splits needed)
+    uint32_t max_split;  // in: cap on the split count (0: vgemm_max_split())
 };
 cudaError_t launch_vgemm(VgemmArgs& a, cudaStream_t s, int sms);
 uint32_t vgemm_max_split();
@@ -156,6 +157,9 @@ struct FinishArgs {
     unsigned long long* ts;  // optional phase timestamps (profiling)
 };
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s);
+// true when launch_finish(I, R) sums FinishArgs::nsplit V partials itself
+// (the cluster kernel); the single-CTA kernel needs nsplit == 1
+bool finish_sums_splits(uint64_t I, uint32_t R);
 // variants (cluster.cu / finish.cu): launch_finish picks the cluster kernel
 // when its shared-memory plan fits, else the single-CTA one
 cudaError_t launch_finish_cluster(const FinishArgs& a, cudaStream_t s);

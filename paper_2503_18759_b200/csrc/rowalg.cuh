@@ -65,6 +65,21 @@ struct LaneRow {
             t[s] = k < R ? src[k] : 0.0;
         }
     }
+    // sum of n row copies src[p * stride + k], p = 0..n-1 in order (the
+    // V-GEMM's split-K partials: fixed order -> deterministic)
+    __device__ __forceinline__ void load_sum(const double* src, uint64_t stride, uint32_t n,
+                                             int R, int q) {
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int k = s * T + q;
+            double v = 0.0;
+            if (k < R) {
+#pragma unroll 8
+                for (uint32_t p = 0; p < n; ++p) v += src[p * stride + k];
+            }
+            t[s] = v;
+        }
+    }
     __device__ __forceinline__ void store(double* dst, int R, int q) const {
 #pragma unroll
         for (int s = 0; s < S; ++s) {
@@ -349,6 +364,71 @@ __device__ bool chol(double* g, int ld, int R) {
     } else {
         return block_chol<NT, (RM * RM + NT - 1) / NT>(g, ld, R);
     }
+}
+
+// ---------------------------------------------------------------- near-identity Cholesky
+// The second CholeskyQR pass factors G = Q1^T Q1 = I + E with |E| ~ kappa^2
+// eps (Q1 is already orthonormal to working accuracy).  Its Cholesky factor
+// is U = I + X, X upper, with X + X^T + X^T X = E, i.e. the fixed point
+//     X = up(E - X^T X),   up(S) = strict upper part of S + diag(S) / 2.
+// From X_1 = up(E) every step multiplies the error by ~rho = 2 R max|E|, so
+// the whole factorisation is a few R x R products (all entries in parallel)
+// instead of an R-step pivot chain (block_chol: ~8 us at R = 32).  The step
+// count is a deterministic function of max|E| (error <= 1e-18 absolute, far
+// below the rounding of U's unit diagonal).  g (stride R) holds G on entry
+// and U on exit (strict lower zeroed); xa, xb are R x R scratch.  Returns
+// the number of products + 1, or 0 (block-uniform) when |E| is too large for
+// the series: the caller then runs chol() on the untouched g.
+template <int NT>
+__device__ int near_identity_chol(double* g, int R, double* xa, double* xb, double* red) {
+    double m = 0.0;
+    for (int e = threadIdx.x; e < R * R; e += NT) {
+        const int i = e / R, j = e % R;
+        m = fmax(m, fabs(g[e] - (i == j ? 1.0 : 0.0)));
+    }
+    m = block_max<NT>(m, red);
+    const double rho = 2.0 * double(R) * m;
+    if (!(rho < 0.05)) return 0;  // (NaN lands here too)
+    int steps = 1;
+    for (double err = m * rho; err > 1e-18 && steps < 8; err *= rho) ++steps;
+    if (steps >= 8) return 0;
+    // X_1 = up(E)
+    for (int e = threadIdx.x; e < R * R; e += NT) {
+        const int i = e / R, j = e % R;
+        xa[e] = i < j ? g[e] : (i == j ? 0.5 * (g[e] - 1.0) : 0.0);
+    }
+    __syncthreads();
+    double* x = xa;
+    double* xn = xb;
+    for (int it = 1; it < steps; ++it) {
+        for (int e = threadIdx.x; e < R * R; e += NT) {
+            const int i = e / R, j = e % R;
+            double v = 0.0;
+            if (i <= j) {
+                // (X^T X)_ij = sum_{p <= i} X[p][i] X[p][j]
+                double s0 = 0.0, s1 = 0.0;
+                int p = 0;
+                for (; p + 1 <= i; p += 2) {
+                    s0 = fma(x[p * R + i], x[p * R + j], s0);
+                    s1 = fma(x[(p + 1) * R + i], x[(p + 1) * R + j], s1);
+                }
+                if (p <= i) s0 = fma(x[p * R + i], x[p * R + j], s0);
+                const double s = g[e] - (i == j ? 1.0 : 0.0) - (s0 + s1);
+                v = i < j ? s : 0.5 * s;
+            }
+            xn[e] = v;
+        }
+        __syncthreads();
+        double* t = x;
+        x = xn;
+        xn = t;
+    }
+    for (int e = threadIdx.x; e < R * R; e += NT) {
+        const int i = e / R, j = e % R;
+        g[e] = i < j ? x[e] : (i == j ? 1.0 + x[e] : 0.0);
+    }
+    __syncthreads();
+    return steps;
 }
 
 }  // namespace cpdb

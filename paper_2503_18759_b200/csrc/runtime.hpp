@@ -171,6 +171,7 @@ std::vector<uint64_t> natural_to_reference(uint32_t order, uint64_t R);
 // tensor with local extents `sd` using factor Q (I_c x R) / packed Qp.
 void run_ttm(cpdb_ctx* ctx, const double* src, const std::vector<uint64_t>& sd, uint32_t c,
              const double* q, const double* qp, uint32_t R, double* dst,
-             cudaStream_t stream = nullptr, bool one_tile_per_cta = false, bool no_pdl = false);
+             cudaStream_t stream = nullptr, bool one_tile_per_cta = false, bool no_pdl = false,
+             int sms = 0);
 
 }  // namespace cpdb

@@ -179,6 +179,12 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
                            numel(c->ldims) < (1ull << 32);
         const char* cs = std::getenv("CPDB_CHAIN_SIDE");
         chain_side = c->overlap && !sharded && !(cs && cs[0] == '0');
+        // An update that runs beside the prefetched root TTM is off the
+        // critical path (the root is): its branch TTMs and V-GEMM take a few
+        // SMs for longer instead of every SM briefly, so the root keeps more.
+        const char* os = std::getenv("CPDB_OVERLAP_SMS");
+        overlap_sms = os ? std::atoi(os) : -1;
+        if (overlap_sms >= c->sms) overlap_sms = 0;
     }
 
     // ---- factor state (factor_state.hpp:28-34) -----------------------------
@@ -343,7 +349,7 @@ void Session::pack_local0() {
 
 void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32_t flags,
                        uint32_t k, double* dst, bool is_root, cudaStream_t st, bool prefetch,
-                       bool no_pdl) {
+                       bool no_pdl, int sms) {
     if (!st) st = s;
     const double* q = fb[k].q.p;
     const double* qp = fb[k].qp.p;
@@ -359,7 +365,7 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32
         CPDB_CK(cudaEventRecord(t.a, st));
     }
     cudaEvent_t tla = tl_begin(st);
-    run_ttm(c, src, sd, k, q, qp, R, dst, st, prefetch, no_pdl);
+    run_ttm(c, src, sd, k, q, qp, R, dst, st, prefetch, no_pdl, sms);
     tl_end(tla, st, prefetch ? "root_prefetch" : is_root ? "root" : "branch");
     if (c->timing) {
         CPDB_CK(cudaEventRecord(t.b, st));
@@ -410,11 +416,36 @@ void Session::prefetch_root(uint64_t sweep, uint32_t b) {
         CPDB_CK(cudaStreamWaitEvent(c->lo, ev_fin, 0));
         ttm_step(c->x, c->ldims, 0, cm, pre.p, true, c->lo, true, true);
         CPDB_CK(cudaEventRecord(pf.ev, c->lo));
+        // SM budget of the updates in between: they are off the critical
+        // path when the root is long (it, not they, gates update b2), so their
+        // TTMs get just enough SMs to finish in about half the root's time
+        // and the root keeps the rest.  Short roots (C4: ~30 us) are not
+        // worth it (the updates become the critical path).
+        pf.sms = overlap_sms >= 0 ? overlap_sms : 0;
+        if (overlap_sms < 0) {
+            const double xb = 8.0 * double(numel(c->ldims));
+            const double root_s = std::max(2.0 * double(numel(c->ldims)) * R / 31.5e12, xb / 6.0e12);
+            double upd = 0.0;
+            for (uint32_t bm = b + 1; bm < b2; ++bm)
+                for (const Step& st : sw.updates[bm].steps) upd += step_flops(st);
+            const double per_sm = 0.15e12;  // FP64 FLOP/s per SM on a small grid
+            const int need = int(std::ceil(upd / (0.5 * root_s * per_sm)));
+            if (root_s >= 150e-6 && need < c->sms / 2) pf.sms = std::max(need, 16);
+        }
         pf.active = true;
         pf.sweep = sweep;
         pf.block = b2;
         return;
     }
+}
+
+double Session::step_flops(const Step& st) const {
+    uint64_t out = 1;
+    for (uint32_t k = 0; k < order; ++k)
+        out *= (st.produces & (1u << k)) ? c->ldims[k] : uint64_t(R);
+    return 2.0 * double(out) * double(st.source == plan.root() || (st.source & (1u << st.contract))
+                                          ? c->ldims[st.contract]
+                                          : R);
 }
 
 // ---------------------------------------------------------------- one mode update
@@ -472,7 +503,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         CPDB_CK(cudaMemcpyAsync(ts, z.ts, sizeof ts, cudaMemcpyDeviceToHost, zs));
         CPDB_CK(cudaStreamSynchronize(zs));
         std::fprintf(stderr, "zqr mode %u phases(us):", n);
-        for (int k = 1; k < 11; ++k)
+        for (int k = 1; k < 13; ++k)
             std::fprintf(stderr, " %d:%.2f", k, ts[k] ? (ts[k] - ts[0]) * 1e-3 : -1.0);
         std::fprintf(stderr, "\n");
     }
@@ -527,7 +558,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
             double* dst =
                 (st.produces == (1u << n)) ? ybuf[n].p : cache[st.produces].buf.ensure(numel(od));
             ttm_step(src, sd, flags, st.contract, dst, st.source == root, ts, false,
-                     after_wait);
+                     after_wait, budget(sweep, b));
             after_wait = false;
         }
         // global-extent flop count, exactly as the reference counts it
@@ -590,10 +621,22 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     tl_sweep = sweep;
     tl_mode = n;
     cudaEvent_t tla = tl_begin(s);
-    CPDB_CK(launch_vgemm(v, s, c->sms));
+    // partials summed by the finisher: few enough that its 8 CTAs read them
+    // quickly (env CPDB_VSPLIT_MAX, default 16)
+    static const uint32_t vsplit_max = [] {
+        const char* e = std::getenv("CPDB_VSPLIT_MAX");
+        return e ? uint32_t(std::atoi(e)) : 16u;
+    }();
+    v.max_split = (vsplit_max > 0 && !gather && finish_sums_splits(v.I, R)) ? vsplit_max : 0;
+    const int vsms = budget(sweep, b);
+    CPDB_CK(launch_vgemm(v, s, vsms > 0 ? vsms : c->sms));
     tl_end(tla, s, "vgemm");
     c->launches += 1;
-    if (!v.reduced) {
+    // the cluster finisher sums the split-K partials itself (no reduction
+    // launch on the chain); gathered (sharded mode-0) V needs them reduced
+    const bool fused = vsplit_max > 0 && !v.reduced && !gather && v.nsplit <= 64 &&
+                       finish_sums_splits(v.I, R);
+    if (!v.reduced && !fused) {
         tla = tl_begin(s);
         CPDB_CK(reduce_splits(v.vpart, v.nsplit, v.I * R, vfull.p + off, s));
         if (v.dual) CPDB_CK(reduce_splits(v.vfitpart, v.nsplit, v.I * R, vfitfull.p + off, s));
@@ -607,9 +650,9 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     // 6-9. A_hat, lambda, factor QR, fitness (solvers.hpp:272-292)
     FinishArgs f{};
     f.init = 0;
-    f.vpart = vfull.p;
-    f.vfitpart = v.dual ? vfitfull.p : nullptr;
-    f.nsplit = 1;
+    f.vpart = fused ? v.vpart : vfull.p;
+    f.vfitpart = v.dual ? (fused ? v.vfitpart : vfitfull.p) : nullptr;
+    f.nsplit = fused ? v.nsplit : 1;
     f.dual = v.dual;
     f.r0 = r0buf.p;
     f.I = c->dims[n];
@@ -639,7 +682,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
         CPDB_CK(cudaMemcpyAsync(ts, f.ts, sizeof ts, cudaMemcpyDeviceToHost, s));
         CPDB_CK(cudaStreamSynchronize(s));
         std::fprintf(stderr, "finish mode %u phases(us):", n);
-        for (int k = 1; k < 19; ++k)
+        for (int k = 1; k < 21; ++k)
             std::fprintf(stderr, " %d:%.2f", k, ts[k] ? (ts[k] - ts[0]) * 1e-3 : -1.0);
         std::fprintf(stderr, "\n");
     }

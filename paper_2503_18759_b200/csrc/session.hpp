@@ -54,12 +54,20 @@ struct Session {
         bool active = false;
         uint64_t sweep = 0;
         uint32_t block = 0;
+        int sms = 0;  // SM budget of the updates it overlaps (0: all SMs)
         cudaEvent_t ev = nullptr;
     } pf;
     DevBuf pre;
     cudaEvent_t ev_fin = nullptr;
     bool prefetch_enabled = false;
     bool chain_side = false;  // TTM chain on the side stream, Z-QR on the main one
+    // SM budget of the branch TTMs and the V-GEMM of an update that runs
+    // while a prefetched root TTM is in flight (0: all SMs)
+    int overlap_sms = -1;  // CPDB_OVERLAP_SMS: fixed budget (-1: per root, see prefetch_root)
+    int budget(uint64_t sweep, uint32_t b) const {
+        return (pf.active && pf.sweep == sweep && pf.block > b) ? pf.sms : 0;
+    }
+    double step_flops(const Step& st) const;
     std::vector<Timer> timers;
     cudaEvent_t t_start = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_zqr = nullptr;  // main -> side -> main fork/join
@@ -94,7 +102,7 @@ private:
     void pack_local0();
     void ttm_step(const double* src, const std::vector<uint64_t>& sd, int32_t flags,
                   uint32_t k, double* dst, bool is_root, cudaStream_t st = nullptr,
-                  bool prefetch = false, bool no_pdl = false);
+                  bool prefetch = false, bool no_pdl = false, int sms = 0);
     void prefetch_root(uint64_t sweep, uint32_t b);
     void mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer, void* user,
                      double& beta_used);
