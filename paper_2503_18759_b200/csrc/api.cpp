@@ -88,6 +88,9 @@ void init_ctx(cpdb_ctx* c, int device) {
     CPDB_CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, greatest));
     CPDB_CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, greatest));
     CPDB_CK(cudaStreamCreateWithPriority(&c->lo, cudaStreamNonBlocking, least));
+    // a TTM chain that must yield SMs to a concurrent multi-kernel Z-QR
+    CPDB_CK(cudaStreamCreateWithPriority(&c->mid, cudaStreamNonBlocking,
+                                         greatest < least ? greatest + 1 : greatest));
     CPDB_CK(cudaMalloc(&c->dstatus, 64));
     CPDB_CK(cudaMemset(c->dstatus, 0, 64));
     CPDB_CK(cudaMallocHost(&c->pinned, 64 * sizeof(double)));

@@ -299,6 +299,7 @@ void run_ttm(cpdb_ctx* ctx, const double* src, const std::vector<uint64_t>& sd, 
 cpdb_ctx::~cpdb_ctx() {
     if (stream) cudaStreamSynchronize(stream);
     if (lo) cudaStreamSynchronize(lo);
+    if (mid) cudaStreamSynchronize(mid);
     if (comm) {
         const cpdb::Nccl& N = cpdb::nccl();
         if (N.ok) N.CommDestroy(static_cast<ncclComm_t>(comm));
@@ -308,4 +309,5 @@ cpdb_ctx::~cpdb_ctx() {
     if (stream) cudaStreamDestroy(stream);
     if (side) cudaStreamDestroy(side);
     if (lo) cudaStreamDestroy(lo);
+    if (mid) cudaStreamDestroy(mid);
 }

@@ -74,6 +74,7 @@ Session::~Session() {
     if (c && c->stream) cudaStreamSynchronize(c->stream);
     if (c && c->side) cudaStreamSynchronize(c->side);
     if (c && c->lo) cudaStreamSynchronize(c->lo);
+    if (c && c->mid) cudaStreamSynchronize(c->mid);
     if (ev_fin) cudaEventDestroy(ev_fin);
     if (pf.ev) cudaEventDestroy(pf.ev);
     if (t_start) cudaEventDestroy(t_start);
@@ -95,7 +96,7 @@ void Session::tl_end(cudaEvent_t a, cudaStream_t st, const char* label) {
     cudaEvent_t b;
     CPDB_CK(cudaEventCreate(&b));
     CPDB_CK(cudaEventRecord(b, st));
-    const int sid = st == c->side ? 1 : st == c->lo ? 2 : 0;
+    const int sid = st == c->side ? 1 : st == c->lo ? 2 : st == c->mid ? 3 : 0;
     marks.push_back(Mark{label, sid, tl_sweep, tl_mode, a, b});
 }
 
@@ -182,6 +183,8 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         // An update that runs beside the prefetched root TTM is off the
         // critical path (the root is): its branch TTMs and V-GEMM take a few
         // SMs for longer instead of every SM briefly, so the root keeps more.
+        const char* zy = std::getenv("CPDB_ZQR_YIELD");
+        zqr_yield = chain_side && zy && zy[0] == '1' && !zqr_cluster_fits(zrows, R, order - 1);
         const char* os = std::getenv("CPDB_OVERLAP_SMS");
         overlap_sms = os ? std::atoi(os) : -1;
         if (overlap_sms >= c->sms) overlap_sms = 0;
@@ -365,7 +368,7 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32
         CPDB_CK(cudaEventRecord(t.a, st));
     }
     cudaEvent_t tla = tl_begin(st);
-    run_ttm(c, src, sd, k, q, qp, R, dst, st, prefetch, no_pdl, sms);
+    run_ttm(c, src, sd, k, q, qp, R, dst, st, prefetch || yield_now, no_pdl, sms);
     tl_end(tla, st, prefetch ? "root_prefetch" : is_root ? "root" : "branch");
     if (c->timing) {
         CPDB_CK(cudaEventRecord(t.b, st));
@@ -489,8 +492,9 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         z.ts = reinterpret_cast<unsigned long long*>(zts.ensure(32));
         CPDB_CK(cudaMemsetAsync(z.ts, 0, 32 * sizeof(double), zs));
     }
+    const cudaStream_t ts = chain_side ? (zqr_yield ? c->mid : c->side) : s;
     CPDB_CK(cudaEventRecord(ev_ready, s));
-    CPDB_CK(cudaStreamWaitEvent(c->side, ev_ready, 0));
+    CPDB_CK(cudaStreamWaitEvent(chain_side ? ts : c->side, ev_ready, 0));
     z.pdl = chain_side && !trace_phases ? 1 : 0;
     tl_sweep = sweep;
     tl_mode = n;
@@ -518,7 +522,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         observer(user, sweep, n, ref.data(), zrows, R);
     }
     // 4. the scheduled TTM chain (execute, dim_tree.hpp:496-541)
-    const cudaStream_t ts = chain_side ? c->side : s;
+    yield_now = zqr_yield;
     bool after_wait = chain_side;  // the side stream's first kernel follows an event wait
     for (size_t si = 0; si < sw.updates[b].steps.size(); ++si) {
         const Step& st = sw.updates[b].steps[si];
@@ -579,7 +583,8 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     const std::vector<ModeSet> keep = retained_keys(plan, sweep - 1, b);
     for (auto& kv : cache)
         if (std::find(keep.begin(), keep.end(), kv.first) == keep.end()) kv.second.valid = false;
-    if (chain_side) CPDB_CK(cudaEventRecord(ev_zqr, c->side));  // join: V needs Y_(n)
+    yield_now = false;
+    if (chain_side) CPDB_CK(cudaEventRecord(ev_zqr, ts));  // join: V needs Y_(n)
 
 }
 

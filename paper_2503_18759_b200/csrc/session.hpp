@@ -68,6 +68,12 @@ struct Session {
         return (pf.active && pf.sweep == sweep && pf.block > b) ? pf.sms : 0;
     }
     double step_flops(const Step& st) const;
+    // tall Z (multi-kernel Z-QR, C5): the TTM chain runs one tile per CTA on
+    // the mid-priority stream so the Z-QR's CTAs take SMs as tiles retire
+    // instead of waiting for a persistent grid to drain (CPDB_ZQR_YIELD=1; off by
+    // default: measured at C5 the one-tile TTMs lose more than the Z-QR gains)
+    bool zqr_yield = false;
+    bool yield_now = false;
     std::vector<Timer> timers;
     cudaEvent_t t_start = nullptr;
     cudaEvent_t ev_ready = nullptr, ev_zqr = nullptr;  // main -> side -> main fork/join

@@ -515,7 +515,10 @@ cudaError_t vgemm_run(VgemmArgs& a, cudaStream_t s, int sms) {
         const uint64_t ktiles = (K + kDK - 1) / kDK;
         uint64_t nsplit = std::max<uint64_t>(1, (2 * uint64_t(sms)) / iblocks);
         nsplit = std::min<uint64_t>({nsplit, ktiles, uint64_t(vgemm_max_split())});
-        if (a.max_split) nsplit = std::min<uint64_t>(nsplit, a.max_split);
+        // the cap only bites when the CTAs' K-chunks are short (C2: 2 tiles);
+        // long-K V-GEMMs (C5) keep the full split
+        if (a.max_split)
+            nsplit = std::min<uint64_t>(nsplit, std::max<uint64_t>(a.max_split, ktiles / 8));
         const uint64_t kchunk = ((ktiles + nsplit - 1) / nsplit) * kDK;
         nsplit = (K + kchunk - 1) / kchunk;
         a.nsplit = uint32_t(nsplit);

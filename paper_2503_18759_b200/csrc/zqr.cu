@@ -74,18 +74,24 @@ __global__ void __launch_bounds__(kNT) zqr_rows_kernel(ZqrArgs a, int tile_rows)
         for (int li = grp; li < tile_rows + (G - tile_rows % G) % G; li += G) {
             const bool act = li < rows;
             Row x;
+            // the row's digits once (32-bit: zrows < 2^32 on this path),
+            // shared by the lane group's columns
+            int off[8];
+            {
+                uint32_t rem = uint32_t(row0) + uint32_t(act ? li : 0);
+                for (int k = nm - 1; k >= 0; --k) {
+                    const uint32_t qt = rem / uint32_t(R);
+                    off[k] = (k * R + int(rem - qt * uint32_t(R))) * R;
+                    rem = qt;
+                }
+            }
 #pragma unroll
             for (int s = 0; s < Row::S; ++s) {
                 const int c = s * T + q;
                 double z = 0.0;
                 if (c < R && act) {
-                    uint64_t rem = row0 + li;
-                    for (int k = nm - 1; k >= 0; --k) {
-                        const int dig = int(rem % R);
-                        rem /= R;
-                        const double v = mats[(k * R + dig) * R + c];
-                        z = (k == nm - 1) ? v : z * v;
-                    }
+                    z = mats[off[nm - 1] + c];
+                    for (int k = nm - 2; k >= 0; --k) z *= mats[off[k] + c];
                 }
                 x.t[s] = z;
             }
@@ -131,7 +137,11 @@ __global__ void __launch_bounds__(kNT) zqr_fin_kernel(ZqrArgs a) {
         u1[e] = a.work[e];
     }
     __syncthreads();
-    if (!chol<kNT, RM>(g, R, R) && threadIdx.x == 0) *a.status = 2;
+    // G2 = Q1^T Q1 = I + O(kappa^2 eps): series factorisation (rowalg.cuh)
+    __shared__ double red[32];
+    const bool ok = near_identity_chol<kNT>(g, R, g + 2 * R * R, g + 3 * R * R, red) > 0 ||
+                    chol<kNT, RM>(g, R, R);
+    if (!ok && threadIdx.x == 0) *a.status = 2;
     for (int e = threadIdx.x; e < R * R; e += kNT) {
         const int i = e / R, j = e % R;
         double s = 0.0;
@@ -166,6 +176,7 @@ __global__ void __launch_bounds__(kNT) zqr_apply_kernel(ZqrArgs a) {
 template <int RM>
 cudaError_t run_multi(const ZqrArgs& a, cudaStream_t s, int sms) {
     const int R = a.R;
+    if (a.zrows >= (1ull << 32)) return cudaErrorInvalidValue;  // 32-bit row digits
     const size_t fixed = size_t(a.nm) * R * R + RM * RM + RM + size_t(R) * R;
     constexpr size_t kBudget = 220 * 1024 / sizeof(double);
     if (fixed + 32 * size_t(R + 1) > kBudget) return cudaErrorInvalidValue;
@@ -181,9 +192,9 @@ cudaError_t run_multi(const ZqrArgs& a, cudaStream_t s, int sms) {
     zqr_rows_kernel<RM><<<grid, kNT, rows_smem, s>>>(a, tile);
     zqr_reduce_kernel<<<(R * R + kNT - 1) / kNT, kNT, 0, s>>>(a, grid);
     e = cudaFuncSetAttribute(zqr_fin_kernel<RM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             int(2 * RM * RM * sizeof(double)));
+                             int(4 * RM * RM * sizeof(double)));
     if (e != cudaSuccess) return e;
-    zqr_fin_kernel<RM><<<1, kNT, 2 * size_t(R) * R * sizeof(double), s>>>(a);
+    zqr_fin_kernel<RM><<<1, kNT, 4 * size_t(R) * R * sizeof(double), s>>>(a);
     const uint64_t groups = (a.zrows + (kNT / LaneRow<RM>::T) - 1) / (kNT / LaneRow<RM>::T);
     const int agrid = int(std::min<uint64_t>(groups, uint64_t(4 * sms)));
     zqr_apply_kernel<RM><<<agrid, kNT, 0, s>>>(a);
