@@ -37,6 +37,7 @@ constexpr int kNT = 512;  // threads per CTA
 
 // rank 0: G = sum_r P_r over the cluster, fixed rank order
 __device__ void cluster_reduce(cg::cluster_group& cl, const double* P, int n, double* G) {
+#pragma unroll 1
     for (int e = threadIdx.x; e < n; e += kNT) {
         double s = 0.0;
 #pragma unroll
@@ -130,6 +131,7 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
             if (act) x.store(S.w + li * ld, R, q);
         }
     } else {
+#pragma unroll 1
         for (int e = threadIdx.x; e < rows * R; e += kNT)
             S.w[(e / R) * ld + e % R] = a.a_out[(r0 + e / R) * R + e % R];
     }
@@ -155,12 +157,14 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
         CPDB_TS(4);
         if (!a.init) {
             // lambda = column norms of A_hat = sqrt(diag G); G1 = D G D
+#pragma unroll 1
             for (int c = threadIdx.x; c < R; c += kNT) {
                 const double l = sqrt(S.g[c * R + c]);
                 scratch[c] = l;                             // lambda (published)
                 S.vec[c] = l < 1e-300 ? 0.0 : __drcp_rn(l);  // 1/lambda
             }
             __syncthreads();
+#pragma unroll 1
             for (int e = threadIdx.x; e < R * R; e += kNT) {
                 const double li = S.vec[e / R], lj = S.vec[e % R];
                 S.g[e] = (li == 0.0 || lj == 0.0) ? (e / R == e % R ? 1.0 : 0.0)
@@ -179,6 +183,7 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
         stage_tri<RM>(g0, R, R, S.u, S.dinv, kNT);
         if (!a.init) {
             const double* l0 = cl.map_shared_rank(scratch, 0);
+#pragma unroll 1
             for (int c = threadIdx.x; c < RM; c += kNT) {
                 const double l = c < R ? l0[c] : 0.0;
                 S.vec[c] = l < 1e-300 ? 0.0 : __drcp_rn(l);
@@ -232,6 +237,7 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
         CPDB_TS(11);
         if (ok) {
             // R_n = U2 U1 (U1 in S.u, stride RM)
+#pragma unroll 1
             for (int e = threadIdx.x; e < R * R; e += kNT) {
                 const int i = e / R, j = e % R;
                 double s = 0.0;
@@ -242,10 +248,12 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
             __syncthreads();
             if (!a.init && a.fitness) {
                 // R0 into rank 0's free Gram partial (conflict-free reads below)
+#pragma unroll 1
                 for (int e = threadIdx.x; e < R * R; e += kNT) S.p[e] = a.r0[e];
                 __syncthreads();
                 // ||K||^2 = sum_ij (R0^T R0)_ij l_i (Rn^T Rn)_ij l_j  (kruskal.hpp:457-462)
                 double s = 0.0;
+#pragma unroll 1
                 for (int e = threadIdx.x; e < R * R; e += kNT) {
                     const int i = e / R, j = e % R;
                     const double li = a.lambda[i], lj = a.lambda[j];
@@ -275,6 +283,7 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
             // zero padding rows of the packed Q (k >= I)
             const uint32_t Rp = ttm_rpad_dev(R);
             const uint64_t Kpad = ((I + 31) / 32) * 32;
+#pragma unroll 1
             for (uint64_t e = I * Rp + threadIdx.x; e < Kpad * Rp; e += kNT) {
                 const uint64_t k = e / Rp, r = e % Rp;
                 a.qp_out[((k >> 2) * Rp + r) * 4 + (k & 3)] = 0.0;
@@ -340,10 +349,12 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
     const int grp = threadIdx.x / T, q = threadIdx.x % T;
 
     for (int t = 0; t < nm; ++t)
+#pragma unroll 1
         for (int e = threadIdx.x; e < R * R; e += kNT) mats[t * R * R + e] = a.rmats[t][e];
     __syncthreads();
     // G1 = Hadamard_t (R_t^T R_t), computed redundantly by every rank (tiny);
     // four independent accumulators break the FMA dependency chain
+#pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) {
         const int i = e / R, j = e % R;
         const int lo = i < j ? i : j, hi = i < j ? j : i;
@@ -376,26 +387,27 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
     for (int li = grp; li < rows + (G - rows % G) % G; li += G) {
         const bool act = li < rows;
         Row x;
-        // digits of the row index (32-bit: the cluster path has R^(N-1) rows
-        // in shared memory), shared by the lane group's columns
-        int digs[8];
+        // Z row = product over the other modes (descending, like the
+        // reference Khatri-Rao fold) of one row of each R_k; the row index's
+        // digits are peeled in the same order (32-bit: the cluster path has
+        // R^(N-1) rows in shared memory).  Rolled over the modes: compact code.
         {
             uint32_t rem = uint32_t(r0) + uint32_t(act ? li : 0);
+#pragma unroll 1
             for (int k = nm - 1; k >= 0; --k) {
                 const uint32_t qt = rem / uint32_t(R);
-                digs[k] = int(rem - qt * uint32_t(R));
+                const double* m = mats + (k * R + int(rem - qt * uint32_t(R))) * R;
                 rem = qt;
-            }
-        }
 #pragma unroll
-        for (int s = 0; s < Row::S; ++s) {
-            const int c = s * T + q;
-            double z = 0.0;
-            if (c < R && act) {
-                z = mats[((nm - 1) * R + digs[nm - 1]) * R + c];
-                for (int k = nm - 2; k >= 0; --k) z *= mats[(k * R + digs[k]) * R + c];
+                for (int s = 0; s < Row::S; ++s) {
+                    const int c = s * T + q;
+                    const double v = m[c < R ? c : 0];
+                    x.t[s] = (k == nm - 1) ? v : x.t[s] * v;
+                }
             }
-            x.t[s] = z;
+#pragma unroll
+            for (int s = 0; s < Row::S; ++s)
+                if (!(act && s * T + q < R)) x.t[s] = 0.0;
         }
         x.uinv(S.u, S.dinv, R, q);
         if (act) x.store(S.w + li * ld, R, q);
@@ -408,6 +420,7 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
     CPDB_TS(5);
     if (rank == 0) {
         double* u1 = S.w + per * ld;  // keep U1 (stride R) for R0 = U2 U1
+#pragma unroll 1
         for (int e = threadIdx.x; e < R * R; e += kNT) u1[e] = S.g[e];
         __syncthreads();
         cluster_reduce(cl, S.p, R * R, S.g);
@@ -419,6 +432,7 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
         if (a.ts && threadIdx.x == 0) a.ts[12] = a.ts[0] + 1000ull * steps;
         const bool ok2 = steps > 0 || chol<kNT, RM>(S.g, R, R);
         if (!ok2 && threadIdx.x == 0) *a.status = 2;
+#pragma unroll 1
         for (int e = threadIdx.x; e < R * R; e += kNT) {  // R0 = U2 U1
             const int i = e / R, j = e % R;
             double s0 = 0.0, s1 = 0.0;
@@ -478,6 +492,7 @@ __global__ void __launch_bounds__(kNT) als_finish_cluster_kernel(AlsFinishArgs a
 
     if (rank == 0) {
         double mabs = 0.0, masym = 0.0;
+#pragma unroll 1
         for (int e = threadIdx.x; e < R * R; e += kNT) {
             double h = 1.0;
             for (uint32_t t = 0; t < a.ng; ++t) h = h * a.grams[t][e];
@@ -485,6 +500,7 @@ __global__ void __launch_bounds__(kNT) als_finish_cluster_kernel(AlsFinishArgs a
             S.g[e] = h;
         }
         __syncthreads();
+#pragma unroll 1
         for (int e = threadIdx.x; e < R * R; e += kNT) {
             const int i = e / R, j = e % R;
             mabs = fmax(mabs, fabs(gam[e]));
@@ -501,6 +517,7 @@ __global__ void __launch_bounds__(kNT) als_finish_cluster_kernel(AlsFinishArgs a
                 double tr = 0.0;
                 for (int i = 0; i < R; ++i) tr += gam[i * R + i];
                 const double delta = 1e-12 * tr / double(R);
+#pragma unroll 1
                 for (int e = threadIdx.x; e < R * R; e += kNT)
                     S.g[e] = gam[e] + ((e / R == e % R) ? delta : 0.0);
                 __syncthreads();
@@ -558,11 +575,13 @@ __global__ void __launch_bounds__(kNT) als_finish_cluster_kernel(AlsFinishArgs a
             S.misc[1] = x;  // <M, A_hat>
         }
         __syncthreads();
+#pragma unroll 1
         for (int c = threadIdx.x; c < R; c += kNT) S.vec[c] = sqrt(S.g[c * R + c]);  // lambda
     }
     cl.sync();  // ---- 3: lambda published (rank 0's vec)
     {
         const double* l0 = cl.map_shared_rank(S.vec, 0);
+#pragma unroll 1
         for (int c = threadIdx.x; c < RM; c += kNT) {
             const double l = c < R ? l0[c] : 0.0;
             S.dinv[c] = l < 1e-300 ? 0.0 : __drcp_rn(l);  // 1/lambda (U is no longer needed)
@@ -571,6 +590,7 @@ __global__ void __launch_bounds__(kNT) als_finish_cluster_kernel(AlsFinishArgs a
     }
     __syncthreads();
     // A_n = A_hat / lambda (vanishing column -> e1, weight 0)
+#pragma unroll 1
     for (int e = threadIdx.x; e < rows * R; e += kNT) {
         const int li = e / R, c = e % R;
         const double il = S.dinv[c];
@@ -584,10 +604,12 @@ __global__ void __launch_bounds__(kNT) als_finish_cluster_kernel(AlsFinishArgs a
     if (rank == 0) {
         cluster_reduce(cl, S.p, R * R, S.g);
         __syncthreads();
+#pragma unroll 1
         for (int e = threadIdx.x; e < R * R; e += kNT) a.g_out[e] = S.g[e];
         if (a.fitness) {
             // ||K||^2 = sum_ij Gamma_ij l_i G_ij l_j  (kruskal.hpp:97-100)
             double kk = 0.0;
+#pragma unroll 1
             for (int e = threadIdx.x; e < R * R; e += kNT) {
                 const int i = e / R, j = e % R;
                 const double li = S.vec[i] < 1e-300 ? 0.0 : S.vec[i];

@@ -63,18 +63,21 @@ __global__ void __launch_bounds__(kNT) finish_single_kernel(FinishArgs a, int w_
             if (act) x.store(w + i * ld, R, q);
         }
     } else {
+#pragma unroll 1
         for (int e = threadIdx.x; e < I * R; e += kNT) w[(e / R) * ld + e % R] = a.a_out[e];
     }
     __syncthreads();
     gram_dmma<kNT>(w, ld, I, R, g, R);
     __syncthreads();
     if (!a.init) {
+#pragma unroll 1
         for (int c = threadIdx.x; c < RM; c += kNT) {
             const double l = c < R ? sqrt(g[c * R + c]) : 0.0;
             vec[c] = l < 1e-300 ? 0.0 : __drcp_rn(l);
             if (c < R) a.lambda[c] = l < 1e-300 ? 0.0 : l;
         }
         __syncthreads();
+#pragma unroll 1
         for (int e = threadIdx.x; e < R * R; e += kNT) {
             const double li = vec[e / R], lj = vec[e % R];
             g[e] = (li == 0.0 || lj == 0.0) ? (e / R == e % R ? 1.0 : 0.0) : g[e] * li * lj;
@@ -85,6 +88,7 @@ __global__ void __launch_bounds__(kNT) finish_single_kernel(FinishArgs a, int w_
         if (threadIdx.x == 0) *a.status = 2;
         return;
     }
+#pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) g1[e] = g[e];
     stage_tri<RM>(g, R, R, u, dinv, kNT);
     __syncthreads();
@@ -136,6 +140,7 @@ __global__ void __launch_bounds__(kNT) finish_single_kernel(FinishArgs a, int w_
         const uint64_t k = e / Rp, r = e % Rp;
         a.qp_out[((k >> 2) * Rp + r) * 4 + (k & 3)] = 0.0;
     }
+#pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) {
         const int i = e / R, j = e % R;
         double s = 0.0;
@@ -145,6 +150,7 @@ __global__ void __launch_bounds__(kNT) finish_single_kernel(FinishArgs a, int w_
     __syncthreads();
     if (a.fitness && !a.init) {
         double s = 0.0;
+#pragma unroll 1
         for (int e = threadIdx.x; e < R * R; e += kNT) {
             const int i = e / R, j = e % R;
             double p0 = 0.0, pn = 0.0;

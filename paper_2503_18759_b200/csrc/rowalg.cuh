@@ -70,14 +70,29 @@ struct LaneRow {
     __device__ __forceinline__ void load_sum(const double* src, uint64_t stride, uint32_t n,
                                              int R, int q) {
 #pragma unroll
-        for (int s = 0; s < S; ++s) {
-            const int k = s * T + q;
-            double v = 0.0;
-            if (k < R) {
-#pragma unroll 8
-                for (uint32_t p = 0; p < n; ++p) v += src[p * stride + k];
-            }
-            t[s] = v;
+        for (int s = 0; s < S; ++s) t[s] = 0.0;
+        // four partials' loads in flight per step, summed in order
+        uint32_t p = 0;
+#pragma unroll 1
+        for (; p + 4 <= n; p += 4) {
+            const double* row = src + p * stride + q;
+            double v[4][S];
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int s = 0; s < S; ++s)
+                    v[u][s] = s * T + q < R ? row[u * stride + s * T] : 0.0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u)
+#pragma unroll
+                for (int s = 0; s < S; ++s) t[s] += v[u][s];
+        }
+#pragma unroll 1
+        for (; p < n; ++p) {
+            const double* row = src + p * stride + q;
+#pragma unroll
+            for (int s = 0; s < S; ++s)
+                if (s * T + q < R) t[s] += row[s * T];
         }
     }
     __device__ __forceinline__ void store(double* dst, int R, int q) const {
@@ -87,25 +102,31 @@ struct LaneRow {
             if (k < R) dst[k] = t[s];
         }
     }
+    // The solves below run j (the pivot column) as an UNROLLED loop over the
+    // owner's slot js and a ROLLED loop over the owner lane o (j = js*T + o),
+    // so every register index stays static while the code is S x (S FMAs)
+    // instead of RM x S.  Measured (ncu source counters, C2): the fully
+    // unrolled form made the mode-update kernels instruction-fetch bound
+    // (~12k SASS instructions executed once per launch, "no instruction"
+    // the top stall of their serial phases).  Same operations in the same
+    // order as the unrolled form -> bit-identical results.
+
     // x <- x U^-1, U upper with stride RM (zero padded, unit diagonal beyond
     // R), dinv[j] = 1/U[j][j]: right-looking forward substitution.
     __device__ __forceinline__ void uinv(const double* U, const double* dinv, int R, int q) {
 #pragma unroll
-        for (int j = 0; j < RM; ++j) {
-            if (j < R) {
-                constexpr int dummy = 0;
-                (void)dummy;
-                const int owner = j % T, slot = j / T;
-                double xj = t[slot] * dinv[j];
-                xj = __shfl_sync(0xffffffffu, xj, owner, T);
-                if (q == owner) t[slot] = xj;
+        for (int js = 0; js < S; ++js) {
+#pragma unroll 1
+            for (int o = 0; o < T; ++o) {
+                const int j = js * T + o;
+                if (j >= R) break;  // uniform
+                double xj = t[js] * dinv[j];
+                xj = __shfl_sync(0xffffffffu, xj, o, T);
+                const double* Uj = U + j * RM + q;
+                if (q == o) t[js] = xj;
+                else if (q > o) t[js] = fma(-xj, Uj[js * T], t[js]);
 #pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    if (s * T + T - 1 > j) {  // compile-time: slot may hold a k > j
-                        const int k = s * T + q;
-                        if (k > j) t[s] = fma(-xj, U[j * RM + k], t[s]);
-                    }
-                }
+                for (int s2 = js + 1; s2 < S; ++s2) t[s2] = fma(-xj, Uj[s2 * T], t[s2]);
             }
         }
     }
@@ -115,19 +136,18 @@ struct LaneRow {
     // Ut is U TRANSPOSED (stride RM), so a lane group reads consecutive words.
     __device__ __forceinline__ void utinv(const double* Ut, const double* dinv, int R, int q) {
 #pragma unroll
-        for (int c = RM - 1; c >= 0; --c) {
-            if (c < R) {
-                const int owner = c % T, slot = c / T;
-                double xc = t[slot] * dinv[c];
-                xc = __shfl_sync(0xffffffffu, xc, owner, T);
-                if (q == owner) t[slot] = xc;
+        for (int cs = S - 1; cs >= 0; --cs) {
+#pragma unroll 1
+            for (int o = T - 1; o >= 0; --o) {
+                const int c = cs * T + o;
+                if (c >= R) continue;  // uniform
+                double xc = t[cs] * dinv[c];
+                xc = __shfl_sync(0xffffffffu, xc, o, T);
+                const double* Uc = Ut + c * RM + q;
+                if (q == o) t[cs] = xc;
+                else if (q < o) t[cs] = fma(-xc, Uc[cs * T], t[cs]);
 #pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    if (s * T < c) {  // compile-time: slot may hold a k < c
-                        const int k = s * T + q;
-                        if (k < c) t[s] = fma(-xc, Ut[c * RM + k], t[s]);
-                    }
-                }
+                for (int s2 = 0; s2 < cs; ++s2) t[s2] = fma(-xc, Uc[s2 * T], t[s2]);
             }
         }
     }
@@ -137,16 +157,16 @@ struct LaneRow {
 #pragma unroll
         for (int s = 0; s < S; ++s) t[s] = 0.0;
 #pragma unroll
-        for (int j = 0; j < RM; ++j) {
-            if (j < R) {
-                const double vj = __shfl_sync(0xffffffffu, v.t[j / T], j % T, T);
+        for (int js = 0; js < S; ++js) {
+#pragma unroll 1
+            for (int o = 0; o < T; ++o) {
+                const int j = js * T + o;
+                if (j >= R) break;  // uniform
+                const double vj = __shfl_sync(0xffffffffu, v.t[js], o, T);
+                const double* Uj = U + j * RM + q;
+                if (q >= o) t[js] = fma(vj, Uj[js * T], t[js]);
 #pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    if (s * T + T - 1 >= j) {
-                        const int k = s * T + q;
-                        if (k >= j) t[s] = fma(vj, U[j * RM + k], t[s]);
-                    }
-                }
+                for (int s2 = js + 1; s2 < S; ++s2) t[s2] = fma(vj, Uj[s2 * T], t[s2]);
             }
         }
     }
@@ -163,10 +183,12 @@ struct LaneRow {
 template <int RM>
 __device__ void stage_tri(const double* src, int ld_src, int R, double* dst, double* dinv,
                           int nthreads) {
+#pragma unroll 1
     for (int e = threadIdx.x; e < RM * RM; e += nthreads) {
         const int i = e / RM, j = e % RM;
         dst[e] = (i < R && j < R) ? src[i * ld_src + j] : (i == j ? 1.0 : 0.0);
     }
+#pragma unroll 1
     for (int j = threadIdx.x; j < RM; j += nthreads)
         dinv[j] = j < R ? __drcp_rn(src[j * ld_src + j]) : 1.0;
 }
@@ -175,10 +197,12 @@ __device__ void stage_tri(const double* src, int ld_src, int R, double* dst, dou
 template <int RM>
 __device__ void stage_tri_t(const double* src, int ld_src, int R, double* dst, double* dinv,
                             int nthreads) {
+#pragma unroll 1
     for (int e = threadIdx.x; e < RM * RM; e += nthreads) {
         const int i = e / RM, j = e % RM;
         dst[j * RM + i] = (i < R && j < R) ? src[i * ld_src + j] : (i == j ? 1.0 : 0.0);
     }
+#pragma unroll 1
     for (int j = threadIdx.x; j < RM; j += nthreads)
         dinv[j] = j < R ? __drcp_rn(src[j * ld_src + j]) : 1.0;
 }
@@ -280,8 +304,10 @@ __device__ bool block_chol(double* g, int ld, int R) {
         return false;
     }
     __shared__ double rs[64];
+#pragma unroll 1
     for (int j = threadIdx.x; j < R; j += NT) rs[j] = rsqrt(g[j * ld + j]);
     __syncthreads();
+#pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += NT) {
         const int i = e / R, k = e % R;
         g[i * ld + k] = k >= i ? g[i * ld + k] * rs[i] : 0.0;
@@ -340,8 +366,10 @@ __device__ bool reg_chol(double* g, int ld, int R) {
     __syncthreads();
     if (bad) return false;
     __shared__ double rs[64];
+#pragma unroll 1
     for (int j = threadIdx.x; j < R; j += NT) rs[j] = rsqrt(g[j * ld + j]);
     __syncthreads();
+#pragma unroll 1
     for (int x = threadIdx.x; x < R * R; x += NT) {
         const int i = x / R, k = x % R;
         g[i * ld + k] = k >= i ? g[i * ld + k] * rs[i] : 0.0;
@@ -382,6 +410,7 @@ __device__ bool chol(double* g, int ld, int R) {
 template <int NT>
 __device__ int near_identity_chol(double* g, int R, double* xa, double* xb, double* red) {
     double m = 0.0;
+#pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += NT) {
         const int i = e / R, j = e % R;
         m = fmax(m, fabs(g[e] - (i == j ? 1.0 : 0.0)));
@@ -393,6 +422,7 @@ __device__ int near_identity_chol(double* g, int R, double* xa, double* xb, doub
     for (double err = m * rho; err > 1e-18 && steps < 8; err *= rho) ++steps;
     if (steps >= 8) return 0;
     // X_1 = up(E)
+#pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += NT) {
         const int i = e / R, j = e % R;
         xa[e] = i < j ? g[e] : (i == j ? 0.5 * (g[e] - 1.0) : 0.0);
@@ -401,6 +431,7 @@ __device__ int near_identity_chol(double* g, int R, double* xa, double* xb, doub
     double* x = xa;
     double* xn = xb;
     for (int it = 1; it < steps; ++it) {
+#pragma unroll 1
         for (int e = threadIdx.x; e < R * R; e += NT) {
             const int i = e / R, j = e % R;
             double v = 0.0;
@@ -423,6 +454,7 @@ __device__ int near_identity_chol(double* g, int R, double* xa, double* xb, doub
         x = xn;
         xn = t;
     }
+#pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += NT) {
         const int i = e / R, j = e % R;
         g[e] = i < j ? x[e] : (i == j ? 1.0 + x[e] : 0.0);

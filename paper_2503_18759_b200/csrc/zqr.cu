@@ -32,6 +32,7 @@ __global__ void __launch_bounds__(kNT) zqr_prep_kernel(ZqrArgs a) {
     extern __shared__ double sm[];
     const int R = a.R, nm = a.nm;
     double* g = sm;
+#pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) {
         const int p = e / R, q = e % R;
         const int lo = p < q ? p : q, hi = p < q ? q : p;
@@ -46,6 +47,7 @@ __global__ void __launch_bounds__(kNT) zqr_prep_kernel(ZqrArgs a) {
     }
     __syncthreads();
     if (!chol<kNT, RM>(g, R, R) && threadIdx.x == 0) *a.status = 2;
+#pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) a.work[e] = g[e];
 }
 
@@ -62,8 +64,10 @@ __global__ void __launch_bounds__(kNT) zqr_rows_kernel(ZqrArgs a, int tile_rows)
     double* part = dinv + RM;          // R x R  (this CTA's G2 partial)
     double* tile = part + R * R;       // kTile x (R+1)
     for (int t = 0; t < nm; ++t)
+#pragma unroll 1
         for (int e = threadIdx.x; e < R * R; e += kNT) mats[t * R * R + e] = a.rmats[t][e];
     stage_tri<RM>(a.work, R, R, u, dinv, kNT);
+#pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) part[e] = 0.0;
     const int grp = threadIdx.x / T, q = threadIdx.x % T;
     const uint64_t ntiles = (a.zrows + tile_rows - 1) / tile_rows;
@@ -74,26 +78,26 @@ __global__ void __launch_bounds__(kNT) zqr_rows_kernel(ZqrArgs a, int tile_rows)
         for (int li = grp; li < tile_rows + (G - tile_rows % G) % G; li += G) {
             const bool act = li < rows;
             Row x;
-            // the row's digits once (32-bit: zrows < 2^32 on this path),
-            // shared by the lane group's columns
-            int off[8];
+            // Z row = product over the other modes (descending, like the
+            // reference Khatri-Rao fold), digits peeled in the same order
+            // (32-bit: zrows < 2^32 on this path); rolled over the modes
             {
                 uint32_t rem = uint32_t(row0) + uint32_t(act ? li : 0);
+#pragma unroll 1
                 for (int k = nm - 1; k >= 0; --k) {
                     const uint32_t qt = rem / uint32_t(R);
-                    off[k] = (k * R + int(rem - qt * uint32_t(R))) * R;
+                    const double* m = mats + (k * R + int(rem - qt * uint32_t(R))) * R;
                     rem = qt;
-                }
-            }
 #pragma unroll
-            for (int s = 0; s < Row::S; ++s) {
-                const int c = s * T + q;
-                double z = 0.0;
-                if (c < R && act) {
-                    z = mats[off[nm - 1] + c];
-                    for (int k = nm - 2; k >= 0; --k) z *= mats[off[k] + c];
+                    for (int s = 0; s < Row::S; ++s) {
+                        const int c = s * T + q;
+                        const double v = m[c < R ? c : 0];
+                        x.t[s] = (k == nm - 1) ? v : x.t[s] * v;
+                    }
                 }
-                x.t[s] = z;
+#pragma unroll
+                for (int s = 0; s < Row::S; ++s)
+                    if (!(act && s * T + q < R)) x.t[s] = 0.0;
             }
             x.uinv(u, dinv, R, q);
             if (act) {
@@ -106,6 +110,7 @@ __global__ void __launch_bounds__(kNT) zqr_rows_kernel(ZqrArgs a, int tile_rows)
     }
     __syncthreads();
     double* out = a.work + 2 * R * R + size_t(blockIdx.x) * R * R;
+#pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) out[e] = part[e];
 }
 
@@ -132,6 +137,7 @@ __global__ void __launch_bounds__(kNT) zqr_fin_kernel(ZqrArgs a) {
     const int R = a.R;
     double* g = sm;
     double* u1 = g + R * R;
+#pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) {
         g[e] = a.work[R * R + e];
         u1[e] = a.work[e];
@@ -142,6 +148,7 @@ __global__ void __launch_bounds__(kNT) zqr_fin_kernel(ZqrArgs a) {
     const bool ok = near_identity_chol<kNT>(g, R, g + 2 * R * R, g + 3 * R * R, red) > 0 ||
                     chol<kNT, RM>(g, R, R);
     if (!ok && threadIdx.x == 0) *a.status = 2;
+#pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) {
         const int i = e / R, j = e % R;
         double s = 0.0;
