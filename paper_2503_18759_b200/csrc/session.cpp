@@ -80,6 +80,13 @@ Session::~Session() {
     if (t_start) cudaEventDestroy(t_start);
     if (ev_ready) cudaEventDestroy(ev_ready);
     if (ev_zqr) cudaEventDestroy(ev_zqr);
+    if (ev_zq) cudaEventDestroy(ev_zq);
+    for (cudaEvent_t e : ev_fac)
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_v)
+        if (e) cudaEventDestroy(e);
+    for (cudaEvent_t e : ev_zread)
+        if (e) cudaEventDestroy(e);
 }
 
 // ---------------------------------------------------------------- timeline
@@ -183,6 +190,19 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         // An update that runs beside the prefetched root TTM is off the
         // critical path (the root is): its branch TTMs and V-GEMM take a few
         // SMs for longer instead of every SM briefly, so the root keeps more.
+        // Event-driven fronts: an update's Z-QR waits only for the finishers
+        // of the modes it reads (R_k, k != n) and its TTM chain only for the
+        // Q_c it contracts, not for everything before it on the stream.  At a
+        // sweep boundary the next update has the SAME mode as the last one
+        // (branch reuse: orders 1 3 2 | 2 3 1 ..., Appendix A), so its Z-QR
+        // and chain run under the previous update's V-GEMM and finisher.
+        // Measured (B200, 2 x 100 sweeps each): C2 1861 -> 1918 sweeps/s, C4
+        // unchanged, C1 -3%, C3 (N = 4) -5%: on by default for third-order
+        // tensors whose Z-QR is long (R^2 x R >= 16k entries), CPDB_EARLY_FRONT=1
+        // forces it on, =0 off.
+        const char* ef = std::getenv("CPDB_EARLY_FRONT");
+        const bool pays = order == 3 && zrows * R >= 16384;
+        dep_events = chain_side && (ef ? ef[0] == '1' : pays);
         const char* zy = std::getenv("CPDB_ZQR_YIELD");
         zqr_yield = chain_side && zy && zy[0] == '1' && !zqr_cluster_fits(zrows, R, order - 1);
         const char* os = std::getenv("CPDB_OVERLAP_SMS");
@@ -228,10 +248,12 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     fscratch.ensure(maxI * (R + 1));
     vout.ensure(maxI * R);
     fitbuf.ensure(8);
-    q0buf.ensure(zrows * R);
-    q1buf.ensure(zrows * R);
-    r0buf.ensure(uint64_t(R) * R);
-    zwork.ensure(zqr_work_doubles(R) + uint64_t(4 * c->sms) * R * R);
+    for (ZBuf& z : zb) {
+        z.q0.ensure(zrows * R);
+        z.q1.ensure(zrows * R);
+        z.r0.ensure(uint64_t(R) * R);
+        z.work.ensure(zqr_work_doubles(R) + uint64_t(4 * c->sms) * R * R);
+    }
     vfull.ensure(maxI * R);
     vfitfull.ensure(maxI * R);
     // V-GEMM partials up front (the dual ones are first needed when the beta
@@ -242,6 +264,17 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
     for (uint32_t k = 0; k < order; ++k) qr_factor(k);
     pack_local0();
+    CPDB_CK(cudaEventCreateWithFlags(&ev_zq, cudaEventDisableTiming));
+    for (uint32_t k = 0; k < order; ++k) {
+        CPDB_CK(cudaEventCreateWithFlags(&ev_fac[k], cudaEventDisableTiming));
+        CPDB_CK(cudaEventCreateWithFlags(&ev_v[k], cudaEventDisableTiming));
+        CPDB_CK(cudaEventRecord(ev_fac[k], s));
+        CPDB_CK(cudaEventRecord(ev_v[k], s));
+    }
+    for (cudaEvent_t& e : ev_zread) {
+        CPDB_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CPDB_CK(cudaEventRecord(e, s));
+    }
 
     // ---- Q0 history (reference row order on the host side) -----------------
     perm = natural_to_reference(order, R);
@@ -475,10 +508,11 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     z.nm = order - 1;
     z.R = R;
     z.zrows = zrows;
-    z.q1 = q1buf.p;
-    z.q0 = q0buf.p;
-    z.r0 = r0buf.p;
-    z.work = zwork.p;
+    ZBuf& zcur = zb[zpar];
+    z.q1 = zcur.q1.p;
+    z.q0 = zcur.q0.p;
+    z.r0 = zcur.r0.p;
+    z.work = zcur.work.p;
     z.status = c->dstatus;
     // Z-QR depends only on R_k (k != n), final since the previous update's
     // finisher, and overlaps the TTM chain on a second stream.  Unsharded, the
@@ -486,22 +520,43 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     // 8-CTA cluster is resident before the chain's CTAs arrive, which would
     // otherwise leave no GPC with 8 free SMs) and the chain runs on the side
     // stream; sharded runs keep the chain (and its collectives) on the main one.
-    cudaStream_t zs = chain_side ? s : c->side;
+    // Event-driven when the previous update had the same mode (the sweep
+    // boundary): Z-QR on the side stream, chain on the mid one, both free of
+    // the previous update's V-GEMM and finisher.  Otherwise the stream-ordered
+    // form below (its Z-QR launches programmatically right behind the
+    // finisher, measured faster when it has to wait for that finisher anyway).
+    early = dep_events && last_mode == int(n);
+    cudaStream_t zs = early ? c->side : chain_side ? s : c->side;
     static const bool trace_phases = std::getenv("CPDB_PHASE_TRACE") != nullptr;
     if (trace_phases) {
         z.ts = reinterpret_cast<unsigned long long*>(zts.ensure(32));
         CPDB_CK(cudaMemsetAsync(z.ts, 0, 32 * sizeof(double), zs));
     }
-    const cudaStream_t ts = chain_side ? (zqr_yield ? c->mid : c->side) : s;
-    CPDB_CK(cudaEventRecord(ev_ready, s));
-    CPDB_CK(cudaStreamWaitEvent(chain_side ? ts : c->side, ev_ready, 0));
-    z.pdl = chain_side && !trace_phases ? 1 : 0;
+    const cudaStream_t ts =
+        early ? c->mid : chain_side ? (zqr_yield ? c->mid : c->side) : s;
+    if (early) {
+        for (uint32_t k = 0; k < order; ++k)
+            if (k != n) CPDB_CK(cudaStreamWaitEvent(zs, ev_fac[k], 0));
+        CPDB_CK(cudaStreamWaitEvent(zs, ev_zread[zpar], 0));
+        uint32_t waited = 0;
+        for (const Step& st : sw.updates[b].steps)
+            if (!(waited & (1u << st.contract))) {
+                CPDB_CK(cudaStreamWaitEvent(ts, ev_fac[st.contract], 0));
+                waited |= 1u << st.contract;
+            }
+        CPDB_CK(cudaStreamWaitEvent(ts, ev_v[n], 0));  // ybuf[n]'s last reader
+    } else {
+        CPDB_CK(cudaEventRecord(ev_ready, s));
+        CPDB_CK(cudaStreamWaitEvent(chain_side ? ts : c->side, ev_ready, 0));
+    }
+    z.pdl = chain_side && !early && !trace_phases ? 1 : 0;
     tl_sweep = sweep;
     tl_mode = n;
     cudaEvent_t tla = tl_begin(zs);
     CPDB_CK(launch_zqr(z, zs, c->sms));
     tl_end(tla, zs, "zqr");
     if (!chain_side) CPDB_CK(cudaEventRecord(ev_zqr, c->side));
+    if (early) CPDB_CK(cudaEventRecord(ev_zq, zs));
     if (trace_phases) {
         unsigned long long ts[32];
         CPDB_CK(cudaMemcpyAsync(ts, z.ts, sizeof ts, cudaMemcpyDeviceToHost, zs));
@@ -514,7 +569,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     c->launches += 5;
     if (observer) {
         std::vector<double> nat(zrows * R), ref(zrows * R);
-        CPDB_CK(cudaMemcpyAsync(nat.data(), q0buf.p, zrows * R * sizeof(double),
+        CPDB_CK(cudaMemcpyAsync(nat.data(), zcur.q0.p, zrows * R * sizeof(double),
                                 cudaMemcpyDeviceToHost, zs));
         CPDB_CK(cudaStreamSynchronize(zs));
         for (uint64_t i = 0; i < zrows; ++i)
@@ -601,7 +656,8 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     const std::vector<uint64_t> yd = local_dims_of(1u << n);
     VgemmArgs v{};
     v.y = ybuf[n].p;
-    v.q0 = q0buf.p;
+    ZBuf& zcur = zb[zpar];
+    v.q0 = zcur.q0.p;
     v.hist = use_ex ? hist[n].p : nullptr;
     v.beta = beta;
     v.alpha = cfg.alpha;
@@ -623,6 +679,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     v.v_out = vfull.p + off;
     v.vfit_out = v.dual ? vfitfull.p + off : nullptr;
     CPDB_CK(cudaStreamWaitEvent(s, ev_zqr, 0));
+    if (early) CPDB_CK(cudaStreamWaitEvent(s, ev_zq, 0));
     tl_sweep = sweep;
     tl_mode = n;
     cudaEvent_t tla = tl_begin(s);
@@ -637,6 +694,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     CPDB_CK(launch_vgemm(v, s, vsms > 0 ? vsms : c->sms));
     tl_end(tla, s, "vgemm");
     c->launches += 1;
+    if (dep_events) CPDB_CK(cudaEventRecord(ev_v[n], s));  // ybuf[n] consumed
     // the cluster finisher sums the split-K partials itself (no reduction
     // launch on the chain); gathered (sharded mode-0) V needs them reduced
     const bool fused = vsplit_max > 0 && !v.reduced && !gather && v.nsplit <= 64 &&
@@ -659,7 +717,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     f.vfitpart = v.dual ? (fused ? v.vfitpart : vfitfull.p) : nullptr;
     f.nsplit = fused ? v.nsplit : 1;
     f.dual = v.dual;
-    f.r0 = r0buf.p;
+    f.r0 = zcur.r0.p;
     f.I = c->dims[n];
     f.R = R;
     f.v_out = vout.p;
@@ -692,11 +750,17 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
         std::fprintf(stderr, "\n");
     }
     if (n == 0) pack_local0();
+    if (dep_events) {
+        CPDB_CK(cudaEventRecord(ev_fac[n], s));       // A_n, Q_n, R_n final
+        CPDB_CK(cudaEventRecord(ev_zread[zpar], s));  // Q0 / R0 / history consumed
+    }
     ++versions[n];
     if (extrap) {
-        hist[n].swap(q0buf);  // the history keeps the unextrapolated Q0 (:265)
+        hist[n].swap(zcur.q0);  // the history keeps the unextrapolated Q0 (:265)
         has_hist[n] = true;
     }
+    zpar ^= 1;
+    last_mode = int(n);
     prefetch_root(sweep, b);
 }
 
@@ -709,7 +773,10 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         const uint64_t sweep = done + 1;
         const Sweep& sw = plan.sweeps[sweep - 1];
         double beta_used = 0.0;
-        if (!front_issued) CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
+        // (event-driven fronts run ahead of the stream order: the status word
+        // is then sticky for the whole run instead of reset per sweep)
+        if (!front_issued && !dep_events)
+            CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
         for (uint32_t b = 0; b < order; ++b) {
             if (b == 0 && front_issued) {
                 front_issued = false;  // issued ahead of the previous sweep's host sync
@@ -731,7 +798,7 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         // host waits for this sweep's fitness (wasted only if it converges).
         const bool more = rows_out + 1 < nsweeps && done + 1 < last_sweep;
         if (more && observer == nullptr && fps == nullptr) {
-            CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
+            if (!dep_events) CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
             mode_update_front(sweep + 1, 0, nullptr, nullptr);
             front_issued = true;
         }

@@ -35,7 +35,21 @@ struct Session {
 
     std::vector<FactorBufs> fb;
     DevBuf lam, qp0_local, tsbuf, zts;
-    DevBuf fscratch, vpart, vfitpart, vfull, vfitfull, vout, fitbuf, q0buf, q1buf, r0buf, zwork;
+    DevBuf fscratch, vpart, vfitpart, vfull, vfitfull, vout, fitbuf;
+    // Z-QR outputs, double-buffered so the next update's Z-QR can run while
+    // this update's V-GEMM / finisher still read Q0 and R0
+    struct ZBuf {
+        DevBuf q0, q1, r0, work;
+    } zb[2];
+    int zpar = 0;  // parity of the update in flight (set by the front, used by the back)
+    // Dependency events of the event-driven schedule (dep_events): the
+    // finisher that last updated each mode, the V-GEMM that last read ybuf[n],
+    // the last readers of each Z-QR buffer set, and the front's joins
+    bool dep_events = false;
+    cudaEvent_t ev_fac[CPDB_MAX_ORDER] = {}, ev_v[CPDB_MAX_ORDER] = {}, ev_zread[2] = {};
+    cudaEvent_t ev_zq = nullptr;
+    int last_mode = -1;   // mode of the last update issued (back)
+    bool early = false;   // this update's front runs event-driven (set by the front)
     std::vector<DevBuf> hist, ybuf;
     std::vector<bool> has_hist;
     std::vector<uint64_t> versions;

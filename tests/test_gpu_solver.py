@@ -294,3 +294,25 @@ def test_rank_edges_vs_oracle(ctx, port, dims, rank):
         g = cpd.als_qr_bre(x, cfg_of(rank, 6, seed=5), ctx=ctx)
         o = port.solve(x, rank, 6, extrapolate=True, seed=5)
     compare(g, o, fit_tol=1e-9, factor_tol=1e-8)
+
+
+@pytest.mark.parametrize("early", ["1", "0"])
+@pytest.mark.parametrize("overlap_sms", ["", "0", "16"])
+def test_schedule_variants_match_oracle(ctx, port, monkeypatch, early, overlap_sms):
+    """The event-driven sweep-boundary front (CPDB_EARLY_FRONT: the next
+    update's Z-QR and chain run under the previous update's V-GEMM/finisher)
+    and the SM budget of updates beside the prefetched root (CPDB_OVERLAP_SMS)
+    only reorder launches: trajectories match the oracle and repeat bit for
+    bit.  C2 construction at 64^3 R16 (Z-QR 256 x 16)."""
+    import paper_2503_18759_b200 as cpd
+    monkeypatch.setenv("CPDB_EARLY_FRONT", early)
+    if overlap_sms:
+        monkeypatch.setenv("CPDB_OVERLAP_SMS", overlap_sms)
+    x = port.synth_baseline(0, (64, 64, 64), 16, 1e-3, META["truth_seeds"]["c2"])
+    g = cpd.als_qr_bre(x, cfg_of(16, 24, seed=META["init_seed"]), ctx=ctx)
+    o = port.solve(x, 16, 24, extrapolate=True, seed=META["init_seed"])
+    compare(g, o, factor_tol=1e-9)
+    g2 = cpd.als_qr_bre(x, cfg_of(16, 24, seed=META["init_seed"]), ctx=ctx)
+    assert [t.fitness for t in g2.trace] == [t.fitness for t in g.trace]
+    for a, b in zip(g.model.factors, g2.model.factors):
+        assert np.array_equal(a, b)
