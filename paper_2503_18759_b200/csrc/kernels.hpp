@@ -73,7 +73,16 @@ struct VgemmArgs {
     uint32_t nsplit;     // out: split count used
     int reduced;         // out: 1 = V written to v_out (no reduce_splits needed)
     uint32_t max_split;  // in: cap on the split count (0: vgemm_max_split())
+    // device copy of the beta state (beta_gate); when set and extrap != 0 the
+    // kernel extrapolates iff gate[0] != 0 && gate[1] != 0, with beta = gate[1]
+    const double* gate;
 };
+// The beta state machine of run_qr (solvers.hpp:297-301) on the device, so the
+// next sweep's first V-GEMM needs no host round trip.  gate = {has_beta, beta,
+// has_prev, prev_fitness}; fit = the sweep's fitness (finisher output);
+// allow = extrapolation on, no override, sweep >= 2.  Same arithmetic as
+// cpdb_select_beta -> the host mirror takes identical decisions.
+cudaError_t beta_gate(double* gate, const double* fit, int allow, double gap, cudaStream_t s);
 cudaError_t launch_vgemm(VgemmArgs& a, cudaStream_t s, int sms);
 uint32_t vgemm_max_split();
 

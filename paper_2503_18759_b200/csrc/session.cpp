@@ -196,13 +196,14 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         // sweep boundary the next update has the SAME mode as the last one
         // (branch reuse: orders 1 3 2 | 2 3 1 ..., Appendix A), so its Z-QR
         // and chain run under the previous update's V-GEMM and finisher.
-        // Measured (B200, 2 x 100 sweeps each): C2 1861 -> 1918 sweeps/s, C4
-        // unchanged, C1 -3%, C3 (N = 4) -5%: on by default for third-order
-        // tensors whose Z-QR is long (R^2 x R >= 16k entries), CPDB_EARLY_FRONT=1
-        // forces it on, =0 off.
+        // Pays together with the speculative next-sweep update (Session::run:
+        // no host round trip at the sweep boundary left to hide the front
+        // under).  Measured (B200, 100 sweeps): C1 6040 -> 6860 sweeps/s, C2
+        // 1911 -> 2003, C3 1258 -> 1310, C4 4626 -> 5259.  CPDB_EARLY_FRONT=0: off.
         const char* ef = std::getenv("CPDB_EARLY_FRONT");
-        const bool pays = order == 3 && zrows * R >= 16384;
-        dep_events = chain_side && (ef ? ef[0] == '1' : pays);
+        dep_events = chain_side && !(ef && ef[0] == '0');
+        const char* sp = std::getenv("CPDB_SPECULATE");
+        speculate = !(sp && sp[0] == '0');
         const char* zy = std::getenv("CPDB_ZQR_YIELD");
         zqr_yield = chain_side && zy && zy[0] == '1' && !zqr_cluster_fits(zrows, R, order - 1);
         const char* os = std::getenv("CPDB_OVERLAP_SMS");
@@ -219,7 +220,16 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         fb[k].qp.ensure(uint64_t(ttm_kpad(I)) * Rp);
         fb[k].r.ensure(uint64_t(R) * R);
     }
+    fb_alt.resize(order);
+    for (uint32_t k = 0; k < order; ++k) {
+        const uint64_t I = c->dims[k];
+        fb_alt[k].a.ensure(I * R);
+        fb_alt[k].q.ensure(I * R);
+        fb_alt[k].qp.ensure(uint64_t(ttm_kpad(I)) * Rp);
+        fb_alt[k].r.ensure(uint64_t(R) * R);
+    }
     lam.ensure(R);
+    lam_alt.ensure(R);
     {
         std::vector<double> init(nfac);
         const bool given = state && state->factors;
@@ -304,6 +314,13 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     }
     has_prev = state && state->has_prev_fitness;
     prev_fit = has_prev ? state->prev_fitness : 0.0;
+    {
+        const double g[4] = {has_beta ? 1.0 : 0.0, has_beta ? beta : 0.0, has_prev ? 1.0 : 0.0,
+                             prev_fit};
+        gate.ensure(4);
+        CPDB_CK(cudaMemcpyAsync(gate.p, g, sizeof g, cudaMemcpyHostToDevice, s));
+        CPDB_CK(cudaStreamSynchronize(s));
+    }
 
     // cost accounting continues from the sweeps already done (dim_tree.hpp:523-526)
     total = done > 0 ? measured_cost(plan, c->dims, R, done) : Cost{};
@@ -648,8 +665,13 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     const Sweep& sw = plan.sweeps[sweep - 1];
     const uint32_t n = sw.updates[b].mode;
     const bool last = (b == order - 1);
-    // 3. extrapolation gate (solvers.hpp:260-265)
-    const bool use_ex = extrap && has_beta && beta != 0.0 && has_hist[n];
+    // 3. extrapolation gate (solvers.hpp:260-265).  The V-GEMM takes the beta
+    // decision from the device copy of the state (gate), which is already
+    // current when this update was issued before the host read the previous
+    // sweep's fitness (speculation, Session::run); the host mirror below is
+    // current otherwise and only feeds the trace.
+    const bool maybe_ex = extrap && has_hist[n];
+    const bool use_ex = maybe_ex && has_beta && beta != 0.0;
     if (use_ex) beta_used = beta;
 
     // 5. V = Y_(n) Q0_hat (+ the unextrapolated V for the fitness, :277-284)
@@ -658,11 +680,13 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     v.y = ybuf[n].p;
     ZBuf& zcur = zb[zpar];
     v.q0 = zcur.q0.p;
-    v.hist = use_ex ? hist[n].p : nullptr;
+    v.hist = maybe_ex ? hist[n].p : nullptr;
     v.beta = beta;
     v.alpha = cfg.alpha;
-    v.extrap = use_ex ? 1 : 0;
-    v.dual = (last && use_ex) ? 1 : 0;
+    v.extrap = maybe_ex ? 1 : 0;
+    v.gate = maybe_ex ? gate.p : nullptr;
+    // (dual with the gate closed: V and Vfit come out bit-identical)
+    v.dual = (last && maybe_ex) ? 1 : 0;
     v.I = yd[n];
     v.O = 1;
     for (uint32_t k = 0; k < n; ++k) v.O *= R;
@@ -721,11 +745,11 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     f.I = c->dims[n];
     f.R = R;
     f.v_out = vout.p;
-    f.a_out = fb[n].a.p;
-    f.q_out = fb[n].q.p;
-    f.qp_out = fb[n].qp.p;
-    f.r_out = fb[n].r.p;
-    f.lambda = lam.p;
+    f.a_out = fb_alt[n].a.p;
+    f.q_out = fb_alt[n].q.p;
+    f.qp_out = fb_alt[n].qp.p;
+    f.r_out = fb_alt[n].r.p;
+    f.lambda = lam_alt.p;
     f.scratch = fscratch.p;
     f.fitness = last ? 1 : 0;
     f.norm_x_sq = nx2;
@@ -740,6 +764,8 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     CPDB_CK(launch_finish(f, s));
     tl_end(tla, s, "finish");
     c->launches += 1;
+    fb[n].swap(fb_alt[n]);  // the new factor state (the old one stays for undo)
+    lam.swap(lam_alt);
     if (trace_phases) {
         unsigned long long ts[32];
         CPDB_CK(cudaMemcpyAsync(ts, f.ts, sizeof ts, cudaMemcpyDeviceToHost, s));
@@ -783,8 +809,19 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
             } else {
                 mode_update_front(sweep, b, observer, user);
             }
-            mode_update_back(sweep, b, beta_used);
+            if (b == 0 && spec.issued) {
+                spec.issued = false;  // issued (whole) ahead of the previous sweep's host sync
+                beta_used = spec.beta_used;
+            } else {
+                mode_update_back(sweep, b, beta_used);
+            }
         }
+        // the beta state machine of this sweep on the device (solvers.hpp:297-301),
+        // read by the next sweep's V-GEMMs (the host mirrors it below)
+        if (extrap)
+            CPDB_CK(beta_gate(gate.p, fitbuf.p,
+                              (!cfg.has_beta_override && sweep >= 2) ? 1 : 0,
+                              cfg.activation_gap, s));
         cudaEvent_t e_end = events.get();
         CPDB_CK(cudaEventRecord(e_end, s));
         CPDB_CK(cudaMemcpyAsync(c->pinned, fitbuf.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
@@ -801,6 +838,20 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
             if (!dep_events) CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
             mode_update_front(sweep + 1, 0, nullptr, nullptr);
             front_issued = true;
+            // ... and, with the beta decision taken on the device, its V-GEMM
+            // and finisher too: the GPU goes straight on while the host reads
+            // this sweep's fitness.  If the stop test fires on it, the update
+            // is undone (factor buffers swapped back, undo_speculative_update).
+            if (speculate && lps == nullptr) {
+                const uint32_t n1 = plan.sweeps[sweep].updates[0].mode;
+                spec.mode = n1;
+                spec.had_hist = has_hist[n1];
+                spec.prev_last_mode = last_mode;
+                double unused = 0.0;
+                mode_update_back(sweep + 1, 0, unused);
+                spec.issued = true;
+                spec.beta_used = 0.0;
+            }
         }
         CPDB_CK(cudaEventSynchronize(e_fit));
         int status;
@@ -873,6 +924,13 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         prev_fit = fit;
         has_prev = true;
         if (fit >= cfg.fitness_threshold) converged = true;  // :301
+        if (spec.issued) {
+            if (converged) {
+                undo_speculative_update();
+            } else if (extrap && spec.had_hist && has_beta && beta != 0.0) {
+                spec.beta_used = beta;  // what the device gate decided for it
+            }
+        }
     }
     tl_flush();
     c->prof.sweeps = done - first_sweep;
@@ -880,6 +938,21 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         c->prof.solve_ms - c->prof.root_ttm_ms - c->prof.branch_ttm_ms - c->prof.comm_ms;
     c->prof.kernel_launches = c->launches - launches0;
     return rows_out;
+}
+
+// The stop test fired on the sweep before a speculatively issued update:
+// restore the state the reference returns (factors, lambda, Q0 history).
+void Session::undo_speculative_update() {
+    CPDB_CK(cudaStreamSynchronize(s));
+    const uint32_t n = spec.mode;
+    fb[n].swap(fb_alt[n]);
+    lam.swap(lam_alt);
+    zpar ^= 1;
+    if (extrap) hist[n].swap(zb[zpar].q0);
+    has_hist[n] = spec.had_hist;
+    --versions[n];
+    last_mode = spec.prev_last_mode;
+    spec.issued = false;
 }
 
 // ---------------------------------------------------------------- results

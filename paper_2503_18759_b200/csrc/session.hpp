@@ -19,6 +19,12 @@ struct EventPool {
 
 struct FactorBufs {
     DevBuf a, q, qp, r;  // A_n, Q_n, packed Q_n, R_n
+    void swap(FactorBufs& o) noexcept {
+        a.swap(o.a);
+        q.swap(o.q);
+        qp.swap(o.qp);
+        r.swap(o.r);
+    }
 };
 
 struct Session {
@@ -34,7 +40,23 @@ struct Session {
     uint64_t launches0 = 0;
 
     std::vector<FactorBufs> fb;
-    DevBuf lam, qp0_local, tsbuf, zts;
+    // A mode update writes the OTHER copy of its factor buffers and of lambda
+    // and swaps them in after the launch, so a speculatively issued update
+    // (the next sweep's first, before the host has read this sweep's fitness)
+    // can be undone by swapping back when the stop test fires.
+    std::vector<FactorBufs> fb_alt;
+    DevBuf lam, lam_alt, qp0_local, tsbuf, zts;
+    DevBuf gate;  // {has_beta, beta, has_prev, prev_fitness} on the device (beta_gate)
+    // the next sweep's first update issued before the host read this sweep's
+    // fitness (Session::run); what undoing it needs
+    struct Spec {
+        bool issued = false;
+        uint32_t mode = 0;
+        bool had_hist = false;  // has_hist[mode] before it (extrapolation possible)
+        int prev_last_mode = -1;
+        double beta_used = 0.0;  // its trace contribution, once the host knows the gate
+    } spec;
+    bool speculate = false;  // CPDB_SPECULATE=0 turns it off
     DevBuf fscratch, vpart, vfitpart, vfull, vfitfull, vout, fitbuf;
     // Z-QR outputs, double-buffered so the next update's Z-QR can run while
     // this update's V-GEMM / finisher still read Q0 and R0
@@ -128,6 +150,7 @@ private:
                      double& beta_used);
     void mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer observer, void* user);
     void mode_update_back(uint64_t sweep, uint32_t b, double& beta_used);
+    void undo_speculative_update();
 };
 
 }  // namespace cpdb

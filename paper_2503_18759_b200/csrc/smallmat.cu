@@ -59,6 +59,16 @@ constexpr int kVThreads = 256;
 constexpr int kVBI = 64;  // rows of V per block
 constexpr int kVBK = 16;  // k per smem tile
 
+// extrapolation decision of a V-GEMM launch: the host's, or the device
+// gate's when the launch carries one (uniform over the grid)
+__device__ __forceinline__ bool extrap_on(const VgemmArgs& a) {
+    if (!a.extrap) return false;
+    return a.gate ? (a.gate[0] != 0.0 && a.gate[1] != 0.0) : true;
+}
+__device__ __forceinline__ double extrap_beta(const VgemmArgs& a) {
+    return a.gate ? a.gate[1] : a.beta;
+}
+
 template <int RM, bool DUAL>
 __global__ void __launch_bounds__(kVThreads)
 vgemm_kernel(VgemmArgs a, uint64_t kchunk) {
@@ -79,6 +89,8 @@ vgemm_kernel(VgemmArgs a, uint64_t kchunk) {
 #pragma unroll
     for (int u = 0; u < (DUAL ? RPT : 1); ++u) accf[u] = 0.0;
     const bool jfast = J >= kVBK;
+    const bool ex = extrap_on(a);
+    const double beta = extrap_beta(a);
     for (uint64_t k0 = kb; k0 < ke; k0 += kVBK) {
         for (int e = threadIdx.x; e < kVBI * kVBK; e += kVThreads) {
             int r_, c_;
@@ -107,7 +119,7 @@ vgemm_kernel(VgemmArgs a, uint64_t kchunk) {
             if (k < ke && r < R) {
                 q = a.q0[k * R + r];
                 p = q;
-                if (a.extrap) p = q + a.beta * (q - a.alpha * a.hist[k * R + r]);
+                if (ex) p = q + beta * (q - a.alpha * a.hist[k * R + r]);
             }
             pt[kk][r] = p;
             if (DUAL) ft[kk][r] = q;
@@ -180,6 +192,8 @@ __device__ __forceinline__ void vgemm_tile(const VgemmArgs& a, uint64_t i0, uint
     const uint32_t J = uint32_t(a.J);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const bool jrun = (J % kDK) == 0;  // a 16-k tile is 16 consecutive j of one o
+    const bool ex = extrap_on(a);
+    const double beta = extrap_beta(a);
 
     // two register sets: tiles t+1 and t+2 are in flight during tile t's MMAs
     struct Regs {
@@ -207,7 +221,7 @@ __device__ __forceinline__ void vgemm_tile(const VgemmArgs& a, uint64_t i0, uint
             double q = 0.0, p = 0.0;
             if (e < kDK * RM && k < ke && r < R) {
                 q = a.q0[uint64_t(k) * R + r];
-                p = a.extrap ? q + a.beta * (q - a.alpha * a.hist[uint64_t(k) * R + r]) : q;
+                p = ex ? q + beta * (q - a.alpha * a.hist[uint64_t(k) * R + r]) : q;
             }
             rg.p[u] = p;
             if (DUAL) rg.f[u] = q;
@@ -574,7 +588,30 @@ cudaError_t sum_slots(const double* slots, uint64_t stride, uint32_t world, uint
     return cudaGetLastError();
 }
 
-uint32_t vgemm_max_split() { return 296; }  // 2 CTAs per SM on 148 SMs
+uint32_t vgemm_max_split() { return 296; }
+
+namespace {
+__global__ void beta_gate_kernel(double* gate, const double* fit, int allow, double gap) {
+    pdl_entry();
+    const double now = fit[0];
+    if (allow && gate[0] == 0.0 && gate[2] != 0.0) {
+        // cpdb_select_beta (solvers.hpp:92-101)
+        const double prev = gate[3];
+        const double p = prev < 0.0 ? 0.0 : (prev > 1.0 ? 1.0 : prev);
+        const double q = now < 0.0 ? 0.0 : (now > 1.0 ? 1.0 : now);
+        if (!(fabs(q - p) >= gap)) {
+            gate[0] = 1.0;
+            gate[1] = q > 0.90 ? 1.0 / 2000.0 : (q >= 0.70 ? 1.0 / 500.0 : 1.0 / 250.0);
+        }
+    }
+    gate[3] = now;
+    gate[2] = 1.0;
+}
+}  // namespace
+
+cudaError_t beta_gate(double* gate, const double* fit, int allow, double gap, cudaStream_t s) {
+    return launch_pdl(beta_gate_kernel, dim3(1), dim3(1), 0, s, gate, fit, allow, gap);
+}  // 2 CTAs per SM on 148 SMs
 
 cudaError_t launch_vgemm(VgemmArgs& a, cudaStream_t s, int sms) {
     const bool d = a.dual != 0;

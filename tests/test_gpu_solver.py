@@ -316,3 +316,21 @@ def test_schedule_variants_match_oracle(ctx, port, monkeypatch, early, overlap_s
     assert [t.fitness for t in g2.trace] == [t.fitness for t in g.trace]
     for a, b in zip(g.model.factors, g2.model.factors):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.parametrize("speculate", ["1", "0"])
+@pytest.mark.parametrize("dims", [(40, 36, 32), (20, 18, 16, 14)])
+def test_stop_test_undoes_speculative_update(ctx, port, monkeypatch, speculate, dims):
+    """The next sweep's first update is issued before the host reads the
+    fitness (beta decided on the device).  When the stop test fires, that
+    update is undone: trace, factors and lambda equal the oracle's, which
+    never ran it (solvers.hpp:301)."""
+    import paper_2503_18759_b200 as cpd
+    monkeypatch.setenv("CPDB_SPECULATE", speculate)
+    x = port.synth_baseline(0, dims, 3, 1e-2, 20250011)
+    # threshold = the oracle's own fitness at sweep 10: the run stops mid-way
+    thr = port.solve(x, 3, 10, extrapolate=True, seed=5).trace[-1]["fitness"]
+    o = port.solve(x, 3, 40, extrapolate=True, seed=5, fitness_threshold=thr)
+    assert 2 < len(o.trace) <= 10
+    g = cpd.als_qr_bre(x, cfg_of(3, 40, seed=5, fitness_threshold=thr), ctx=ctx)
+    compare(g, o, factor_tol=1e-9)
