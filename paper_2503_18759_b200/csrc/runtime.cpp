@@ -300,6 +300,7 @@ cpdb_ctx::~cpdb_ctx() {
     if (stream) cudaStreamSynchronize(stream);
     if (lo) cudaStreamSynchronize(lo);
     if (mid) cudaStreamSynchronize(mid);
+    if (aux) cudaStreamSynchronize(aux);
     if (comm) {
         const cpdb::Nccl& N = cpdb::nccl();
         if (N.ok) N.CommDestroy(static_cast<ncclComm_t>(comm));
@@ -310,4 +311,5 @@ cpdb_ctx::~cpdb_ctx() {
     if (side) cudaStreamDestroy(side);
     if (lo) cudaStreamDestroy(lo);
     if (mid) cudaStreamDestroy(mid);
+    if (aux) cudaStreamDestroy(aux);
 }

@@ -75,12 +75,14 @@ Session::~Session() {
     if (c && c->side) cudaStreamSynchronize(c->side);
     if (c && c->lo) cudaStreamSynchronize(c->lo);
     if (c && c->mid) cudaStreamSynchronize(c->mid);
+    if (c && c->aux) cudaStreamSynchronize(c->aux);
     if (ev_fin) cudaEventDestroy(ev_fin);
     if (pf.ev) cudaEventDestroy(pf.ev);
     if (t_start) cudaEventDestroy(t_start);
     if (ev_ready) cudaEventDestroy(ev_ready);
     if (ev_zqr) cudaEventDestroy(ev_zqr);
     if (ev_zq) cudaEventDestroy(ev_zq);
+    if (ev_aux) cudaEventDestroy(ev_aux);
     for (cudaEvent_t e : ev_fac)
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_v)
@@ -103,7 +105,7 @@ void Session::tl_end(cudaEvent_t a, cudaStream_t st, const char* label) {
     cudaEvent_t b;
     CPDB_CK(cudaEventCreate(&b));
     CPDB_CK(cudaEventRecord(b, st));
-    const int sid = st == c->side ? 1 : st == c->lo ? 2 : st == c->mid ? 3 : 0;
+    const int sid = st == c->side ? 1 : st == c->lo ? 2 : st == c->mid ? 3 : st == c->aux ? 4 : 0;
     marks.push_back(Mark{label, sid, tl_sweep, tl_mode, a, b});
 }
 
@@ -255,7 +257,7 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         CPDB_CK(cudaMemcpyAsync(lam.p, l.data(), R * sizeof(double), cudaMemcpyHostToDevice, s));
         CPDB_CK(cudaStreamSynchronize(s));
     }
-    fscratch.ensure(maxI * (R + 1));
+    for (DevBuf& b : fscratch) b.ensure(maxI * (R + 1));
     vout.ensure(maxI * R);
     fitbuf.ensure(8);
     for (ZBuf& z : zb) {
@@ -264,17 +266,19 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         z.r0.ensure(uint64_t(R) * R);
         z.work.ensure(zqr_work_doubles(R) + uint64_t(4 * c->sms) * R * R);
     }
-    vfull.ensure(maxI * R);
-    vfitfull.ensure(maxI * R);
+    for (DevBuf& b : vfull) b.ensure(maxI * R);
+    for (DevBuf& b : vfitfull) b.ensure(maxI * R);
     // V-GEMM partials up front (the dual ones are first needed when the beta
     // gate opens, mid-run: no allocation inside the sweeps)
-    vpart.ensure(size_t(vgemm_max_split()) * maxI * R);
-    if (extrap) vfitpart.ensure(size_t(vgemm_max_split()) * maxI * R);
+    for (DevBuf& b : vpart) b.ensure(size_t(vgemm_max_split()) * maxI * R);
+    if (extrap)
+        for (DevBuf& b : vfitpart) b.ensure(size_t(vgemm_max_split()) * maxI * R);
     versions.assign(order, 1);
     CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
     for (uint32_t k = 0; k < order; ++k) qr_factor(k);
     pack_local0();
     CPDB_CK(cudaEventCreateWithFlags(&ev_zq, cudaEventDisableTiming));
+    CPDB_CK(cudaEventCreateWithFlags(&ev_aux, cudaEventDisableTiming));
     for (uint32_t k = 0; k < order; ++k) {
         CPDB_CK(cudaEventCreateWithFlags(&ev_fac[k], cudaEventDisableTiming));
         CPDB_CK(cudaEventCreateWithFlags(&ev_v[k], cudaEventDisableTiming));
@@ -384,7 +388,7 @@ void Session::qr_factor(uint32_t k) {
     f.qp_out = fb[k].qp.p;
     f.r_out = fb[k].r.p;
     f.lambda = lam.p;
-    f.scratch = fscratch.p;
+    f.scratch = fscratch[0].p;
     f.status = c->dstatus;
     f.v_out = vout.p;
     CPDB_CK(launch_finish(f, s));
@@ -451,7 +455,7 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32
 // (b, b2) changes Q_c, the root TTM is issued on the low-priority stream into
 // a spare buffer: its CTAs (one tile each) fill the SMs the latency-bound
 // updates in between leave idle, and update b2 adopts the buffer.
-void Session::prefetch_root(uint64_t sweep, uint32_t b) {
+void Session::prefetch_root(uint64_t sweep, uint32_t b, cudaStream_t after) {
     if (!prefetch_enabled || pf.active) return;
     const Sweep& sw = plan.sweeps[sweep - 1];
     for (uint32_t b2 = b + 2; b2 < order; ++b2) {
@@ -465,7 +469,7 @@ void Session::prefetch_root(uint64_t sweep, uint32_t b) {
         std::vector<uint64_t> od = c->ldims;
         od[cm] = R;
         pre.ensure(numel(od));
-        CPDB_CK(cudaEventRecord(ev_fin, s));
+        CPDB_CK(cudaEventRecord(ev_fin, after));  // update b's finisher: Q_cm final
         CPDB_CK(cudaStreamWaitEvent(c->lo, ev_fin, 0));
         ttm_step(c->x, c->ldims, 0, cm, pre.p, true, c->lo, true, true);
         CPDB_CK(cudaEventRecord(pf.ev, c->lo));
@@ -661,7 +665,9 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
 }
 
 // Steps 3 and 5-9: extrapolation gate, V, and the mode-update tail.
-void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
+void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cudaStream_t bs,
+                               bool host_beta) {
+    if (!bs) bs = s;
     const Sweep& sw = plan.sweeps[sweep - 1];
     const uint32_t n = sw.updates[b].mode;
     const bool last = (b == order - 1);
@@ -684,7 +690,8 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     v.beta = beta;
     v.alpha = cfg.alpha;
     v.extrap = maybe_ex ? 1 : 0;
-    v.gate = maybe_ex ? gate.p : nullptr;
+    v.gate = (maybe_ex && !host_beta) ? gate.p : nullptr;
+    if (host_beta && !use_ex) v.extrap = 0;
     // (dual with the gate closed: V and Vfit come out bit-identical)
     v.dual = (last && maybe_ex) ? 1 : 0;
     v.I = yd[n];
@@ -694,19 +701,23 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     for (uint32_t k = n + 1; k < order; ++k) v.J *= R;
     v.R = R;
     const size_t part = size_t(vgemm_max_split()) * v.I * R;
-    v.vpart = vpart.ensure(part);
-    v.vfitpart = v.dual ? vfitpart.ensure(part) : nullptr;
+    // (split partials, V, scratch: one set per update parity -- consecutive
+    // updates may run concurrently, Session::run)
+    DevBuf& vf = vfull[zpar];
+    DevBuf& vff = vfitfull[zpar];
+    v.vpart = vpart[zpar].ensure(part);
+    v.vfitpart = v.dual ? vfitpart[zpar].ensure(part) : nullptr;
     // split-K partials -> V (this rank's rows; sharded mode-0 updates gather
     // the full V on every rank)
     const bool gather = (shard_flags(0, 0, 1u << n, n, sharded) & kGatherV) != 0;
     const uint64_t off = gather ? c->row_begin * R : 0;
-    v.v_out = vfull.p + off;
-    v.vfit_out = v.dual ? vfitfull.p + off : nullptr;
-    CPDB_CK(cudaStreamWaitEvent(s, ev_zqr, 0));
-    if (early) CPDB_CK(cudaStreamWaitEvent(s, ev_zq, 0));
+    v.v_out = vf.p + off;
+    v.vfit_out = v.dual ? vff.p + off : nullptr;
+    CPDB_CK(cudaStreamWaitEvent(bs, ev_zqr, 0));
+    if (early) CPDB_CK(cudaStreamWaitEvent(bs, ev_zq, 0));
     tl_sweep = sweep;
     tl_mode = n;
-    cudaEvent_t tla = tl_begin(s);
+    cudaEvent_t tla = tl_begin(bs);
     // partials summed by the finisher: few enough that its 8 CTAs read them
     // quickly (env CPDB_VSPLIT_MAX, default 16)
     static const uint32_t vsplit_max = [] {
@@ -715,30 +726,30 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     }();
     v.max_split = (vsplit_max > 0 && !gather && finish_sums_splits(v.I, R)) ? vsplit_max : 0;
     const int vsms = budget(sweep, b);
-    CPDB_CK(launch_vgemm(v, s, vsms > 0 ? vsms : c->sms));
-    tl_end(tla, s, "vgemm");
+    CPDB_CK(launch_vgemm(v, bs, vsms > 0 ? vsms : c->sms));
+    tl_end(tla, bs, "vgemm");
     c->launches += 1;
-    if (dep_events) CPDB_CK(cudaEventRecord(ev_v[n], s));  // ybuf[n] consumed
+    if (dep_events) CPDB_CK(cudaEventRecord(ev_v[n], bs));  // ybuf[n] consumed
     // the cluster finisher sums the split-K partials itself (no reduction
     // launch on the chain); gathered (sharded mode-0) V needs them reduced
     const bool fused = vsplit_max > 0 && !v.reduced && !gather && v.nsplit <= 64 &&
                        finish_sums_splits(v.I, R);
     if (!v.reduced && !fused) {
-        tla = tl_begin(s);
-        CPDB_CK(reduce_splits(v.vpart, v.nsplit, v.I * R, vfull.p + off, s));
-        if (v.dual) CPDB_CK(reduce_splits(v.vfitpart, v.nsplit, v.I * R, vfitfull.p + off, s));
-        tl_end(tla, s, "reduce");
+        tla = tl_begin(bs);
+        CPDB_CK(reduce_splits(v.vpart, v.nsplit, v.I * R, vf.p + off, bs));
+        if (v.dual) CPDB_CK(reduce_splits(v.vfitpart, v.nsplit, v.I * R, vff.p + off, bs));
+        tl_end(tla, bs, "reduce");
         c->launches += v.dual ? 2 : 1;
     }
     if (gather) {
-        allgather(c, vfull.p, v.I * R);
-        if (v.dual) allgather(c, vfitfull.p, v.I * R);
+        allgather(c, vf.p, v.I * R);
+        if (v.dual) allgather(c, vff.p, v.I * R);
     }
     // 6-9. A_hat, lambda, factor QR, fitness (solvers.hpp:272-292)
     FinishArgs f{};
     f.init = 0;
-    f.vpart = fused ? v.vpart : vfull.p;
-    f.vfitpart = v.dual ? (fused ? v.vfitpart : vfitfull.p) : nullptr;
+    f.vpart = fused ? v.vpart : vf.p;
+    f.vfitpart = v.dual ? (fused ? v.vfitpart : vff.p) : nullptr;
     f.nsplit = fused ? v.nsplit : 1;
     f.dual = v.dual;
     f.r0 = zcur.r0.p;
@@ -750,7 +761,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     f.qp_out = fb_alt[n].qp.p;
     f.r_out = fb_alt[n].r.p;
     f.lambda = lam_alt.p;
-    f.scratch = fscratch.p;
+    f.scratch = fscratch[zpar].p;
     f.fitness = last ? 1 : 0;
     f.norm_x_sq = nx2;
     f.fit_out = fitbuf.p;
@@ -758,18 +769,18 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     static const bool trace_phases = std::getenv("CPDB_PHASE_TRACE") != nullptr;
     if (trace_phases) {
         f.ts = reinterpret_cast<unsigned long long*>(tsbuf.ensure(32));
-        CPDB_CK(cudaMemsetAsync(f.ts, 0, 32 * sizeof(double), s));
+        CPDB_CK(cudaMemsetAsync(f.ts, 0, 32 * sizeof(double), bs));
     }
-    tla = tl_begin(s);
-    CPDB_CK(launch_finish(f, s));
-    tl_end(tla, s, "finish");
+    tla = tl_begin(bs);
+    CPDB_CK(launch_finish(f, bs));
+    tl_end(tla, bs, "finish");
     c->launches += 1;
     fb[n].swap(fb_alt[n]);  // the new factor state (the old one stays for undo)
     lam.swap(lam_alt);
     if (trace_phases) {
         unsigned long long ts[32];
-        CPDB_CK(cudaMemcpyAsync(ts, f.ts, sizeof ts, cudaMemcpyDeviceToHost, s));
-        CPDB_CK(cudaStreamSynchronize(s));
+        CPDB_CK(cudaMemcpyAsync(ts, f.ts, sizeof ts, cudaMemcpyDeviceToHost, bs));
+        CPDB_CK(cudaStreamSynchronize(bs));
         std::fprintf(stderr, "finish mode %u phases(us):", n);
         for (int k = 1; k < 21; ++k)
             std::fprintf(stderr, " %d:%.2f", k, ts[k] ? (ts[k] - ts[0]) * 1e-3 : -1.0);
@@ -777,8 +788,8 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     }
     if (n == 0) pack_local0();
     if (dep_events) {
-        CPDB_CK(cudaEventRecord(ev_fac[n], s));       // A_n, Q_n, R_n final
-        CPDB_CK(cudaEventRecord(ev_zread[zpar], s));  // Q0 / R0 / history consumed
+        CPDB_CK(cudaEventRecord(ev_fac[n], bs));       // A_n, Q_n, R_n final
+        CPDB_CK(cudaEventRecord(ev_zread[zpar], bs));  // Q0 / R0 / history consumed
     }
     ++versions[n];
     if (extrap) {
@@ -787,7 +798,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used) {
     }
     zpar ^= 1;
     last_mode = int(n);
-    prefetch_root(sweep, b);
+    prefetch_root(sweep, b, bs);
 }
 
 // ---------------------------------------------------------------- sweeps
@@ -848,7 +859,18 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
                 spec.had_hist = has_hist[n1];
                 spec.prev_last_mode = last_mode;
                 double unused = 0.0;
-                mode_update_back(sweep + 1, 0, unused);
+                if (dep_events && (!extrap || has_beta)) {
+                    // beta frozen (or no extrapolation): the update needs
+                    // nothing from this sweep's last V-GEMM / finisher, so
+                    // it runs beside them on its own stream (its front waited
+                    // for the V-GEMM that read ybuf[n]; factor and lambda
+                    // buffers are the other copies, partials the other parity)
+                    mode_update_back(sweep + 1, 0, unused, c->aux, true);
+                    CPDB_CK(cudaEventRecord(ev_aux, c->aux));
+                    CPDB_CK(cudaStreamWaitEvent(s, ev_aux, 0));
+                } else {
+                    mode_update_back(sweep + 1, 0, unused);
+                }
                 spec.issued = true;
                 spec.beta_used = 0.0;
             }

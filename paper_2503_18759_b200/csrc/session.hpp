@@ -57,7 +57,7 @@ struct Session {
         double beta_used = 0.0;  // its trace contribution, once the host knows the gate
     } spec;
     bool speculate = false;  // CPDB_SPECULATE=0 turns it off
-    DevBuf fscratch, vpart, vfitpart, vfull, vfitfull, vout, fitbuf;
+    DevBuf fscratch[2], vpart[2], vfitpart[2], vfull[2], vfitfull[2], vout, fitbuf;
     // Z-QR outputs, double-buffered so the next update's Z-QR can run while
     // this update's V-GEMM / finisher still read Q0 and R0
     struct ZBuf {
@@ -69,7 +69,7 @@ struct Session {
     // the last readers of each Z-QR buffer set, and the front's joins
     bool dep_events = false;
     cudaEvent_t ev_fac[CPDB_MAX_ORDER] = {}, ev_v[CPDB_MAX_ORDER] = {}, ev_zread[2] = {};
-    cudaEvent_t ev_zq = nullptr;
+    cudaEvent_t ev_zq = nullptr, ev_aux = nullptr;
     int last_mode = -1;   // mode of the last update issued (back)
     bool early = false;   // this update's front runs event-driven (set by the front)
     std::vector<DevBuf> hist, ybuf;
@@ -145,11 +145,14 @@ private:
     void ttm_step(const double* src, const std::vector<uint64_t>& sd, int32_t flags,
                   uint32_t k, double* dst, bool is_root, cudaStream_t st = nullptr,
                   bool prefetch = false, bool no_pdl = false, int sms = 0);
-    void prefetch_root(uint64_t sweep, uint32_t b);
+    void prefetch_root(uint64_t sweep, uint32_t b, cudaStream_t after);
     void mode_update(uint64_t sweep, uint32_t b, cpdb_q0_observer observer, void* user,
                      double& beta_used);
     void mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer observer, void* user);
-    void mode_update_back(uint64_t sweep, uint32_t b, double& beta_used);
+    // bs: the stream of the V-GEMM and finisher (default: the main one);
+    // host_beta: the host's beta decision is final (frozen gate), no device gate read
+    void mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cudaStream_t bs = nullptr,
+                          bool host_beta = false);
     void undo_speculative_update();
 };
 
