@@ -346,7 +346,14 @@ def main():
             xh = pinned.reshape(local_dims)
         except Exception:
             xh = x_host
-        ctx2 = cpd.Context(local, rank=rank, world=world, nccl_id=nccl_id) if world > 1 else ctx
+        ctx2 = ctx
+        if world > 1:
+            # a second communicator needs its own NCCL unique id (an id
+            # bootstraps exactly one communicator)
+            import torch.distributed as dist
+            obj = [cpd.Context.nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            ctx2 = cpd.Context(local, rank=rank, world=world, nccl_id=obj[0])
         cfg2 = cpd.SolverConfig(rank=c["rank"], max_iterations=K, seed=INIT_SEED)
         barrier(world)
         t0 = time.perf_counter()

@@ -367,6 +367,27 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     }
     ybuf.resize(order);
     for (uint32_t n = 0; n < order; ++n) ybuf[n].ensure(numel(local_dims_of(1u << n)));
+    // every cache slot the plan will use, allocated now: a first use inside
+    // the sweeps would put a cudaMalloc (device-wide sync; C5: 8.6 GB slots)
+    // in the middle of the run
+    {
+        const uint64_t span = std::min<uint64_t>(
+            plan.sweeps.size(), plan.cycle_start + 2 * std::max<uint64_t>(plan.cycle_length, 1) + 1);
+        for (uint64_t sw = 0; sw < span; ++sw)
+            for (const Update& u : plan.sweeps[sw].updates)
+                for (const Step& st : u.steps)
+                    if (st.produces != (1u << u.mode))
+                        cache[st.produces].buf.ensure(numel(local_dims_of(st.produces)));
+        if (prefetch_enabled) {
+            uint64_t mx = 0;
+            for (uint32_t k = 0; k < order; ++k) {
+                std::vector<uint64_t> od = c->ldims;
+                od[k] = R;
+                mx = std::max(mx, numel(od));
+            }
+            pre.ensure(mx);
+        }
+    }
     CPDB_CK(cudaEventCreate(&t_start));
     CPDB_CK(cudaEventRecord(t_start, s));
     CPDB_CK(cudaStreamSynchronize(s));
