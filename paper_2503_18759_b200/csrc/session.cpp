@@ -491,9 +491,8 @@ void Session::prefetch_root(uint64_t sweep, uint32_t b, cudaStream_t after) {
         od[cm] = R;
         pre.ensure(numel(od));
         CPDB_CK(cudaEventRecord(ev_fin, after));  // update b's finisher: Q_cm final
-        CPDB_CK(cudaStreamWaitEvent(c->lo, ev_fin, 0));
-        ttm_step(c->x, c->ldims, 0, cm, pre.p, true, c->lo, true, true);
-        CPDB_CK(cudaEventRecord(pf.ev, c->lo));
+        pf.cm = cm;
+        pf.launched = false;
         // SM budget of the updates in between: they are off the critical
         // path when the root is long (it, not they, gates update b2), so their
         // TTMs get just enough SMs to finish in about half the root's time
@@ -515,6 +514,17 @@ void Session::prefetch_root(uint64_t sweep, uint32_t b, cudaStream_t after) {
         pf.block = b2;
         return;
     }
+}
+
+// The planned root prefetch goes on the low-priority stream right behind the
+// next update's Z-QR launch: the Z-QR's 8-CTA cluster (on the critical path
+// when the root is short, C4) gets its SMs before the root's CTAs fill them.
+void Session::launch_prefetch() {
+    if (!pf.active || pf.launched) return;
+    CPDB_CK(cudaStreamWaitEvent(c->lo, ev_fin, 0));
+    ttm_step(c->x, c->ldims, 0, pf.cm, pre.p, true, c->lo, true, true);
+    CPDB_CK(cudaEventRecord(pf.ev, c->lo));
+    pf.launched = true;
 }
 
 double Session::step_flops(const Step& st) const {
@@ -597,6 +607,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     cudaEvent_t tla = tl_begin(zs);
     CPDB_CK(launch_zqr(z, zs, c->sms));
     tl_end(tla, zs, "zqr");
+    launch_prefetch();
     if (!chain_side) CPDB_CK(cudaEventRecord(ev_zqr, c->side));
     if (early) CPDB_CK(cudaEventRecord(ev_zq, zs));
     if (trace_phases) {
@@ -649,6 +660,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         od[st.contract] = R;
         if (si == 0 && pf.active && pf.sweep == sweep && pf.block == b) {
             // issued early by prefetch_root: adopt its buffer as the slot
+            launch_prefetch();
             cudaEvent_t tlw = tl_begin(ts);
             CPDB_CK(cudaStreamWaitEvent(ts, pf.ev, 0));
             tl_end(tlw, ts, "adopt_wait");
@@ -838,6 +850,8 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         for (uint32_t b = 0; b < order; ++b) {
             if (b == 0 && front_issued) {
                 front_issued = false;  // issued ahead of the previous sweep's host sync
+            } else if (b == 1 && front1_issued) {
+                front1_issued = false;
             } else {
                 mode_update_front(sweep, b, observer, user);
             }
@@ -889,6 +903,13 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
                     mode_update_back(sweep + 1, 0, unused, c->aux, true);
                     CPDB_CK(cudaEventRecord(ev_aux, c->aux));
                     CPDB_CK(cudaStreamWaitEvent(s, ev_aux, 0));
+                    // and the second update's front (Z-QR + chain: no beta,
+                    // no returned state -- nothing to undo), which also
+                    // launches the root prefetch planned by the first
+                    if (order > 2) {
+                        mode_update_front(sweep + 1, 1, nullptr, nullptr);
+                        front1_issued = true;
+                    }
                 } else {
                     mode_update_back(sweep + 1, 0, unused);
                 }

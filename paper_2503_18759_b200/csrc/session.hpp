@@ -91,8 +91,13 @@ struct Session {
         uint64_t sweep = 0;
         uint32_t block = 0;
         int sms = 0;  // SM budget of the updates it overlaps (0: all SMs)
+        uint32_t cm = 0;        // contracted mode
+        bool launched = false;  // planned at update b's end, launched behind the
+                                // next update's Z-QR (launch_prefetch)
         cudaEvent_t ev = nullptr;
     } pf;
+    void launch_prefetch();
+    bool front1_issued = false;  // next sweep's second front issued ahead (Session::run)
     DevBuf pre;
     cudaEvent_t ev_fin = nullptr;
     bool prefetch_enabled = false;
