@@ -100,3 +100,35 @@ def test_nccl_library_available():
     import paper_2503_18759_b200 as cpd
     uid = cpd.Context.nccl_unique_id()
     assert isinstance(uid, bytes) and len(uid) == 128 and any(uid)
+
+
+@pytest.mark.parametrize("dims,world", [((24, 20, 16), 2), ((12, 10, 8, 6), 2)])
+def test_sharded_stop_test_undoes_speculative_update(ctx, port, dims, world):
+    """Sharded runs also issue the next sweep's first update (its collectives
+    included) before reading the fitness; when the stop test fires every rank
+    undoes it and returns the unsharded run's model."""
+    import paper_2503_18759_b200 as cpd
+    x = port.synth_baseline(0, dims, 3, 1e-2, 20250013)
+    ctx.set_tensor(x)
+    thr = ctx.solve(cpd.SolverConfig(rank=3, max_iterations=6, seed=7),
+                    extrapolate=True).trace[-1].fitness
+    cfg = cpd.SolverConfig(rank=3, max_iterations=30, seed=7, fitness_threshold=thr)
+    ref = ctx.solve(cfg, extrapolate=True)
+    assert len(ref.trace) <= 6
+    rows = dims[0] // world
+    group = cpd.Context.local_group(0, world)
+
+    def rank_run(r, c):
+        c.set_tensor(np.ascontiguousarray(x[r * rows:(r + 1) * rows]), dims)
+        return c.solve(cfg, extrapolate=True)
+
+    res = run_ranks(group, rank_run)
+    for g in res:
+        assert len(g.trace) == len(ref.trace)
+        for a, b in zip(g.trace, ref.trace):
+            assert abs(a.fitness - b.fitness) <= 1e-10 * b.fitness
+        for fa, fb in zip(g.model.factors, ref.model.factors):
+            assert np.linalg.norm(fa - fb) <= 1e-10 * np.linalg.norm(fb)
+        assert np.linalg.norm(g.model.lam - ref.model.lam) <= 1e-10 * np.linalg.norm(ref.model.lam)
+    for c in group:
+        c.close()
