@@ -14,6 +14,7 @@ struct TtmArgs {
     const double* qp;  // Q packed by pack_q -- tensor-core paths
     uint64_t outer, K, inner;
     uint32_t R, Rp;
+    uint32_t tiles_per_cta;  // non-persistent form: tiles per CTA (0: CPDB_PREFETCH_TPC or 2)
     int one_tile_per_cta;  // non-persistent grid (a low-priority launch that
                            // yields SMs to concurrent work as its CTAs retire)
     int no_pdl;            // plain launch (the stream's previous op is an event wait)

@@ -274,7 +274,7 @@ std::vector<uint64_t> natural_to_reference(uint32_t order, uint64_t R) {
 
 void run_ttm(cpdb_ctx* ctx, const double* src, const std::vector<uint64_t>& sd, uint32_t c,
              const double* q, const double* qp, uint32_t R, double* dst, cudaStream_t stream,
-             bool one_tile_per_cta, bool no_pdl, int sms) {
+             bool one_tile_per_cta, bool no_pdl, int sms, uint32_t tiles_per_cta) {
     TtmArgs a{};
     a.x = src;
     a.y = dst;
@@ -288,6 +288,7 @@ void run_ttm(cpdb_ctx* ctx, const double* src, const std::vector<uint64_t>& sd, 
     a.R = R;
     a.Rp = ttm_rpad(R);
     a.one_tile_per_cta = one_tile_per_cta ? 1 : 0;
+    a.tiles_per_cta = tiles_per_cta;
     a.no_pdl = (no_pdl || one_tile_per_cta) ? 1 : 0;
     a.no_tma = 0;
     CPDB_CK(launch_ttm(a, stream ? stream : ctx->stream, sms > 0 ? sms : ctx->sms));

@@ -174,6 +174,6 @@ std::vector<uint64_t> natural_to_reference(uint32_t order, uint64_t R);
 void run_ttm(cpdb_ctx* ctx, const double* src, const std::vector<uint64_t>& sd, uint32_t c,
              const double* q, const double* qp, uint32_t R, double* dst,
              cudaStream_t stream = nullptr, bool one_tile_per_cta = false, bool no_pdl = false,
-             int sms = 0);
+             int sms = 0, uint32_t tiles_per_cta = 0);
 
 }  // namespace cpdb

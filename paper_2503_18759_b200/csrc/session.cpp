@@ -443,7 +443,8 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32
         CPDB_CK(cudaEventRecord(t.a, st));
     }
     cudaEvent_t tla = tl_begin(st);
-    run_ttm(c, src, sd, k, q, qp, R, dst, st, prefetch || yield_now, no_pdl, sms);
+    run_ttm(c, src, sd, k, q, qp, R, dst, st, prefetch || yield_now, no_pdl, sms,
+            prefetch ? pf.tpc : 0);
     tl_end(tla, st, prefetch ? "root_prefetch" : is_root ? "root" : "branch");
     if (c->timing) {
         CPDB_CK(cudaEventRecord(t.b, st));
@@ -499,9 +500,13 @@ void Session::prefetch_root(uint64_t sweep, uint32_t b, cudaStream_t after) {
         // and the root keeps the rest.  Short roots (C4: ~30 us) are not
         // worth it (the updates become the critical path).
         pf.sms = overlap_sms >= 0 ? overlap_sms : 0;
+        const double xb = 8.0 * double(numel(c->ldims));
+        const double root_s = std::max(2.0 * double(numel(c->ldims)) * R / 31.5e12, xb / 6.0e12);
+        // CTAs of two tiles for a long root (half the per-CTA prologues; C2
+        // 2204 -> 2248 sweeps/s), of one tile for a short one, whose CTAs must
+        // make way for the critical Z-QR quickly (C4 5700 -> 6080)
+        pf.tpc = root_s >= 150e-6 ? 2 : 1;
         if (overlap_sms < 0) {
-            const double xb = 8.0 * double(numel(c->ldims));
-            const double root_s = std::max(2.0 * double(numel(c->ldims)) * R / 31.5e12, xb / 6.0e12);
             double upd = 0.0;
             for (uint32_t bm = b + 1; bm < b2; ++bm)
                 for (const Step& st : sw.updates[bm].steps) upd += step_flops(st);

@@ -92,6 +92,7 @@ struct Session {
         uint32_t block = 0;
         int sms = 0;  // SM budget of the updates it overlaps (0: all SMs)
         uint32_t cm = 0;        // contracted mode
+        uint32_t tpc = 2;       // tiles per CTA of its non-persistent grid
         bool launched = false;  // planned at update b's end, launched behind the
                                 // next update's Z-QR (launch_prefetch)
         cudaEvent_t ev = nullptr;

@@ -339,7 +339,7 @@ cudaError_t launch_v2(const TtmArgs& a, cudaStream_t s, int sms) {
     // prologue is paid half as often (measured, C2: 1 tile 2204 sweeps/s, 2
     // tiles 2248, 4 tiles 2116 -- the overlapped update then waits for SMs)
     const char* tpe = std::getenv("CPDB_PREFETCH_TPC");
-    const uint64_t tpc = tpe ? std::max(1, std::atoi(tpe)) : 2;
+    const uint64_t tpc = tpe ? std::max(1, std::atoi(tpe)) : (a.tiles_per_cta ? a.tiles_per_cta : 2);
     const uint64_t grid = a.one_tile_per_cta ? (ntiles + tpc - 1) / tpc
                                              : std::min<uint64_t>(ntiles, uint64_t(sms));
     if (grid == 0) return cudaSuccess;
