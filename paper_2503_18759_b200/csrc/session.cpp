@@ -204,6 +204,8 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         // 1911 -> 2003, C3 1258 -> 1310, C4 4626 -> 5259.  CPDB_EARLY_FRONT=0: off.
         const char* ef = std::getenv("CPDB_EARLY_FRONT");
         dep_events = chain_side && !(ef && ef[0] == '0');
+        const char* ce = std::getenv("CPDB_CHAIN_EVENTS");
+        chain_events = dep_events && !(ce && ce[0] == '0');
         const char* sp = std::getenv("CPDB_SPECULATE");
         speculate = !(sp && sp[0] == '0');
         const char* zy = std::getenv("CPDB_ZQR_YIELD");
@@ -602,6 +604,15 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
                 waited |= 1u << st.contract;
             }
         CPDB_CK(cudaStreamWaitEvent(ts, ev_v[n], 0));  // ybuf[n]'s last reader
+    } else if (chain_events) {
+        // Event-driven chain: not behind the previous update's finisher but
+        // behind the previous chain (cached sources, slot reuse) and the
+        // V-GEMM that last read ybuf[n]; each step then waits for the update
+        // that last changed the Q it contracts (below).  A fourth-order
+        // update's first step usually contracts a mode the previous update
+        // did not touch, so it runs under that update's V-GEMM and finisher.
+        CPDB_CK(cudaStreamWaitEvent(ts, ev_zqr, 0));
+        CPDB_CK(cudaStreamWaitEvent(ts, ev_v[n], 0));
     } else {
         CPDB_CK(cudaEventRecord(ev_ready, s));
         CPDB_CK(cudaStreamWaitEvent(chain_side ? ts : c->side, ev_ready, 0));
@@ -614,7 +625,9 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     tl_end(tla, zs, "zqr");
     launch_prefetch();
     if (!chain_side) CPDB_CK(cudaEventRecord(ev_zqr, c->side));
-    if (early) CPDB_CK(cudaEventRecord(ev_zq, zs));
+    // (the V-GEMM may run on another stream than the Z-QR: the speculative
+    // next-sweep update goes on its own stream, Session::run)
+    if (dep_events) CPDB_CK(cudaEventRecord(ev_zq, zs));
     if (trace_phases) {
         unsigned long long ts[32];
         CPDB_CK(cudaMemcpyAsync(ts, z.ts, sizeof ts, cudaMemcpyDeviceToHost, zs));
@@ -637,6 +650,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     // 4. the scheduled TTM chain (execute, dim_tree.hpp:496-541)
     yield_now = zqr_yield;
     bool after_wait = chain_side;  // the side stream's first kernel follows an event wait
+    uint32_t chain_waited = 0;     // (chain_events) modes whose finisher this chain waited for
     for (size_t si = 0; si < sw.updates[b].steps.size(); ++si) {
         const Step& st = sw.updates[b].steps[si];
         const double* src;
@@ -675,6 +689,11 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         } else {
             double* dst =
                 (st.produces == (1u << n)) ? ybuf[n].p : cache[st.produces].buf.ensure(numel(od));
+            if (chain_events && !early && !(chain_waited & (1u << st.contract))) {
+                CPDB_CK(cudaStreamWaitEvent(ts, ev_fac[st.contract], 0));
+                chain_waited |= 1u << st.contract;
+                after_wait = true;
+            }
             ttm_step(src, sd, flags, st.contract, dst, st.source == root, ts, false,
                      after_wait, budget(sweep, b));
             after_wait = false;
@@ -752,7 +771,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     v.v_out = vf.p + off;
     v.vfit_out = v.dual ? vff.p + off : nullptr;
     CPDB_CK(cudaStreamWaitEvent(bs, ev_zqr, 0));
-    if (early) CPDB_CK(cudaStreamWaitEvent(bs, ev_zq, 0));
+    if (dep_events) CPDB_CK(cudaStreamWaitEvent(bs, ev_zq, 0));  // Q0, R0 ready
     tl_sweep = sweep;
     tl_mode = n;
     cudaEvent_t tla = tl_begin(bs);
