@@ -13,7 +13,26 @@
 //   launch_ttm...  the scheduled TTM chain, cache in HBM        (:267)
 //   launch_vgemm   V = Y_(n) Q0_hat, extrapolation fused        (:258-271,277-284)
 //   launch_finish  A_hat, normalise, lambda, factor QR, fitness (:272-275,291)
-// and the host synchronises once per sweep to read the fitness scalar.
+// and the host reads one fitness scalar per sweep.
+//
+// Streams and ordering (unsharded; sharded runs keep the simple form:
+// Z-QR on `side`, chain + collectives + tail on `stream`):
+//   stream (main, high)  V-GEMM, finisher, beta gate; the Z-QR of an update
+//                        whose mode differs from the previous one (launched
+//                        programmatically right behind that finisher)
+//   side   (high)        chains; the Z-QR of a sweep-boundary update
+//   mid    (high - 1)    the chain of a sweep-boundary update
+//   aux    (high)        the next sweep's first V-GEMM + finisher, issued
+//                        before the host reads this sweep's fitness
+//   lo     (low)         the prefetched root TTM (prefetch_root /
+//                        launch_prefetch), two tiles per CTA (one if short)
+// Dependencies are explicit events: ev_fac[k] (the finisher that last
+// changed A_k/Q_k/R_k), ev_v[n] (the V-GEMM that last read ybuf[n]),
+// ev_zread[p] (last readers of Z-QR buffer set p), ev_zq / ev_zqr (this
+// update's Z-QR / chain done), pf.ev (prefetched root done).  Buffers that
+// consecutive updates may touch concurrently are doubled (factors + lambda,
+// Z-QR outputs, V partials, scratch), so a speculative update can be undone
+// by swapping back (undo_speculative_update).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
