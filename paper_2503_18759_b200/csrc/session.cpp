@@ -302,8 +302,10 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     CPDB_CK(cudaEventCreateWithFlags(&ev_aux, cudaEventDisableTiming));
     for (uint32_t k = 0; k < order; ++k) {
         CPDB_CK(cudaEventCreateWithFlags(&ev_fac[k], cudaEventDisableTiming));
-        CPDB_CK(cudaEventCreateWithFlags(&ev_v[k], cudaEventDisableTiming));
         CPDB_CK(cudaEventRecord(ev_fac[k], s));
+    }
+    for (uint32_t k = 0; k < 2 * order; ++k) {
+        CPDB_CK(cudaEventCreateWithFlags(&ev_v[k], cudaEventDisableTiming));
         CPDB_CK(cudaEventRecord(ev_v[k], s));
     }
     for (cudaEvent_t& e : ev_zread) {
@@ -386,8 +388,10 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         events.recycle();
         timers.clear();
     }
-    ybuf.resize(order);
-    for (uint32_t n = 0; n < order; ++n) ybuf[n].ensure(numel(local_dims_of(1u << n)));
+    // Y_(n) per mode and update parity (consecutive updates of the same mode
+    // -- the sweep boundary -- may be in flight together)
+    ybuf.resize(2 * order);
+    for (uint32_t n = 0; n < 2 * order; ++n) ybuf[n].ensure(numel(local_dims_of(1u << (n / 2))));
     // every cache slot the plan will use, allocated now: a first use inside
     // the sweeps would put a cudaMalloc (device-wide sync; C5: 8.6 GB slots)
     // in the middle of the run
@@ -622,7 +626,11 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
                 CPDB_CK(cudaStreamWaitEvent(ts, ev_fac[st.contract], 0));
                 waited |= 1u << st.contract;
             }
-        CPDB_CK(cudaStreamWaitEvent(ts, ev_v[n], 0));  // ybuf[n]'s last reader
+        // the previous chain (cached sources) and the older V-GEMM that last
+        // read this parity's ybuf -- not the previous update's V-GEMM: its
+        // Y_(n) is the other parity's buffer, so this chain runs beside it
+        CPDB_CK(cudaStreamWaitEvent(ts, ev_zqr, 0));
+        CPDB_CK(cudaStreamWaitEvent(ts, ev_v[2 * n + zpar], 0));
     } else if (chain_events) {
         // Event-driven chain: not behind the previous update's finisher but
         // behind the previous chain (cached sources, slot reuse) and the
@@ -631,7 +639,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         // update's first step usually contracts a mode the previous update
         // did not touch, so it runs under that update's V-GEMM and finisher.
         CPDB_CK(cudaStreamWaitEvent(ts, ev_zqr, 0));
-        CPDB_CK(cudaStreamWaitEvent(ts, ev_v[n], 0));
+        CPDB_CK(cudaStreamWaitEvent(ts, ev_v[2 * n + zpar], 0));
     } else {
         CPDB_CK(cudaEventRecord(ev_ready, s));
         CPDB_CK(cudaStreamWaitEvent(chain_side ? ts : c->side, ev_ready, 0));
@@ -706,8 +714,8 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
             pf.active = false;
             after_wait = true;
         } else {
-            double* dst =
-                (st.produces == (1u << n)) ? ybuf[n].p : cache[st.produces].buf.ensure(numel(od));
+            double* dst = (st.produces == (1u << n)) ? ybuf[2 * n + zpar].p
+                                                    : cache[st.produces].buf.ensure(numel(od));
             if (chain_events && !early && !(chain_waited & (1u << st.contract))) {
                 CPDB_CK(cudaStreamWaitEvent(ts, ev_fac[st.contract], 0));
                 chain_waited |= 1u << st.contract;
@@ -759,7 +767,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     // 5. V = Y_(n) Q0_hat (+ the unextrapolated V for the fitness, :277-284)
     const std::vector<uint64_t> yd = local_dims_of(1u << n);
     VgemmArgs v{};
-    v.y = ybuf[n].p;
+    v.y = ybuf[2 * n + zpar].p;
     ZBuf& zcur = zb[zpar];
     v.q0 = zcur.q0.p;
     v.hist = maybe_ex ? hist[n].p : nullptr;
@@ -805,7 +813,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     CPDB_CK(launch_vgemm(v, bs, vsms > 0 ? vsms : c->sms));
     tl_end(tla, bs, "vgemm");
     c->launches += 1;
-    if (dep_events) CPDB_CK(cudaEventRecord(ev_v[n], bs));  // ybuf[n] consumed
+    if (dep_events) CPDB_CK(cudaEventRecord(ev_v[2 * n + zpar], bs));  // ybuf consumed
     // the cluster finisher sums the split-K partials itself (no reduction
     // launch on the chain); gathered (sharded mode-0) V needs them reduced
     const bool fused = vsplit_max > 0 && !v.reduced && !gather && v.nsplit <= 64 &&

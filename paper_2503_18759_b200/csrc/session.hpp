@@ -68,7 +68,8 @@ struct Session {
     // finisher that last updated each mode, the V-GEMM that last read ybuf[n],
     // the last readers of each Z-QR buffer set, and the front's joins
     bool dep_events = false;
-    cudaEvent_t ev_fac[CPDB_MAX_ORDER] = {}, ev_v[CPDB_MAX_ORDER] = {}, ev_zread[2] = {};
+    // ev_v[2n + parity]: the V-GEMM that last read ybuf[2n + parity]
+    cudaEvent_t ev_fac[CPDB_MAX_ORDER] = {}, ev_v[2 * CPDB_MAX_ORDER] = {}, ev_zread[2] = {};
     cudaEvent_t ev_zq = nullptr, ev_aux = nullptr;
     int last_mode = -1;   // mode of the last update issued (back)
     bool early = false;   // this update's front runs event-driven (set by the front)
