@@ -609,6 +609,13 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     // finisher, measured faster when it has to wait for that finisher anyway).
     early = dep_events && last_mode == int(n);
     cudaStream_t zs = early ? c->side : chain_side ? s : c->side;
+    if (!early && zqr_stream_override) {
+        // right behind the speculative update's finisher on its own stream,
+        // so its cluster is resident before the root prefetch and the chain
+        // fill the GPU; the Z-QR buffer set's last readers ran elsewhere
+        zs = zqr_stream_override;
+        CPDB_CK(cudaStreamWaitEvent(zs, ev_zread[zpar], 0));
+    }
     static const bool trace_phases = std::getenv("CPDB_PHASE_TRACE") != nullptr;
     if (trace_phases) {
         z.ts = reinterpret_cast<unsigned long long*>(zts.ensure(32));
@@ -958,7 +965,15 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
                     // no returned state -- nothing to undo), which also
                     // launches the root prefetch planned by the first
                     if (order > 2) {
+                        // (its Z-QR right behind the speculative finisher on
+                        // aux: measured C4 6270 -> 6440 sweeps/s, C1 +1%; C3
+                        // (fourth order) -2%, so third order only;
+                        // CPDB_ZQR_AUX=0/1 overrides)
+                        static const char* zae = std::getenv("CPDB_ZQR_AUX");
+                        const bool zaux = zae ? zae[0] == '1' : order == 3;
+                        if (zaux) zqr_stream_override = c->aux;
                         mode_update_front(sweep + 1, 1, nullptr, nullptr);
+                        zqr_stream_override = nullptr;
                         front1_issued = true;
                     }
                 } else {

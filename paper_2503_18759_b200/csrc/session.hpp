@@ -72,6 +72,7 @@ struct Session {
     cudaEvent_t ev_fac[CPDB_MAX_ORDER] = {}, ev_v[2 * CPDB_MAX_ORDER] = {}, ev_zread[2] = {};
     cudaEvent_t ev_zq = nullptr, ev_aux = nullptr;
     int last_mode = -1;   // mode of the last update issued (back)
+    cudaStream_t zqr_stream_override = nullptr;  // (run: the speculative second front)
     bool early = false;   // this update's front runs event-driven (set by the front)
     bool chain_events = false;  // CPDB_CHAIN_EVENTS: every chain step waits only for its Q_c
     std::vector<DevBuf> hist, ybuf;
