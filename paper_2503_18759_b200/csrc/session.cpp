@@ -521,7 +521,7 @@ void Session::prefetch_root(uint64_t sweep, uint32_t b, cudaStream_t after) {
         pf.launched = false;
         // SM budget of the updates in between: they are off the critical
         // path when the root is long (it, not they, gates update b2), so their
-        // TTMs get just enough SMs to finish in about half the root's time
+        // TTMs get just enough SMs to finish well within the root's time
         // and the root keeps the rest.  Short roots (C4: ~30 us) are not
         // worth it (the updates become the critical path).
         pf.sms = overlap_sms >= 0 ? overlap_sms : 0;
@@ -536,7 +536,13 @@ void Session::prefetch_root(uint64_t sweep, uint32_t b, cudaStream_t after) {
             for (uint32_t bm = b + 1; bm < b2; ++bm)
                 for (const Step& st : sw.updates[bm].steps) upd += step_flops(st);
             const double per_sm = 0.15e12;  // FP64 FLOP/s per SM on a small grid
-            const int need = int(std::ceil(upd / (0.5 * root_s * per_sm)));
+            // finish in ~0.38 of the root's time (measured: 0.5 C2 2235
+            // sweeps/s, 0.38 2264, 0.3 2192; C3 flat)
+            static const double frac = [] {
+                const char* e = std::getenv("CPDB_OVERLAP_FRAC");
+                return e ? std::atof(e) : 0.38;
+            }();
+            const int need = int(std::ceil(upd / (frac * root_s * per_sm)));
             if (root_s >= 150e-6 && need < c->sms / 2) pf.sms = std::max(need, 16);
         }
         pf.active = true;
