@@ -23,16 +23,17 @@
 //   side   (high)        chains; the Z-QR of a sweep-boundary update
 //   mid    (high - 1)    the chain of a sweep-boundary update
 //   aux    (high)        the next sweep's first V-GEMM + finisher, issued
-//                        before the host reads this sweep's fitness
+//                        before the host reads this sweep's fitness (third
+//                        order: and the second update's Z-QR right behind)
 //   lo     (low)         the prefetched root TTM (prefetch_root /
 //                        launch_prefetch), two tiles per CTA (one if short)
 // Dependencies are explicit events: ev_fac[k] (the finisher that last
-// changed A_k/Q_k/R_k), ev_v[n] (the V-GEMM that last read ybuf[n]),
+// changed A_k/Q_k/R_k), ev_v[2n+p] (the V-GEMM that last read ybuf[2n+p]),
 // ev_zread[p] (last readers of Z-QR buffer set p), ev_zq / ev_zqr (this
 // update's Z-QR / chain done), pf.ev (prefetched root done).  Buffers that
 // consecutive updates may touch concurrently are doubled (factors + lambda,
-// Z-QR outputs, V partials, scratch), so a speculative update can be undone
-// by swapping back (undo_speculative_update).
+// Z-QR outputs, Y_(n), V partials, scratch), so a speculative update can be
+// undone by swapping back (undo_speculative_update).
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
