@@ -90,6 +90,7 @@ void init_ctx(cpdb_ctx* c, int device) {
     CPDB_CK(cudaStreamCreateWithPriority(&c->lo, cudaStreamNonBlocking, least));
     // the next sweep's first V-GEMM + finisher beside this sweep's last ones
     CPDB_CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, greatest));
+    CPDB_CK(cudaStreamCreateWithPriority(&c->zq, cudaStreamNonBlocking, greatest));
     // a TTM chain that must yield SMs to a concurrent multi-kernel Z-QR
     CPDB_CK(cudaStreamCreateWithPriority(&c->mid, cudaStreamNonBlocking,
                                          greatest < least ? greatest + 1 : greatest));

@@ -302,6 +302,7 @@ cpdb_ctx::~cpdb_ctx() {
     if (lo) cudaStreamSynchronize(lo);
     if (mid) cudaStreamSynchronize(mid);
     if (aux) cudaStreamSynchronize(aux);
+    if (zq) cudaStreamSynchronize(zq);
     if (comm) {
         const cpdb::Nccl& N = cpdb::nccl();
         if (N.ok) N.CommDestroy(static_cast<ncclComm_t>(comm));
@@ -313,4 +314,5 @@ cpdb_ctx::~cpdb_ctx() {
     if (lo) cudaStreamDestroy(lo);
     if (mid) cudaStreamDestroy(mid);
     if (aux) cudaStreamDestroy(aux);
+    if (zq) cudaStreamDestroy(zq);
 }

@@ -112,6 +112,7 @@ struct cpdb_ctx {
     cudaStream_t lo = nullptr;    // low priority: root TTM prefetched under the previous update
     cudaStream_t mid = nullptr;   // below stream/side: TTM chain beside a multi-kernel Z-QR
     cudaStream_t aux = nullptr;   // speculative next-sweep update beside the last one
+    cudaStream_t zq = nullptr;    // the sweep-boundary Z-QR (not behind any chain)
 
     // sharding: leading mode split in contiguous slabs
     int rank = 0, world = 1;

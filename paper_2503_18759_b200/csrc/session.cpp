@@ -96,6 +96,7 @@ Session::~Session() {
     if (c && c->lo) cudaStreamSynchronize(c->lo);
     if (c && c->mid) cudaStreamSynchronize(c->mid);
     if (c && c->aux) cudaStreamSynchronize(c->aux);
+    if (c && c->zq) cudaStreamSynchronize(c->zq);
     if (ev_fin) cudaEventDestroy(ev_fin);
     if (pf.ev) cudaEventDestroy(pf.ev);
     if (t_start) cudaEventDestroy(t_start);
@@ -109,6 +110,10 @@ Session::~Session() {
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_zread)
         if (e) cudaEventDestroy(e);
+    for (auto& kv : slot_ready) cudaEventDestroy(kv.second);
+    for (cudaEvent_t e : ev_hist)
+        if (e) cudaEventDestroy(e);
+    if (ev_zq_pending) cudaEventDestroy(ev_zq_pending);
 }
 
 // ---------------------------------------------------------------- timeline
@@ -125,7 +130,7 @@ void Session::tl_end(cudaEvent_t a, cudaStream_t st, const char* label) {
     cudaEvent_t b;
     CPDB_CK(cudaEventCreate(&b));
     CPDB_CK(cudaEventRecord(b, st));
-    const int sid = st == c->side ? 1 : st == c->lo ? 2 : st == c->mid ? 3 : st == c->aux ? 4 : 0;
+    const int sid = st == c->side ? 1 : st == c->lo ? 2 : st == c->mid ? 3 : st == c->aux ? 4 : st == c->zq ? 5 : 0;
     marks.push_back(Mark{label, sid, tl_sweep, tl_mode, a, b});
 }
 
@@ -309,6 +314,12 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         CPDB_CK(cudaEventCreateWithFlags(&ev_v[k], cudaEventDisableTiming));
         CPDB_CK(cudaEventRecord(ev_v[k], s));
     }
+    for (uint32_t k = 0; k < order; ++k) {
+        CPDB_CK(cudaEventCreateWithFlags(&ev_hist[k], cudaEventDisableTiming));
+        CPDB_CK(cudaEventRecord(ev_hist[k], s));
+    }
+    CPDB_CK(cudaEventCreateWithFlags(&ev_zq_pending, cudaEventDisableTiming));
+    CPDB_CK(cudaEventRecord(ev_zq_pending, s));
     for (cudaEvent_t& e : ev_zread) {
         CPDB_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         CPDB_CK(cudaEventRecord(e, s));
@@ -564,6 +575,16 @@ void Session::launch_prefetch() {
     pf.launched = true;
 }
 
+cudaEvent_t Session::ready_event(uint32_t key) {
+    auto it = slot_ready.find(key);
+    if (it != slot_ready.end()) return it->second;
+    cudaEvent_t e;
+    CPDB_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CPDB_CK(cudaEventRecord(e, s));  // (first use: everything issued so far)
+    slot_ready[key] = e;
+    return e;
+}
+
 double Session::step_flops(const Step& st) const {
     uint64_t out = 1;
     for (uint32_t k = 0; k < order; ++k)
@@ -615,7 +636,11 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     // form below (its Z-QR launches programmatically right behind the
     // finisher, measured faster when it has to wait for that finisher anyway).
     early = dep_events && last_mode == int(n);
-    cudaStream_t zs = early ? c->side : chain_side ? s : c->side;
+    // (the sweep-boundary Z-QR on its own stream, not behind the previous
+    // chain on `side`: single-kernel cluster form only -- the multi-kernel
+    // tall-Z form keeps the stream order it was validated with)
+    const bool zq_ok = zqr_cluster_fits(zrows, R, order - 1);
+    cudaStream_t zs = early ? (zq_ok ? c->zq : c->side) : chain_side ? s : c->side;
     if (!early && zqr_stream_override) {
         // right behind the speculative update's finisher on its own stream,
         // so its cluster is resident before the root prefetch and the chain
@@ -640,11 +665,22 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
                 CPDB_CK(cudaStreamWaitEvent(ts, ev_fac[st.contract], 0));
                 waited |= 1u << st.contract;
             }
-        // the previous chain (cached sources) and the older V-GEMM that last
-        // read this parity's ybuf -- not the previous update's V-GEMM: its
-        // Y_(n) is the other parity's buffer, so this chain runs beside it
-        CPDB_CK(cudaStreamWaitEvent(ts, ev_zqr, 0));
+        // the producer of its cached source (the previous update's adopted
+        // root, typically) and the older V-GEMM that last read this parity's
+        // ybuf -- not the previous chain or V-GEMM: this chain (the same
+        // contraction as the previous update's last step) runs beside them.
+        // A chain that also writes cache slots waits for the previous one.
         CPDB_CK(cudaStreamWaitEvent(ts, ev_v[2 * n + zpar], 0));
+        const Step& s0 = sw.updates[b].steps.front();
+        if (s0.source != root) CPDB_CK(cudaStreamWaitEvent(ts, ready_event(s0.source), 0));
+        bool writes_slots = false;
+        for (const Step& st : sw.updates[b].steps) writes_slots |= st.produces != (1u << n);
+        static const bool relaxed = [] {
+            const char* e = std::getenv("CPDB_EARLY_CHAIN_RELAXED");
+            return e && e[0] == '1';
+        }();
+        if (!relaxed || writes_slots || s0.source == root)
+            CPDB_CK(cudaStreamWaitEvent(ts, ev_zqr, 0));
     } else if (chain_events) {
         // Event-driven chain: not behind the previous update's finisher but
         // behind the previous chain (cached sources, slot reuse) and the
@@ -669,6 +705,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     // (the V-GEMM may run on another stream than the Z-QR: the speculative
     // next-sweep update goes on its own stream, Session::run)
     if (dep_events) CPDB_CK(cudaEventRecord(ev_zq, zs));
+    CPDB_CK(cudaEventRecord(ev_zq_pending, zs));  // becomes ev_hist[n] at the back
     if (trace_phases) {
         unsigned long long ts[32];
         CPDB_CK(cudaMemcpyAsync(ts, z.ts, sizeof ts, cudaMemcpyDeviceToHost, zs));
@@ -727,6 +764,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
             cache[st.produces].buf.swap(pre);
             pf.active = false;
             after_wait = true;
+            if (dep_events) CPDB_CK(cudaEventRecord(ready_event(st.produces), ts));
         } else {
             double* dst = (st.produces == (1u << n)) ? ybuf[2 * n + zpar].p
                                                     : cache[st.produces].buf.ensure(numel(od));
@@ -738,6 +776,8 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
             ttm_step(src, sd, flags, st.contract, dst, st.source == root, ts, false,
                      after_wait, budget(sweep, b));
             after_wait = false;
+            if (dep_events && st.produces != (1u << n))
+                CPDB_CK(cudaEventRecord(ready_event(st.produces), ts));
         }
         // global-extent flop count, exactly as the reference counts it
         uint64_t gout = 1;
@@ -813,6 +853,9 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     v.vfit_out = v.dual ? vff.p + off : nullptr;
     CPDB_CK(cudaStreamWaitEvent(bs, ev_zqr, 0));
     if (dep_events) CPDB_CK(cudaStreamWaitEvent(bs, ev_zq, 0));  // Q0, R0 ready
+    // the history Q0 comes from the previous update of this mode's Z-QR, which
+    // nothing else orders before this V-GEMM once the fronts are event-driven
+    if (maybe_ex) CPDB_CK(cudaStreamWaitEvent(bs, ev_hist[n], 0));
     tl_sweep = sweep;
     tl_mode = n;
     cudaEvent_t tla = tl_begin(bs);
@@ -892,6 +935,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     ++versions[n];
     if (extrap) {
         hist[n].swap(zcur.q0);  // the history keeps the unextrapolated Q0 (:265)
+        std::swap(ev_hist[n], ev_zq_pending);
         has_hist[n] = true;
     }
     zpar ^= 1;
@@ -1085,7 +1129,10 @@ void Session::undo_speculative_update() {
     fb[n].swap(fb_alt[n]);
     lam.swap(lam_alt);
     zpar ^= 1;
-    if (extrap) hist[n].swap(zb[zpar].q0);
+    if (extrap) {
+        hist[n].swap(zb[zpar].q0);
+        std::swap(ev_hist[n], ev_zq_pending);
+    }
     has_hist[n] = spec.had_hist;
     --versions[n];
     last_mode = spec.prev_last_mode;

@@ -70,6 +70,11 @@ struct Session {
     bool dep_events = false;
     // ev_v[2n + parity]: the V-GEMM that last read ybuf[2n + parity]
     cudaEvent_t ev_fac[CPDB_MAX_ORDER] = {}, ev_v[2 * CPDB_MAX_ORDER] = {}, ev_zread[2] = {};
+    std::map<uint32_t, cudaEvent_t> slot_ready;  // cache slot -> its producer done
+    // ev_hist[n]: the Z-QR that produced hist[n] (the Q0 history of mode n);
+    // ev_zq_pending: this update's Z-QR, swapped into ev_hist[n] by its back
+    cudaEvent_t ev_hist[CPDB_MAX_ORDER] = {}, ev_zq_pending = nullptr;
+    cudaEvent_t ready_event(uint32_t key);
     cudaEvent_t ev_zq = nullptr, ev_aux = nullptr;
     int last_mode = -1;   // mode of the last update issued (back)
     cudaStream_t zqr_stream_override = nullptr;  // (run: the speculative second front)
