@@ -637,10 +637,8 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     // finisher, measured faster when it has to wait for that finisher anyway).
     early = dep_events && last_mode == int(n);
     // (the sweep-boundary Z-QR on its own stream, not behind the previous
-    // chain on `side`: single-kernel cluster form only -- the multi-kernel
-    // tall-Z form keeps the stream order it was validated with)
-    const bool zq_ok = zqr_cluster_fits(zrows, R, order - 1);
-    cudaStream_t zs = early ? (zq_ok ? c->zq : c->side) : chain_side ? s : c->side;
+    // chain on `side`)
+    cudaStream_t zs = early ? c->zq : chain_side ? s : c->side;
     if (!early && zqr_stream_override) {
         // right behind the speculative update's finisher on its own stream,
         // so its cluster is resident before the root prefetch and the chain
@@ -675,9 +673,10 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         if (s0.source != root) CPDB_CK(cudaStreamWaitEvent(ts, ready_event(s0.source), 0));
         bool writes_slots = false;
         for (const Step& st : sw.updates[b].steps) writes_slots |= st.produces != (1u << n);
+        // (measured: C2 2278 -> 2363 sweeps/s; CPDB_EARLY_CHAIN_RELAXED=0 off)
         static const bool relaxed = [] {
             const char* e = std::getenv("CPDB_EARLY_CHAIN_RELAXED");
-            return e && e[0] == '1';
+            return !(e && e[0] == '0');
         }();
         if (!relaxed || writes_slots || s0.source == root)
             CPDB_CK(cudaStreamWaitEvent(ts, ev_zqr, 0));
