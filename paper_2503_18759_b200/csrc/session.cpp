@@ -20,8 +20,10 @@
 //   stream (main, high)  V-GEMM, finisher, beta gate; the Z-QR of an update
 //                        whose mode differs from the previous one (launched
 //                        programmatically right behind that finisher)
-//   side   (high)        chains; the Z-QR of a sweep-boundary update
-//   mid    (high - 1)    the chain of a sweep-boundary update
+//   side   (high)        chains
+//   zq     (high)        the Z-QR of a sweep-boundary update
+//   mid    (high - 1)    the chain of a sweep-boundary update (waits only for
+//                        its cached source, not for the previous chain)
 //   aux    (high)        the next sweep's first V-GEMM + finisher, issued
 //                        before the host reads this sweep's fitness (third
 //                        order: and the second update's Z-QR right behind)
@@ -30,7 +32,9 @@
 // Dependencies are explicit events: ev_fac[k] (the finisher that last
 // changed A_k/Q_k/R_k), ev_v[2n+p] (the V-GEMM that last read ybuf[2n+p]),
 // ev_zread[p] (last readers of Z-QR buffer set p), ev_zq / ev_zqr (this
-// update's Z-QR / chain done), pf.ev (prefetched root done).  Buffers that
+// update's Z-QR / chain done), ev_hist[n] (the Z-QR that produced the Q0
+// history of mode n), slot_ready (a cache slot's producer), pf.ev
+// (prefetched root done).  Buffers that
 // consecutive updates may touch concurrently are doubled (factors + lambda,
 // Z-QR outputs, Y_(n), V partials, scratch), so a speculative update can be
 // undone by swapping back (undo_speculative_update).
