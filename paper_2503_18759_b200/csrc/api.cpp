@@ -82,18 +82,23 @@ void init_ctx(cpdb_ctx* c, int device) {
     CPDB_CK(cudaSetDevice(device));
     c->sms = p.multiProcessorCount;
     // the solve's critical path (stream, side) at high priority; the root-TTM
-    // prefetch (lo) yields to it CTA by CTA (Session::prefetch_root)
+    // prefetch (lo) yields to it CTA by CTA (Session::prefetch_root).  With a
+    // small Z the chains (side) sit one level below the latency-bound Z-QR /
+    // V-GEMM / finisher kernels so those get SMs first when both are ready
+    // (measured: C3 1447 -> 1506 sweeps/s, C1 C2 C4 flat); a tall-Z run (C5,
+    // TTM-dominated) keeps them on side_hi (low priority there: 25.1 -> 24.3)
     int least = 0, greatest = 0;
     CPDB_CK(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    const int below = greatest < least ? greatest + 1 : greatest;
     CPDB_CK(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, greatest));
-    CPDB_CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, greatest));
+    CPDB_CK(cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, below));
+    CPDB_CK(cudaStreamCreateWithPriority(&c->side_hi, cudaStreamNonBlocking, greatest));
     CPDB_CK(cudaStreamCreateWithPriority(&c->lo, cudaStreamNonBlocking, least));
     // the next sweep's first V-GEMM + finisher beside this sweep's last ones
     CPDB_CK(cudaStreamCreateWithPriority(&c->aux, cudaStreamNonBlocking, greatest));
     CPDB_CK(cudaStreamCreateWithPriority(&c->zq, cudaStreamNonBlocking, greatest));
     // a TTM chain that must yield SMs to a concurrent multi-kernel Z-QR
-    CPDB_CK(cudaStreamCreateWithPriority(&c->mid, cudaStreamNonBlocking,
-                                         greatest < least ? greatest + 1 : greatest));
+    CPDB_CK(cudaStreamCreateWithPriority(&c->mid, cudaStreamNonBlocking, below));
     CPDB_CK(cudaMalloc(&c->dstatus, 64));
     CPDB_CK(cudaMemset(c->dstatus, 0, 64));
     CPDB_CK(cudaMallocHost(&c->pinned, 64 * sizeof(double)));

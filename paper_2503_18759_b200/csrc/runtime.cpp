@@ -303,6 +303,8 @@ cpdb_ctx::~cpdb_ctx() {
     if (mid) cudaStreamSynchronize(mid);
     if (aux) cudaStreamSynchronize(aux);
     if (zq) cudaStreamSynchronize(zq);
+    if (side) cudaStreamSynchronize(side);
+    if (side_hi) cudaStreamSynchronize(side_hi);
     if (comm) {
         const cpdb::Nccl& N = cpdb::nccl();
         if (N.ok) N.CommDestroy(static_cast<ncclComm_t>(comm));
@@ -311,6 +313,7 @@ cpdb_ctx::~cpdb_ctx() {
     if (pinned) cudaFreeHost(pinned);
     if (stream) cudaStreamDestroy(stream);
     if (side) cudaStreamDestroy(side);
+    if (side_hi) cudaStreamDestroy(side_hi);
     if (lo) cudaStreamDestroy(lo);
     if (mid) cudaStreamDestroy(mid);
     if (aux) cudaStreamDestroy(aux);

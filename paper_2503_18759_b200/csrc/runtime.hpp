@@ -109,6 +109,7 @@ struct cpdb_ctx {
     int sms = 148;
     cudaStream_t stream = nullptr;
     cudaStream_t side = nullptr;  // Z-QR overlapped with the TTM chain
+    cudaStream_t side_hi = nullptr;  // the same at top priority (tall-Z runs)
     cudaStream_t lo = nullptr;    // low priority: root TTM prefetched under the previous update
     cudaStream_t mid = nullptr;   // below stream/side: TTM chain beside a multi-kernel Z-QR
     cudaStream_t aux = nullptr;   // speculative next-sweep update beside the last one

@@ -20,7 +20,7 @@
 //   stream (main, high)  V-GEMM, finisher, beta gate; the Z-QR of an update
 //                        whose mode differs from the previous one (launched
 //                        programmatically right behind that finisher)
-//   side   (high)        chains
+//   side   (high - 1)    chains (below the latency-bound kernels)
 //   zq     (high)        the Z-QR of a sweep-boundary update
 //   mid    (high - 1)    the chain of a sweep-boundary update (waits only for
 //                        its cached source, not for the previous chain)
@@ -97,6 +97,7 @@ EventPool::~EventPool() {
 Session::~Session() {
     if (c && c->stream) cudaStreamSynchronize(c->stream);
     if (c && c->side) cudaStreamSynchronize(c->side);
+    if (c && c->side_hi) cudaStreamSynchronize(c->side_hi);
     if (c && c->lo) cudaStreamSynchronize(c->lo);
     if (c && c->mid) cudaStreamSynchronize(c->mid);
     if (c && c->aux) cudaStreamSynchronize(c->aux);
@@ -134,7 +135,7 @@ void Session::tl_end(cudaEvent_t a, cudaStream_t st, const char* label) {
     cudaEvent_t b;
     CPDB_CK(cudaEventCreate(&b));
     CPDB_CK(cudaEventRecord(b, st));
-    const int sid = st == c->side ? 1 : st == c->lo ? 2 : st == c->mid ? 3 : st == c->aux ? 4 : st == c->zq ? 5 : 0;
+    const int sid = st == side ? 1 : st == c->lo ? 2 : st == c->mid ? 3 : st == c->aux ? 4 : st == c->zq ? 5 : 0;
     marks.push_back(Mark{label, sid, tl_sweep, tl_mode, a, b});
 }
 
@@ -195,8 +196,10 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     }
     sharded = c->world > 1;
     s = c->stream;
+    side = c->side;
     zrows = 1;
     for (uint32_t k = 1; k < order; ++k) zrows *= R;
+    if (!zqr_cluster_fits(zrows, R, order - 1)) side = c->side_hi;  // tall Z (api.cpp)
     maxI = 0;
     nfac = 0;
     for (uint64_t d : c->dims) {
@@ -642,7 +645,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     early = dep_events && last_mode == int(n);
     // (the sweep-boundary Z-QR on its own stream, not behind the previous
     // chain on `side`)
-    cudaStream_t zs = early ? c->zq : chain_side ? s : c->side;
+    cudaStream_t zs = early ? c->zq : chain_side ? s : side;
     if (!early && zqr_stream_override) {
         // right behind the speculative update's finisher on its own stream,
         // so its cluster is resident before the root prefetch and the chain
@@ -656,7 +659,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         CPDB_CK(cudaMemsetAsync(z.ts, 0, 32 * sizeof(double), zs));
     }
     const cudaStream_t ts =
-        early ? c->mid : chain_side ? (zqr_yield ? c->mid : c->side) : s;
+        early ? c->mid : chain_side ? (zqr_yield ? c->mid : side) : s;
     if (early) {
         for (uint32_t k = 0; k < order; ++k)
             if (k != n) CPDB_CK(cudaStreamWaitEvent(zs, ev_fac[k], 0));
@@ -695,7 +698,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         CPDB_CK(cudaStreamWaitEvent(ts, ev_v[2 * n + zpar], 0));
     } else {
         CPDB_CK(cudaEventRecord(ev_ready, s));
-        CPDB_CK(cudaStreamWaitEvent(chain_side ? ts : c->side, ev_ready, 0));
+        CPDB_CK(cudaStreamWaitEvent(chain_side ? ts : side, ev_ready, 0));
     }
     z.pdl = chain_side && !early && !trace_phases ? 1 : 0;
     tl_sweep = sweep;
@@ -704,7 +707,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     CPDB_CK(launch_zqr(z, zs, c->sms));
     tl_end(tla, zs, "zqr");
     launch_prefetch();
-    if (!chain_side) CPDB_CK(cudaEventRecord(ev_zqr, c->side));
+    if (!chain_side) CPDB_CK(cudaEventRecord(ev_zqr, side));
     // (the V-GEMM may run on another stream than the Z-QR: the speculative
     // next-sweep update goes on its own stream, Session::run)
     if (dep_events) CPDB_CK(cudaEventRecord(ev_zq, zs));

@@ -80,6 +80,7 @@ struct Session {
     cudaStream_t zqr_stream_override = nullptr;  // (run: the speculative second front)
     bool early = false;   // this update's front runs event-driven (set by the front)
     bool chain_events = false;  // CPDB_CHAIN_EVENTS: every chain step waits only for its Q_c
+    cudaStream_t side = nullptr;  // c->side, or c->side_hi for a tall Z
     std::vector<DevBuf> hist, ybuf;
     std::vector<bool> has_hist;
     std::vector<uint64_t> versions;
