@@ -334,3 +334,14 @@ def test_stop_test_undoes_speculative_update(ctx, port, monkeypatch, speculate, 
     assert 2 < len(o.trace) <= 10
     g = cpd.als_qr_bre(x, cfg_of(3, 40, seed=5, fitness_threshold=thr), ctx=ctx)
     compare(g, o, factor_tol=1e-9)
+
+
+def test_tall_z_fourth_order_vs_oracle(ctx, port):
+    """The tall-Z Z-QR (multi-kernel form, C5's path: Z = 32768 x 32 does not
+    fit the 8-CTA cluster) on a fourth-order tensor, BRE, against the oracle."""
+    import paper_2503_18759_b200 as cpd
+    dims = (40, 36, 34, 33)
+    x = port.synth_baseline(0, dims, 32, 1e-3, META["truth_seeds"]["c5"])
+    g = cpd.als_qr_bre(x, cfg_of(32, 3, seed=META["init_seed"]), ctx=ctx)
+    o = port.solve(x, 32, 3, extrapolate=True, seed=META["init_seed"])
+    compare(g, o, factor_tol=1e-9)
