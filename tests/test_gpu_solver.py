@@ -342,6 +342,7 @@ def test_tall_z_fourth_order_vs_oracle(ctx, port):
     import paper_2503_18759_b200 as cpd
     dims = (40, 36, 34, 33)
     x = port.synth_baseline(0, dims, 32, 1e-3, META["truth_seeds"]["c5"])
-    g = cpd.als_qr_bre(x, cfg_of(32, 3, seed=META["init_seed"]), ctx=ctx)
-    o = port.solve(x, 32, 3, extrapolate=True, seed=META["init_seed"])
+    g = cpd.als_qr_bre(x, cfg_of(32, 8, seed=META["init_seed"]), ctx=ctx)
+    o = port.solve(x, 32, 8, extrapolate=True, seed=META["init_seed"])
     compare(g, o, factor_tol=1e-9)
+    assert any(t.beta_used != 0.0 for t in g.trace)  # the history path runs too
