@@ -257,6 +257,7 @@ class Context:
         if state is None and init is not None:
             state = SweepState(0, np.asarray(init.lam, dtype=np.float64), list(init.factors))
         if state is not None:
+            check_init_state(state, dims, R)
             s_lam = _f64(state.lam).copy()
             s_fac = np.concatenate([_f64(f).ravel() for f in state.factors])
             s_hist = np.zeros(order * zrows * R)
@@ -350,6 +351,32 @@ def _config(cfg: "SolverConfig", extrapolate: bool) -> _cpdb.Config:
                         has_beta_override=0 if cfg.beta_override is None else 1,
                         beta_override=0.0 if cfg.beta_override is None else float(cfg.beta_override),
                         activation_gap=float(cfg.activation_gap), seed=int(cfg.seed))
+
+
+def check_init_state(state: "SweepState", dims: Sequence[int], rank: int) -> None:
+    """initial_factors' guard (solvers.hpp:105-112) for a given model or
+    sweep-boundary state, BEFORE any buffer reaches the C ABI (which copies
+    order x I_k x R factors, R weights and R^(N-1) x R Q0 histories blindly):
+    order / rank mismatch -> "init model does not match tensor/config", row
+    mismatch -> "init factor rows do not match tensor"."""
+    order, R = len(dims), int(rank)
+    facs = list(state.factors)
+    lam = np.asarray(state.lam)
+    if (len(facs) != order or lam.ndim != 1 or lam.shape[0] != R
+            or any(np.asarray(f).ndim != 2 or np.asarray(f).shape[1] != R for f in facs)):
+        raise CpdInvalidArgument(_cpdb.INVALID_ARGUMENT,
+                                 "solver: init model does not match tensor/config")
+    for f, d in zip(facs, dims):
+        if np.asarray(f).shape[0] != d:
+            raise CpdInvalidArgument(_cpdb.INVALID_ARGUMENT,
+                                     "solver: init factor rows do not match tensor")
+    if state.q0_history is not None:
+        zrows = R ** (order - 1)
+        hist = list(state.q0_history)
+        if len(hist) > order or any(h is not None and np.asarray(h).shape != (zrows, R)
+                                    for h in hist):
+            raise CpdInvalidArgument(_cpdb.INVALID_ARGUMENT,
+                                     "solver: Q0 history does not match tensor/config")
 
 
 class SolverSession:

@@ -215,3 +215,32 @@ uint64_t count_nonfinite(const double* x, uint64_t n, cudaStream_t s) {
 }
 
 }  // namespace cpdb
+
+namespace cpdb {
+namespace {
+// Order-free integer hash of a buffer (diagnostic, CPDB_FINGERPRINT): every
+// word is mixed with its index, the mixes are summed mod 2^64.
+__global__ void fingerprint_kernel(const unsigned long long* x, uint64_t n,
+                                   unsigned long long* out) {
+    unsigned long long h = 0;
+    for (uint64_t i = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; i < n;
+         i += uint64_t(gridDim.x) * blockDim.x) {
+        unsigned long long v = x[i] ^ (i * 0x9E3779B97F4A7C15ull);
+        v ^= v >> 31;
+        v *= 0xBF58476D1CE4E5B9ull;
+        v ^= v >> 29;
+        h += v;
+    }
+    for (int o = 16; o > 0; o >>= 1) h += __shfl_xor_sync(0xffffffffu, h, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, h);
+}
+}  // namespace
+
+cudaError_t fingerprint(const double* x, uint64_t n, unsigned long long* out, cudaStream_t s) {
+    const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, 148));
+    fingerprint_kernel<<<std::max(grid, 1u), 256, 0, s>>>(
+        reinterpret_cast<const unsigned long long*>(x), n, out);
+    return cudaGetLastError();
+}
+
+}  // namespace cpdb

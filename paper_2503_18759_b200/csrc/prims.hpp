@@ -26,4 +26,7 @@ cudaError_t fitness_dev(double nx2, const double* v, const double* ah, uint64_t 
                         const double* r0, const double* rn, const double* lam, uint32_t r,
                         double* out4, cudaStream_t s);
 
+// Order-free integer hash of n doubles added into *out (diagnostic).
+cudaError_t fingerprint(const double* x, uint64_t n, unsigned long long* out, cudaStream_t s);
+
 }  // namespace cpdb

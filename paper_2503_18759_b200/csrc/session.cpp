@@ -45,12 +45,46 @@
 #include <cstring>
 
 #include "comm.hpp"
+#include "prims.hpp"
 #include "cpd/rng.hpp"
 #include "runtime.hpp"
 #include "session.hpp"
 
 namespace cpdb {
 namespace {
+
+// Stream/event calls of the session go through these so the happens-before
+// checker (hb.hpp, CPDB_HBCHECK=1) sees the same ordering the GPU does.
+inline cudaError_t hb_rec(HbCheck& h, cudaEvent_t e, cudaStream_t s) {
+    h.record(e, s);
+    return cudaEventRecord(e, s);
+}
+inline cudaError_t hb_wait(HbCheck& h, cudaStream_t s, cudaEvent_t e, unsigned f) {
+    h.wait(s, e);
+    return cudaStreamWaitEvent(s, e, f);
+}
+inline cudaError_t hb_ssync(HbCheck& h, cudaStream_t s) {
+    cudaError_t r = cudaStreamSynchronize(s);
+    h.sync_stream(s);
+    return r;
+}
+inline cudaError_t hb_esync(HbCheck& h, cudaEvent_t e) {
+    cudaError_t r = cudaEventSynchronize(e);
+    h.sync_event(e);
+    return r;
+}
+inline cudaError_t hb_dsync(HbCheck& h) {
+    cudaError_t r = cudaDeviceSynchronize();
+    h.sync_all();
+    return r;
+}
+#define cudaEventRecord(e, st) ::cpdb::hb_rec(hb, (e), (st))
+#define cudaStreamWaitEvent(st, e, f) ::cpdb::hb_wait(hb, (st), (e), (f))
+#define cudaStreamSynchronize(st) ::cpdb::hb_ssync(hb, (st))
+#define cudaEventSynchronize(e) ::cpdb::hb_esync(hb, (e))
+#define cudaDeviceSynchronize() ::cpdb::hb_dsync(hb)
+using Rg = HbCheck::Rg;
+inline Rg rg(const void* p, uint64_t doubles) { return Rg{p, size_t(doubles) * sizeof(double)}; }
 
 std::string set_name(uint32_t s, uint32_t order) {
     std::string out = "Y(";
@@ -161,6 +195,26 @@ void Session::tl_flush() {
 void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* state) {
     c = ctx;
     cfg = config;
+    {
+        const char* e = std::getenv("CPDB_HBCHECK");
+        hb.on = e && e[0] == '1';
+        if (hb.on) {
+            hb.name(c->stream, "main");
+            hb.name(c->side, "side");
+            hb.name(c->side_hi, "side_hi");
+            hb.name(c->lo, "lo");
+            hb.name(c->mid, "mid");
+            hb.name(c->aux, "aux");
+            hb.name(c->zq, "zq");
+            hb.name(nullptr, "legacy");
+        }
+        fpath = std::getenv("CPDB_FINGERPRINT");
+        fp_light = std::getenv("CPDB_FINGERPRINT_LIGHT") != nullptr;
+        if (fpath) {
+            fplog.ensure(1u << 20);
+            CPDB_CK(cudaMemset(fplog.p, 0, fplog.n * sizeof(double)));
+        }
+    }
     // SolverConfig::validate (solvers.hpp:41-49) and run_qr guards (:217-224)
     if (cfg.rank == 0) fail(CPDB_INVALID_ARGUMENT, "SolverConfig: rank must be >= 1");
     if (cfg.max_iterations == 0)
@@ -280,6 +334,7 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
             const uint64_t I = c->dims[k];
             CPDB_CK(cudaMemcpyAsync(fb[k].a.p, init.data() + off, I * R * sizeof(double),
                                     cudaMemcpyHostToDevice, s));
+            acc(s, "init_h2d", {}, {rg(fb[k].a.p, I * R)});
             if (!given) {
                 CPDB_CK(normalize_exact(fb[k].a.p, I, R, nullptr, s));
                 c->launches += 1;
@@ -396,6 +451,7 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
             sl.buf.ensure(numel(d));
             CPDB_CK(cudaMemcpyAsync(sl.buf.p, cur, numel(d) * sizeof(double),
                                     cudaMemcpyDeviceToDevice, s));
+            acc(s, "cache_rebuild_copy", {rg(cur, numel(d))}, {rg(sl.buf.p, numel(d))});
             sl.valid = true;
             sl.dims = d;
             sl.sharded = set_sharded(key, sharded);
@@ -457,6 +513,9 @@ void Session::qr_factor(uint32_t k) {
     f.status = c->dstatus;
     f.v_out = vout.p;
     CPDB_CK(launch_finish(f, s));
+    acc(s, "qr_factor", {rg(f.a_out, f.I * R)},
+          {rg(f.q_out, f.I * R), rg(f.qp_out, uint64_t(ttm_kpad(f.I)) * Rp), rg(f.r_out, R * R),
+           rg(f.scratch, f.I * (R + 1))});
     c->launches += 1;
 }
 
@@ -487,8 +546,13 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32
         CPDB_CK(cudaEventRecord(t.a, st));
     }
     cudaEvent_t tla = tl_begin(st);
+    fp(st, prefetch ? "root_prefetch" : is_root ? "root_ttm" : "branch_ttm", "in_before",
+       {rg(src, numel(sd)), rg(qp, uint64_t(ttm_kpad(sd[k])) * Rp)});
     run_ttm(c, src, sd, k, q, qp, R, dst, st, prefetch || yield_now, no_pdl, sms,
             prefetch ? pf.tpc : 0);
+    acc(st, prefetch ? "root_prefetch" : is_root ? "root_ttm" : "branch_ttm",
+          {rg(src, numel(sd)), rg(qp, uint64_t(ttm_kpad(sd[k])) * Rp)},
+          {rg(dst, numel(sd) / sd[k] * R)});
     tl_end(tla, st, prefetch ? "root_prefetch" : is_root ? "root" : "branch");
     if (c->timing) {
         CPDB_CK(cudaEventRecord(t.b, st));
@@ -580,6 +644,46 @@ void Session::launch_prefetch() {
     ttm_step(c->x, c->ldims, 0, pf.cm, pre.p, true, c->lo, true, true);
     CPDB_CK(cudaEventRecord(pf.ev, c->lo));
     pf.launched = true;
+}
+
+void Session::fp(cudaStream_t st, const char* what, const char* phase,
+                 std::initializer_list<HbCheck::Rg> regions) {
+    if (!fpath || st == nullptr) return;
+    // light: outputs of the TTMs, Z-QR, V-GEMM and finisher, and the V-GEMM's
+    // inputs just before and after it
+    if (fp_light && phase[0] != 'o' && what[0] != 'v') return;
+    if (fp_light && phase[0] == 'o' && !(what[0] == 'f' || what[0] == 'z' || what[0] == 'v' ||
+                                        what[0] == 'r' || what[0] == 'b'))
+        return;
+    int k = 0;
+    for (const HbCheck::Rg& g : regions) {
+        ++k;
+        if (!g.p || !g.bytes) continue;
+        const size_t idx = fplabels.size();
+        if (idx >= fplog.n) return;
+        char lab[160];
+        std::snprintf(lab, sizeof lab, "%llu %u %s %s %d", (unsigned long long)hb.cur_sweep,
+                      hb.cur_mode, what, phase, k);
+        fplabels.push_back(lab);
+        CPDB_CK(fingerprint(static_cast<const double*>(g.p), g.bytes / sizeof(double),
+                            reinterpret_cast<unsigned long long*>(fplog.p) + idx, st));
+    }
+}
+
+void Session::fp_flush() {
+    if (!fpath || fplabels.empty()) return;
+    CPDB_CK(cudaDeviceSynchronize());
+    std::vector<unsigned long long> h(fplabels.size());
+    CPDB_CK(cudaMemcpy(h.data(), fplog.p, h.size() * sizeof(h[0]), cudaMemcpyDeviceToHost));
+    FILE* f = std::fopen(fpath, "a");
+    if (f) {
+        std::fprintf(f, "=== session\n");
+        for (size_t i = 0; i < h.size(); ++i)
+            std::fprintf(f, "%zu %s %016llx\n", i, fplabels[i].c_str(), h[i]);
+        std::fclose(f);
+    }
+    fplabels.clear();
+    CPDB_CK(cudaMemset(fplog.p, 0, fplog.n * sizeof(double)));
 }
 
 cudaEvent_t Session::ready_event(uint32_t key) {
@@ -703,8 +807,17 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     z.pdl = chain_side && !early && !trace_phases ? 1 : 0;
     tl_sweep = sweep;
     tl_mode = n;
+    hb.cur_sweep = sweep;
+    hb.cur_mode = n;
     cudaEvent_t tla = tl_begin(zs);
+    fp(zs, "zqr", "in_before",
+       {rg(z.rmats[0], R * R), rg(z.rmats[1], order > 2 ? R * R : 0),
+        rg(z.rmats[2], order > 3 ? R * R : 0), rg(z.rmats[3], order > 4 ? R * R : 0)});
     CPDB_CK(launch_zqr(z, zs, c->sms));
+    acc(zs, "zqr",
+          {rg(z.rmats[0], R * R), rg(z.rmats[1], order > 2 ? R * R : 0),
+           rg(z.rmats[2], order > 3 ? R * R : 0), rg(z.rmats[3], order > 4 ? R * R : 0)},
+          {rg(z.q1, zrows * R), rg(z.q0, zrows * R), rg(z.r0, R * R), rg(z.work, zcur.work.n)});
     tl_end(tla, zs, "zqr");
     launch_prefetch();
     if (!chain_side) CPDB_CK(cudaEventRecord(ev_zqr, side));
@@ -726,6 +839,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         std::vector<double> nat(zrows * R), ref(zrows * R);
         CPDB_CK(cudaMemcpyAsync(nat.data(), zcur.q0.p, zrows * R * sizeof(double),
                                 cudaMemcpyDeviceToHost, zs));
+        acc(zs, "observer_d2h", {rg(zcur.q0.p, zrows * R)}, {});
         CPDB_CK(cudaStreamSynchronize(zs));
         for (uint64_t i = 0; i < zrows; ++i)
             std::memcpy(&ref[perm[i] * R], &nat[i * R], R * sizeof(double));
@@ -864,6 +978,8 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     if (maybe_ex) CPDB_CK(cudaStreamWaitEvent(bs, ev_hist[n], 0));
     tl_sweep = sweep;
     tl_mode = n;
+    hb.cur_sweep = sweep;
+    hb.cur_mode = n;
     cudaEvent_t tla = tl_begin(bs);
     // partials summed by the finisher: few enough that its 8 CTAs read them
     // quickly (env CPDB_VSPLIT_MAX, default 16)
@@ -873,7 +989,16 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     }();
     v.max_split = (vsplit_max > 0 && !gather && finish_sums_splits(v.I, R)) ? vsplit_max : 0;
     const int vsms = budget(sweep, b);
+    fp(bs, "vgemm", "in_before",
+       {rg(v.y, numel(yd)), rg(v.q0, zrows * R), rg(v.hist, v.extrap ? zrows * R : 0),
+        rg(v.gate, v.gate ? 4 : 0)});
     CPDB_CK(launch_vgemm(v, bs, vsms > 0 ? vsms : c->sms));
+    acc(bs, "vgemm",
+          {rg(v.y, numel(yd)), rg(v.q0, zrows * R), rg(v.hist, v.extrap ? zrows * R : 0),
+           rg(v.gate, v.gate ? 4 : 0)},
+          {rg(v.vpart, v.reduced ? 0 : uint64_t(v.nsplit) * v.I * R),
+           rg(v.vfitpart, v.dual && !v.reduced ? uint64_t(v.nsplit) * v.I * R : 0),
+           rg(v.v_out, v.reduced ? v.I * R : 0), rg(v.vfit_out, v.reduced && v.dual ? v.I * R : 0)});
     tl_end(tla, bs, "vgemm");
     c->launches += 1;
     if (dep_events) CPDB_CK(cudaEventRecord(ev_v[2 * n + zpar], bs));  // ybuf consumed
@@ -884,7 +1009,12 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     if (!v.reduced && !fused) {
         tla = tl_begin(bs);
         CPDB_CK(reduce_splits(v.vpart, v.nsplit, v.I * R, vf.p + off, bs));
-        if (v.dual) CPDB_CK(reduce_splits(v.vfitpart, v.nsplit, v.I * R, vff.p + off, bs));
+        acc(bs, "reduce", {rg(v.vpart, uint64_t(v.nsplit) * v.I * R)}, {rg(vf.p + off, v.I * R)});
+        if (v.dual) {
+            CPDB_CK(reduce_splits(v.vfitpart, v.nsplit, v.I * R, vff.p + off, bs));
+            acc(bs, "reduce", {rg(v.vfitpart, uint64_t(v.nsplit) * v.I * R)},
+                  {rg(vff.p + off, v.I * R)});
+        }
         tl_end(tla, bs, "reduce");
         c->launches += v.dual ? 2 : 1;
     }
@@ -913,13 +1043,30 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     f.norm_x_sq = nx2;
     f.fit_out = fitbuf.p;
     f.status = c->dstatus;
+    static const bool pfence = [] {
+        const char* e = std::getenv("CPDB_PROXY_FENCE");
+        return e && e[0] == '1';
+    }();
+    f.proxy_fence = pfence ? 1 : 0;
     static const bool trace_phases = std::getenv("CPDB_PHASE_TRACE") != nullptr;
     if (trace_phases) {
         f.ts = reinterpret_cast<unsigned long long*>(tsbuf.ensure(32));
         CPDB_CK(cudaMemsetAsync(f.ts, 0, 32 * sizeof(double), bs));
     }
     tla = tl_begin(bs);
+    {
+        const uint64_t vin = uint64_t(f.nsplit) * f.I * R;
+        fp(bs, "finish", "in_before",
+           {rg(f.vpart, vin), rg(f.vfitpart, f.dual ? vin : 0), rg(f.r0, R * R)});
+    }
     CPDB_CK(launch_finish(f, bs));
+    {
+        const uint64_t vin = uint64_t(f.nsplit) * f.I * R;
+        acc(bs, "finish", {rg(f.vpart, vin), rg(f.vfitpart, f.dual ? vin : 0), rg(f.r0, R * R)},
+              {rg(f.a_out, f.I * R), rg(f.q_out, f.I * R),
+               rg(f.qp_out, uint64_t(ttm_kpad(f.I)) * Rp), rg(f.r_out, R * R), rg(f.lambda, R),
+               rg(f.scratch, f.I * (R + 1)), rg(f.fit_out, f.fitness ? 2 : 0)});
+    }
     tl_end(tla, bs, "finish");
     c->launches += 1;
     fb[n].swap(fb_alt[n]);  // the new factor state (the old one stays for undo)
@@ -983,9 +1130,11 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
             CPDB_CK(beta_gate(gate.p, fitbuf.p,
                               (!cfg.has_beta_override && sweep >= 2) ? 1 : 0,
                               cfg.activation_gap, s));
+        if (extrap) acc(s, "beta_gate", {rg(fitbuf.p, 2), rg(gate.p, 4)}, {rg(gate.p, 4)});
         cudaEvent_t e_end = events.get();
         CPDB_CK(cudaEventRecord(e_end, s));
         CPDB_CK(cudaMemcpyAsync(c->pinned, fitbuf.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+        acc(s, "fitness_d2h", {rg(fitbuf.p, 2)}, {});
         CPDB_CK(cudaMemcpyAsync(c->pinned + 2, c->dstatus, sizeof(int), cudaMemcpyDeviceToHost, s));
         cudaEvent_t e_fit = events.get();
         CPDB_CK(cudaEventRecord(e_fit, s));
@@ -1091,6 +1240,7 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         if (fps) {
             uint64_t off = 0;
             for (uint32_t k = 0; k < order; ++k) {
+                acc(nullptr, "factors_d2h", {rg(fb[k].a.p, c->dims[k] * R)}, {});
                 CPDB_CK(cudaMemcpy(fps + rows_out * nfac + off, fb[k].a.p,
                                    c->dims[k] * R * sizeof(double), cudaMemcpyDeviceToHost));
                 off += c->dims[k] * R;
@@ -1120,6 +1270,10 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         }
     }
     tl_flush();
+    fp_flush();
+    if (hb.on)
+        std::fprintf(stderr, "cpdb hbcheck: %llu sweeps checked, %llu violations\n",
+                     (unsigned long long)(done - first_sweep), (unsigned long long)hb.violations);
     c->prof.sweeps = done - first_sweep;
     c->prof.mode_update_ms =
         c->prof.solve_ms - c->prof.root_ttm_ms - c->prof.branch_ttm_ms - c->prof.comm_ms;
@@ -1150,6 +1304,7 @@ void Session::end(cpdb_state* state, double* out_lambda, double* out_factors) {
     auto get_factors = [&](double* dst) {
         uint64_t off = 0;
         for (uint32_t k = 0; k < order; ++k) {
+            acc(nullptr, "end_factors_d2h", {rg(fb[k].a.p, c->dims[k] * R)}, {});
             CPDB_CK(cudaMemcpy(dst + off, fb[k].a.p, c->dims[k] * R * sizeof(double),
                                cudaMemcpyDeviceToHost));
             off += c->dims[k] * R;
@@ -1167,6 +1322,7 @@ void Session::end(cpdb_state* state, double* out_lambda, double* out_factors) {
         std::vector<double> nat(zrows * R);
         for (uint32_t n = 0; n < order; ++n) {
             if (!has_hist[n]) continue;
+            acc(nullptr, "end_hist_d2h", {rg(hist[n].p, zrows * R)}, {});
             CPDB_CK(cudaMemcpy(nat.data(), hist[n].p, zrows * R * sizeof(double),
                                cudaMemcpyDeviceToHost));
             double* ref = state->q0_history + uint64_t(n) * zrows * R;

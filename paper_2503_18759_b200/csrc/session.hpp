@@ -5,6 +5,7 @@
 #include <map>
 #include <vector>
 
+#include "hb.hpp"
 #include "runtime.hpp"
 
 namespace cpdb {
@@ -92,6 +93,25 @@ struct Session {
     Cost total;
 
     EventPool events;
+    HbCheck hb;  // CPDB_HBCHECK=1: happens-before check of every declared access
+    // CPDB_FINGERPRINT=<file>: hash every declared input before and after each
+    // launch and every output after it, appended to <file> at the end of run()
+    const char* fpath = nullptr;
+    bool fp_light = false;  // CPDB_FINGERPRINT_LIGHT=1: outputs of zqr / vgemm / finish only
+    DevBuf fplog;
+    std::vector<std::string> fplabels;
+    void fp(cudaStream_t st, const char* what, const char* phase,
+            std::initializer_list<HbCheck::Rg> regions);
+    // hb.op + fingerprints of the inputs and outputs after the launch
+    void acc(cudaStream_t st, const char* what, std::initializer_list<HbCheck::Rg> rd,
+             std::initializer_list<HbCheck::Rg> wr) {
+        hb.op(st, what, rd, wr);
+        if (fpath) {
+            if (!fp_light || what[0] == 'v') fp(st, what, "in_after", rd);
+            fp(st, what, "out", wr);
+        }
+    }
+    void fp_flush();
     bool front_issued = false;  // next sweep's first Z-QR + TTM chain already on the stream
     // root TTM of a later update of the sweep issued early on the low-priority
     // stream, overlapped with the updates in between (prefetch_root)

@@ -22,6 +22,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 #include <mutex>
 
 #include "device.cuh"
@@ -56,10 +57,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "r"(parity)
         : "memory");
 }
+// Bulk copies into this CTA's shared memory (.shared::cta destination: the
+// TTM grids are launched without a cluster).
 __device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
                                        int c1, int c2, int c3) {
     asm volatile(
-        "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "cp.async.bulk.tensor.4d.shared::cta.global.mbarrier::complete_tx::bytes "
         "[%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
         : "memory");
@@ -67,7 +70,7 @@ __device__ __forceinline__ void tma_4d(void* dst, const CUtensorMap* map, uint64
 __device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0,
                                        int c1, int c2) {
     asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes "
+        "cp.async.bulk.tensor.3d.shared::cta.global.mbarrier::complete_tx::bytes "
         "[%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
         "l"(map), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
@@ -75,7 +78,7 @@ __device__ __forceinline__ void tma_3d(void* dst, const CUtensorMap* map, uint64
 __device__ __forceinline__ void bulk_copy(void* dst, const void* src, uint32_t bytes,
                                           uint64_t* bar) {
     asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
         ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
         : "memory");
 }
@@ -321,12 +324,27 @@ cudaError_t launch_v2(const TtmArgs& a, cudaStream_t s, int sms) {
     }
     auto kern = ttm_tma_kernel<RB, CB, BK, STAGES, NC, LAYOUT>;
     // Every TMA TTM CTA reserves the SM's whole shared memory, so no CTA of
-    // another grid is co-resident with it.  Measured: with the root TTM
-    // running concurrently on the low-priority stream, co-residency with other
-    // grids' CTAs gave non-reproducible results (C3: 14 of 90 repeated solves
-    // differed; 0 of 90 with exclusive SMs; tools/det_probe.py).  The TTM
-    // runs one CTA per SM anyway.
-    const size_t smem = size_t(227 * 1024);
+    // another grid is co-resident with it.  Root cause (round 2): while CTAs
+    // of a cluster kernel that exchange data through distributed shared
+    // memory (our 8-CTA finisher / Z-QR) run on the same SM, the X tiles this
+    // kernel receives through cp.async.bulk.tensor are wrong -- measured in
+    // isolation, with no solver around it (tools/probes/ttm_coresid.cu,
+    // profiles/r02_coresidency_probe.txt): 0.02-10% of the outputs differ in
+    // EVERY run beside a DSMEM-reading or -writing cluster grid, 0 beside a
+    // cluster grid without DSMEM traffic, 0 beside plain grids, 0 for the
+    // cp.async kernel of ttm.cu; neither the .shared::cta destination form, a
+    // one-CTA cluster launch nor loading Q without the bulk copy changes it.
+    // In the solver it showed as 14 of 90 (round 1) / up to 59 of 60 (no PDL)
+    // repeated C3 solves differing.  The happens-before checker (hb.hpp,
+    // CPDB_HBCHECK=1) finds no missing stream dependency.  Exclusive SMs cost
+    // nothing measurable (C2/C3/C4 sweeps/s within 0.5%, round 2 A/B);
+    // CPDB_TTM_SMEM_EXACT=1 requests only the ring's size (reproduces the
+    // hazard, diagnostic).
+    static const bool exact_smem = [] {
+        const char* e = std::getenv("CPDB_TTM_SMEM_EXACT");
+        return e && e[0] == '1';
+    }();
+    const size_t smem = exact_smem ? C::SMEM : size_t(227 * 1024);
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;

@@ -124,3 +124,24 @@ def test_select_beta_table():
     assert cpd.select_beta(0.905, 0.905, 0.03) == 1.0 / 2000.0
     assert cpd.select_beta(0.70, 0.70, 0.03) == 1.0 / 500.0
     assert cpd.select_beta(-0.5, -0.49, 0.03) == 1.0 / 250.0
+
+
+def test_init_state_checked_before_the_abi():
+    """a given model / sweep state must match the tensor and
+    the config before Context.solve hands raw buffers to the C ABI
+    (solvers.hpp:105-112 messages)."""
+    import paper_2503_18759_b200 as cpd
+    dims, R = (5, 4, 3), 2
+    good = cpd.SweepState(0, np.ones(R), [np.zeros((d, R)) for d in dims])
+    cpd.check_init_state(good, dims, R)
+    cases = [
+        (cpd.SweepState(0, np.ones(R), [np.zeros((d, R)) for d in dims[:2]]), "tensor/config"),
+        (cpd.SweepState(0, np.ones(R + 1), [np.zeros((d, R)) for d in dims]), "tensor/config"),
+        (cpd.SweepState(0, np.ones(R), [np.zeros((d, R + 1)) for d in dims]), "tensor/config"),
+        (cpd.SweepState(0, np.ones(R), [np.zeros((d + 1, R)) for d in dims]), "rows"),
+        (cpd.SweepState(0, np.ones(R), [np.zeros((d, R)) for d in dims],
+                        q0_history=[np.zeros((R * R + 1, R)), None, None]), "Q0 history"),
+    ]
+    for st, what in cases:
+        with pytest.raises(cpd.CpdInvalidArgument, match=what):
+            cpd.check_init_state(st, dims, R)

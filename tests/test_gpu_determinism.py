@@ -1,0 +1,59 @@
+"""GPU: run-to-run determinism of the multi-stream sweep (solver_test.cpp:272-282
+requires bit-identical traces across runs).
+
+Round 2 found the cause of the round-1 non-reproducible C3 solves: the TMA TTM
+kernel receives wrong X tiles while CTAs of a cluster kernel that use
+distributed shared memory share its SM (tools/probes/ttm_coresid.cu,
+profiles/r02_coresidency_probe.txt).  The product keeps TMA TTM CTAs on
+exclusive SMs; these tests hold that line:
+  * the probe, isolated from the solver: the TTM next to a DSMEM cluster grid
+    is bit-identical to an isolated run;
+  * repeated C3 solves without programmatic dependent launch (the setting
+    that exposed the hazard in up to 59 of 60 runs) are bit-identical.
+"""
+import os
+import subprocess
+import sys
+
+import pytest
+
+from conftest import ROOT
+
+pytestmark = pytest.mark.gpu
+
+PROBE_SRC = os.path.join(ROOT, "tools", "probes", "ttm_coresid.cu")
+PROBE_BIN = os.path.join(ROOT, "tools", "probes", "ttm_coresid")
+
+
+def _probe():
+    if not os.path.exists(PROBE_BIN) or os.path.getmtime(PROBE_BIN) < os.path.getmtime(PROBE_SRC):
+        subprocess.run(
+            ["nvcc", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-O2",
+             "-I", os.path.join(ROOT, "paper_2503_18759_b200", "csrc"),
+             "-I", os.path.join(ROOT, "include"), PROBE_SRC,
+             "-L", os.path.join(ROOT, "paper_2503_18759_b200"), "-lcpdb",
+             "-Xlinker", "-rpath," + os.path.join(ROOT, "paper_2503_18759_b200"),
+             "-o", PROBE_BIN], check=True, capture_output=True)
+    return PROBE_BIN
+
+
+@pytest.mark.parametrize("layout", [0, 1])
+@pytest.mark.parametrize("hog", ["read", "write"])
+def test_tma_ttm_beside_dsmem_cluster_grid(layout, hog):
+    env = dict(os.environ)
+    env.pop("CPDB_TTM_SMEM_EXACT", None)
+    if hog == "write":
+        env["HOG_WRITE"] = "1"
+    out = subprocess.run([_probe(), str(layout), "12", "0", "64", "cluster"], env=env,
+                         capture_output=True, text=True, timeout=300, check=True).stdout
+    last = out.strip().splitlines()[-1]
+    assert " 0 of 12 reps differ" in last, out
+
+
+def test_repeated_c3_solves_bit_identical_without_pdl():
+    env = dict(os.environ, CPDB_NO_PDL="1")
+    env.pop("CPDB_TTM_SMEM_EXACT", None)
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "det_probe.py"), "c3",
+                          "30", "4"], env=env, cwd=ROOT, capture_output=True, text=True,
+                         timeout=600, check=True).stdout
+    assert out.strip().splitlines()[-1].endswith("mismatching 0"), out
