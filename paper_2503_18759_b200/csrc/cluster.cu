@@ -322,9 +322,6 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
         *a.status = 2;
     }
     CPDB_TS(14);
-    // the packed Q_n is read by later TTM grids through the async proxy
-    // (cp.async.bulk)
-    if (a.proxy_fence) asm volatile("fence.proxy.async.global;" ::: "memory");
     cl.sync();  // rank 0's smem must outlive the other ranks' DSMEM reads
     CPDB_TS(15);
 }

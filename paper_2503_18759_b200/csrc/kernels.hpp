@@ -165,7 +165,6 @@ struct FinishArgs {
     double* fit_out;       // [fitness, raw]
     int* status;           // 1 singular R0 (+col<<8), 2 Cholesky breakdown
     unsigned long long* ts;  // optional phase timestamps (profiling)
-    int proxy_fence;       // fence.proxy.async after the packed-Q stores
 };
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s);
 // true when launch_finish(I, R) sums FinishArgs::nsplit V partials itself

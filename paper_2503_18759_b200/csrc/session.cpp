@@ -1043,11 +1043,6 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     f.norm_x_sq = nx2;
     f.fit_out = fitbuf.p;
     f.status = c->dstatus;
-    static const bool pfence = [] {
-        const char* e = std::getenv("CPDB_PROXY_FENCE");
-        return e && e[0] == '1';
-    }();
-    f.proxy_fence = pfence ? 1 : 0;
     static const bool trace_phases = std::getenv("CPDB_PHASE_TRACE") != nullptr;
     if (trace_phases) {
         f.ts = reinterpret_cast<unsigned long long*>(tsbuf.ensure(32));
