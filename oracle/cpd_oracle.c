@@ -13,8 +13,10 @@
 #include <stdarg.h>
 #include <stdio.h>
 #include <stdlib.h>
+#include <pthread.h>
 #include <string.h>
 #include <time.h>
+#include <unistd.h>
 
 static char g_err[512];
 
@@ -37,7 +39,7 @@ static void* xcalloc(size_t n, size_t sz) {
     return p;
 }
 
-static double* dup(const double* src, size_t n) {
+static double* dupd(const double* src, size_t n) {
     double* p = (double*)xcalloc(n, sizeof(double));
     memcpy(p, src, n * sizeof(double));
     return p;
@@ -108,38 +110,121 @@ static uint64_t prod(const uint64_t* d, uint32_t from, uint32_t to) {
     return p;
 }
 
+/* Static parallel-for over [0, n) on host threads (CPDO_THREADS, default: the
+ * online cores).  The oracle splits OUTPUT elements between threads only:
+ * every element keeps the reference's operation order, so the result is
+ * bit-identical to the serial loops (tests/test_oracle.py checks it against
+ * oracle/_ref). */
+typedef void (*range_fn)(void* ctx, uint64_t begin, uint64_t end);
+typedef struct {
+    range_fn fn;
+    void* ctx;
+    uint64_t begin, end;
+} range_job;
+
+static void* range_run(void* p) {
+    range_job* j = (range_job*)p;
+    j->fn(j->ctx, j->begin, j->end);
+    return NULL;
+}
+
+static int oracle_threads(void) {
+    static int n = 0;
+    if (n == 0) {
+        const char* e = getenv("CPDO_THREADS");
+        n = e ? atoi(e) : (int)sysconf(_SC_NPROCESSORS_ONLN);
+        if (n < 1) n = 1;
+        if (n > 64) n = 64;
+    }
+    return n;
+}
+
+static void par_for(uint64_t n, uint64_t min_per_thread, range_fn fn, void* ctx) {
+    int nt = oracle_threads();
+    if ((uint64_t)nt > n / (min_per_thread ? min_per_thread : 1)) nt = (int)(n / (min_per_thread ? min_per_thread : 1));
+    if (nt <= 1) {
+        fn(ctx, 0, n);
+        return;
+    }
+    pthread_t th[64];
+    range_job jobs[64];
+    for (int t = 0; t < nt; ++t) {
+        jobs[t].fn = fn;
+        jobs[t].ctx = ctx;
+        jobs[t].begin = n * (uint64_t)t / (uint64_t)nt;
+        jobs[t].end = n * (uint64_t)(t + 1) / (uint64_t)nt;
+    }
+    for (int t = 1; t < nt; ++t) pthread_create(&th[t], NULL, range_run, &jobs[t]);
+    range_run(&jobs[0]);
+    for (int t = 1; t < nt; ++t) pthread_join(th[t], NULL);
+}
+
 /* tensor.hpp:288-315 with the loops of detail::gemm (:137-149) and
  * detail::gemm_bt (:153-165): every output element accumulates its K products
  * in ascending contraction index, starting from +0. */
+typedef struct {
+    const double *t, *b;
+    double* out;
+    uint64_t outer, inner, ext, rows, jc, nj;
+} ttm_ctx;
+
+static void ttm_rows_range(void* p, uint64_t i0, uint64_t i1) { /* gemm_bt, tensor.hpp:153-165 */
+    const ttm_ctx* c = (const ttm_ctx*)p;
+    for (uint64_t i = i0; i < i1; ++i) {
+        const double* xrow = c->t + i * c->ext;
+        for (uint64_t r = 0; r < c->rows; ++r) {
+            const double* brow = c->b + r * c->ext;
+            double acc = 0.0;
+            for (uint64_t k = 0; k < c->ext; ++k) acc += xrow[k] * brow[k];
+            c->out[i * c->rows + r] = acc;
+        }
+    }
+}
+
+static void ttm_items_range(void* p, uint64_t a, uint64_t z) { /* gemm, tensor.hpp:137-149 */
+    const ttm_ctx* c = (const ttm_ctx*)p;
+    /* item = (o, j-chunk): the rows x chunk block of Y stays in cache while
+     * the slab X[o][:][chunk] streams once (the reference's r-outer loop
+     * would re-read it per r); each Y element still sums over k ascending */
+    for (uint64_t it = a; it < z; ++it) {
+        const uint64_t o = it / c->nj;
+        const uint64_t j0 = (it % c->nj) * c->jc;
+        const uint64_t j1 = j0 + c->jc < c->inner ? j0 + c->jc : c->inner;
+        const double* xs = c->t + o * c->ext * c->inner;
+        double* ys = c->out + o * c->rows * c->inner;
+        for (uint64_t r = 0; r < c->rows; ++r)
+            for (uint64_t j = j0; j < j1; ++j) ys[r * c->inner + j] = 0.0;
+        for (uint64_t k = 0; k < c->ext; ++k) {
+            const double* xrow = xs + k * c->inner;
+            for (uint64_t r = 0; r < c->rows; ++r) {
+                const double w = c->b[r * c->ext + k];
+                double* yrow = ys + r * c->inner;
+                for (uint64_t j = j0; j < j1; ++j) yrow[j] += w * xrow[j];
+            }
+        }
+    }
+}
+
+/* Every output element accumulates its ext products in ascending contraction
+ * index from +0 (the reference's order); work items are (o, j-chunk) so a
+ * contraction of the leading mode (outer == 1) still spreads. */
 static void ttm_raw(const double* t, const uint64_t* dims, uint32_t order, const double* b,
                     uint64_t rows, uint32_t mode, double* out) {
-    const uint64_t outer = prod(dims, 0, mode), inner = prod(dims, mode + 1, order);
-    const uint64_t ext = dims[mode];
-    if (inner == 1) {
-        for (uint64_t i = 0; i < outer; ++i) {
-            const double* xrow = t + i * ext;
-            for (uint64_t r = 0; r < rows; ++r) {
-                const double* brow = b + r * ext;
-                double acc = 0.0;
-                for (uint64_t k = 0; k < ext; ++k) acc += xrow[k] * brow[k];
-                out[i * rows + r] = acc;
-            }
-        }
+    ttm_ctx c;
+    c.t = t;
+    c.b = b;
+    c.out = out;
+    c.outer = prod(dims, 0, mode);
+    c.inner = prod(dims, mode + 1, order);
+    c.ext = dims[mode];
+    c.rows = rows;
+    c.jc = 256;
+    c.nj = (c.inner + c.jc - 1) / c.jc;
+    if (c.inner == 1) {
+        par_for(c.outer, 256, ttm_rows_range, &c);
         return;
     }
-    for (uint64_t o = 0; o < outer; ++o) {
-        const double* xs = t + o * ext * inner;
-        double* ys = out + o * rows * inner;
-        memset(ys, 0, rows * inner * sizeof(double));
-        for (uint64_t r = 0; r < rows; ++r) {
-            double* yrow = ys + r * inner;
-            for (uint64_t k = 0; k < ext; ++k) {
-                const double w = b[r * ext + k];
-                const double* xrow = xs + k * inner;
-                for (uint64_t j = 0; j < inner; ++j) yrow[j] += w * xrow[j];
-            }
-        }
-    }
+    par_for(c.outer * c.nj, 4, ttm_items_range, &c);
 }
 
 int cpdo_ttm(const double* t, const uint64_t* dims, uint32_t order, const double* b,
@@ -150,28 +235,58 @@ int cpdo_ttm(const double* t, const uint64_t* dims, uint32_t order, const double
 }
 
 /* tensor.hpp:217-250: row = index of `mode`; column runs over the other modes
- * with the EARLIEST mode fastest. */
-int cpdo_unfold(const double* t, const uint64_t* dims, uint32_t order, uint32_t mode,
-                double* out) {
-    if (mode >= order) return fail(CPDO_INVALID_ARGUMENT, "unfold: mode out of range");
-    const uint64_t total = prod(dims, 0, order), cols = total / dims[mode];
-    uint64_t weight[CPDO_MAX_ORDER] = {0}, w = 1;
-    for (uint32_t k = 0; k < order; ++k)
-        if (k != mode) {
-            weight[k] = w;
-            w *= dims[k];
-        }
-    uint64_t idx[CPDO_MAX_ORDER] = {0};
-    for (uint64_t lin = 0; lin < total; ++lin) {
-        uint64_t col = 0;
-        for (uint32_t k = 0; k < order; ++k)
-            if (k != mode) col += idx[k] * weight[k];
-        out[idx[mode] * cols + col] = t[lin];
-        for (uint32_t k = order; k-- > 0;) {
-            if (++idx[k] < dims[k]) break;
+ * with the EARLIEST mode fastest.  (A permutation: threads take ranges of
+ * the input, the column index is updated incrementally.) */
+typedef struct {
+    const double* t;
+    double* out;
+    const uint64_t* dims;
+    uint64_t weight[CPDO_MAX_ORDER];
+    uint64_t cols;
+    uint32_t order, mode;
+} unfold_ctx;
+
+static void unfold_range(void* p, uint64_t lin0, uint64_t lin1) {
+    const unfold_ctx* c = (const unfold_ctx*)p;
+    uint64_t idx[CPDO_MAX_ORDER] = {0}, rem = lin0, col = 0;
+    for (uint32_t k = c->order; k-- > 0;) {
+        idx[k] = rem % c->dims[k];
+        rem /= c->dims[k];
+        if (k != c->mode) col += idx[k] * c->weight[k];
+    }
+    for (uint64_t lin = lin0; lin < lin1; ++lin) {
+        c->out[idx[c->mode] * c->cols + col] = c->t[lin];
+        for (uint32_t k = c->order; k-- > 0;) {
+            const uint64_t w = k == c->mode ? 0 : c->weight[k];
+            if (++idx[k] < c->dims[k]) {
+                col += w;
+                break;
+            }
+            col -= (c->dims[k] - 1) * w;
             idx[k] = 0;
         }
     }
+}
+
+int cpdo_unfold(const double* t, const uint64_t* dims, uint32_t order, uint32_t mode,
+                double* out) {
+    if (mode >= order) return fail(CPDO_INVALID_ARGUMENT, "unfold: mode out of range");
+    unfold_ctx c;
+    memset(&c, 0, sizeof c);
+    c.t = t;
+    c.out = out;
+    c.dims = dims;
+    c.order = order;
+    c.mode = mode;
+    const uint64_t total = prod(dims, 0, order);
+    c.cols = total / dims[mode];
+    uint64_t w = 1;
+    for (uint32_t k = 0; k < order; ++k)
+        if (k != mode) {
+            c.weight[k] = w;
+            w *= dims[k];
+        }
+    par_for(total, 1u << 16, unfold_range, &c);
     return CPDO_OK;
 }
 
@@ -181,7 +296,7 @@ int cpdo_khatri_rao(const double* const* mats, const uint64_t* rows, uint32_t co
     if (count == 0) return fail(CPDO_INVALID_ARGUMENT, "khatri_rao: empty list");
     uint64_t cur_rows = rows[0], total = 1;
     for (uint32_t i = 0; i < count; ++i) total *= rows[i];
-    double* cur = dup(mats[0], rows[0] * cols);
+    double* cur = dupd(mats[0], rows[0] * cols);
     for (uint32_t li = 1; li < count; ++li) {
         const double* m = mats[li];
         const uint64_t mr = rows[li];
@@ -202,55 +317,105 @@ int cpdo_khatri_rao(const double* const* mats, const uint64_t* rows, uint32_t co
 /* linalg.hpp:39-99: Householder with alpha = -sign(x_k) ||x||, Q accumulated
  * backwards from the first n columns of I, then rows of R / columns of Q
  * flipped so diag(R) >= 0.  A zero column leaves its reflector empty. */
+/* out (cols x rows) = in (rows x cols)^T, tiled, threads over row tiles */
+typedef struct {
+    const double* in;
+    double* out;
+    uint64_t rows, cols;
+} tp_ctx;
+
+static void tp_range(void* p, uint64_t t0, uint64_t t1) {
+    const tp_ctx* c = (const tp_ctx*)p;
+    for (uint64_t t = t0; t < t1; ++t) {
+        const uint64_t i0 = t * 64, i1 = i0 + 64 < c->rows ? i0 + 64 : c->rows;
+        for (uint64_t j0 = 0; j0 < c->cols; j0 += 64) {
+            const uint64_t j1 = j0 + 64 < c->cols ? j0 + 64 : c->cols;
+            for (uint64_t i = i0; i < i1; ++i)
+                for (uint64_t j = j0; j < j1; ++j) c->out[j * c->rows + i] = c->in[i * c->cols + j];
+        }
+    }
+}
+
+static void transpose_par(const double* in, uint64_t rows, uint64_t cols, double* out) {
+    tp_ctx c = {in, out, rows, cols};
+    par_for((rows + 63) / 64, 64, tp_range, &c);
+}
+
+/* The QR works on a COLUMN-MAJOR copy: each column is contiguous, so the
+ * column loop of linalg.hpp:62-67 (s_j = beta * sum_i v_i w_ij ascending in
+ * i, then w_ij -= s_j v_i) streams one contiguous column per j, and threads
+ * take disjoint columns.  Same operations in the same order per column ->
+ * bit-identical to the reference (tests/test_oracle.py checks it). */
+typedef struct {
+    double* wt; /* n columns of length m */
+    const double* v;
+    uint64_t m, k, j_lo;
+    double beta;
+} refl_ctx;
+
+static void refl_range(void* p, uint64_t c0, uint64_t c1) {
+    const refl_ctx* c = (const refl_ctx*)p;
+    for (uint64_t jj = c0; jj < c1; ++jj) {
+        double* col = c->wt + (c->j_lo + jj) * c->m;
+        const double* v = c->v - c->k;  /* v[i] for i >= k */
+        double s = 0.0;
+        for (uint64_t i = c->k; i < c->m; ++i) s += v[i] * col[i];
+        s *= c->beta;
+        for (uint64_t i = c->k; i < c->m; ++i) col[i] -= s * v[i];
+    }
+}
+
+static void apply_reflector(double* wt, uint64_t m, uint64_t n, uint64_t k, uint64_t j_lo,
+                            const double* v, double beta) {
+    refl_ctx c = {wt, v, m, k, j_lo, beta};
+    par_for(n - j_lo, (m - k) > (1u << 14) ? 1 : (uint64_t)-1, refl_range, &c);
+}
+
+/* linalg.hpp:39-99: Householder with alpha = -sign(x_k) ||x||, Q accumulated
+ * backwards from the first n columns of I, then rows of R / columns of Q
+ * flipped so diag(R) >= 0.  A zero column leaves its reflector empty. */
 int cpdo_thin_qr(const double* a, uint64_t m, uint64_t n, double* q, double* r) {
     if (m < n) return fail(CPDO_INVALID_ARGUMENT, "thin_qr: requires rows >= cols");
-    double* w = dup(a, m * n);
+    double* wt = (double*)xcalloc(m * n, sizeof(double)); /* column-major work */
+    transpose_par(a, m, n, wt);
     double* refl = (double*)xcalloc(m * n, sizeof(double)); /* column k: v in rows k.. */
     double* beta = (double*)xcalloc(n, sizeof(double));
     char* has = (char*)xcalloc(n, 1);
     for (uint64_t k = 0; k < n; ++k) {
+        const double* ck = wt + k * m;
         double nsq = 0.0;
-        for (uint64_t i = k; i < m; ++i) nsq += w[i * n + k] * w[i * n + k];
+        for (uint64_t i = k; i < m; ++i) nsq += ck[i] * ck[i];
         const double nrm = sqrt(nsq);
         if (nrm == 0.0) continue;
-        const double alpha = w[k * n + k] >= 0.0 ? -nrm : nrm;
+        const double alpha = ck[k] >= 0.0 ? -nrm : nrm;
         double* v = refl + k * m; /* v[0..m-k) */
-        v[0] = w[k * n + k] - alpha;
-        for (uint64_t i = k + 1; i < m; ++i) v[i - k] = w[i * n + k];
+        v[0] = ck[k] - alpha;
+        for (uint64_t i = k + 1; i < m; ++i) v[i - k] = ck[i];
         double vsq = 0.0;
         for (uint64_t i = 0; i < m - k; ++i) vsq += v[i] * v[i];
         const double bt = 2.0 / vsq;
-        for (uint64_t j = k; j < n; ++j) {
-            double s = 0.0;
-            for (uint64_t i = k; i < m; ++i) s += v[i - k] * w[i * n + j];
-            s *= bt;
-            for (uint64_t i = k; i < m; ++i) w[i * n + j] -= s * v[i - k];
-        }
-        w[k * n + k] = alpha;
+        apply_reflector(wt, m, n, k, k, v, bt);
+        wt[k * m + k] = alpha;
         beta[k] = bt;
         has[k] = 1;
     }
     memset(r, 0, n * n * sizeof(double));
     for (uint64_t i = 0; i < n; ++i)
-        for (uint64_t j = i; j < n; ++j) r[i * n + j] = w[i * n + j];
-    memset(q, 0, m * n * sizeof(double));
-    for (uint64_t j = 0; j < n; ++j) q[j * n + j] = 1.0;
+        for (uint64_t j = i; j < n; ++j) r[i * n + j] = wt[j * m + i];
+    double* qt = wt; /* reuse: Q column-major */
+    memset(qt, 0, m * n * sizeof(double));
+    for (uint64_t j = 0; j < n; ++j) qt[j * m + j] = 1.0;
     for (uint64_t k = n; k-- > 0;) {
         if (!has[k]) continue;
-        const double* v = refl + k * m;
-        for (uint64_t j = 0; j < n; ++j) {
-            double s = 0.0;
-            for (uint64_t i = k; i < m; ++i) s += v[i - k] * q[i * n + j];
-            s *= beta[k];
-            for (uint64_t i = k; i < m; ++i) q[i * n + j] -= s * v[i - k];
-        }
+        apply_reflector(qt, m, n, k, 0, refl + k * m, beta[k]);
     }
     for (uint64_t k = 0; k < n; ++k)
         if (r[k * n + k] < 0.0) {
             for (uint64_t j = k; j < n; ++j) r[k * n + j] = -r[k * n + j];
-            for (uint64_t i = 0; i < m; ++i) q[i * n + k] = -q[i * n + k];
+            for (uint64_t i = 0; i < m; ++i) qt[k * m + i] = -qt[k * m + i];
         }
-    free(w);
+    transpose_par(qt, n, m, q);
+    free(wt);
     free(refl);
     free(beta);
     free(has);
@@ -923,7 +1088,7 @@ static double* rebuild_entry(const double* x, const uint64_t* xdims, const fstat
     const uint32_t order = st->order;
     uint64_t d[CPDO_MAX_ORDER];
     memcpy(d, xdims, order * sizeof(uint64_t));
-    double* cur = dup(x, prod(d, 0, order));
+    double* cur = dupd(x, prod(d, 0, order));
     for (uint32_t k = order; k-- > 0;) {
         if (key & (1u << k)) continue;
         double* qt = (double*)xcalloc(st->rank * d[k], sizeof(double));
@@ -942,15 +1107,34 @@ static double* rebuild_entry(const double* x, const uint64_t* xdims, const fstat
     return cur;
 }
 
-/* V = unfold(Y, n) * Q (tensor.hpp:184-189 matmul, ikj loop) */
+/* V = unfold(Y, n) * Q (tensor.hpp:184-189 matmul, ikj loop); threads take
+ * disjoint rows of V */
+typedef struct {
+    const double *yn, *q;
+    double* v;
+    uint64_t K, R;
+} vg_ctx;
+
+static void v_gemm_range(void* p, uint64_t i0, uint64_t i1) {
+    const vg_ctx* c = (const vg_ctx*)p;
+    /* blocks of 512 rows of Q stay in cache across this thread's rows of V;
+     * each V element still sums over pp ascending */
+    const uint64_t pb = 512;
+    for (uint64_t p0 = 0; p0 < c->K; p0 += pb) {
+        const uint64_t p1 = p0 + pb < c->K ? p0 + pb : c->K;
+        for (uint64_t i = i0; i < i1; ++i)
+            for (uint64_t pp = p0; pp < p1; ++pp) {
+                const double a = c->yn[i * c->K + pp];
+                for (uint64_t j = 0; j < c->R; ++j) c->v[i * c->R + j] += a * c->q[pp * c->R + j];
+            }
+    }
+}
+
 static void v_gemm(const double* yn, uint64_t rows, uint64_t K, const double* q, uint64_t R,
                    double* v) {
     memset(v, 0, rows * R * sizeof(double));
-    for (uint64_t i = 0; i < rows; ++i)
-        for (uint64_t p = 0; p < K; ++p) {
-            const double a = yn[i * K + p];
-            for (uint64_t j = 0; j < R; ++j) v[i * R + j] += a * q[p * R + j];
-        }
+    vg_ctx c = {yn, q, v, K, R};
+    par_for(rows, K * R > (1u << 16) ? 1 : rows, v_gemm_range, &c);
 }
 
 int cpdo_solve(const double* x, const uint64_t* dims, uint32_t order, const cpdo_config* cfg,
@@ -1019,7 +1203,7 @@ int cpdo_solve(const double* x, const uint64_t* dims, uint32_t order, const cpdo
     double* hist[CPDO_MAX_ORDER] = {0};
     if (stin && stin->q0_history)
         for (uint32_t n = 0; n < order; ++n)
-            if (stin->history_mask & (1u << n)) hist[n] = dup(stin->q0_history + n * zrows * R, zrows * R);
+            if (stin->history_mask & (1u << n)) hist[n] = dupd(stin->q0_history + n * zrows * R, zrows * R);
     int has_beta = 0;
     double beta = 0.0;
     if (extrap && cfg->has_beta_override) {
@@ -1071,8 +1255,11 @@ int cpdo_solve(const double* x, const uint64_t* dims, uint32_t order, const cpdo
                     mats[cnt] = st.r[k];
                     mrows[cnt++] = R;
                 }
+            double tp0 = now_seconds();
             cpdo_khatri_rao(mats, mrows, cnt, R, z);
+            double tp1 = now_seconds();
             cpdo_thin_qr(z, zrows, R, q0, r0);
+            double tp2 = now_seconds();
             if (observer) observer(observer_user, sweep, n, q0, zrows, R);
             const double* qused = q0;
             if (extrap && has_beta && beta != 0.0 && hist[n]) {
@@ -1086,12 +1273,19 @@ int cpdo_solve(const double* x, const uint64_t* dims, uint32_t order, const cpdo
             }
             double* y = NULL;
             uint64_t yd[CPDO_MAX_ORDER];
+            double tp3 = now_seconds();
             rc = execute(&s, x, dims, &st, &cache, sweep - 1, n, &y, yd, &tot_flops, &tot_roots);
             if (rc) break;
             const uint64_t I = dims[n];
+            double tp4 = now_seconds();
             cpdo_unfold(y, yd, order, n, yn);
             free(y);
+            double tp5 = now_seconds();
             v_gemm(yn, I, zrows, qused, R, v);
+            double tp6 = now_seconds();
+            if (getenv("CPDO_PROFILE"))
+                fprintf(stderr, "mode %u: kr %.3f qr %.3f ex %.3f ttm %.3f unfold %.3f vgemm %.3f\n", n,
+                        tp1 - tp0, tp2 - tp1, tp3 - tp2, tp4 - tp3, tp5 - tp4, tp6 - tp5);
             transpose(r0, R, R, r0t);
             rc = cpdo_solve_rows_lower(r0t, R, v, I, ah, NULL);
             if (rc) break;

@@ -164,3 +164,36 @@ def port_init(port, dims, rank, seed):
         out.append(port.normalize_columns(draws[off:off + d * rank].reshape(d, rank))[0])
         off += d * rank
     return out
+
+
+@pytest.mark.parametrize("m,n", [(20000, 64), (3001, 33), (700, 8)])
+def test_threaded_thin_qr_bit_identical_to_reference(port, ref, m, n):
+    """The port's Householder QR runs rows-outer and on several host threads
+    (output columns split between threads); every operation keeps the
+    reference's order, so Q and R equal oracle/_ref bit for bit -- including a
+    tall C5-like Khatri-Rao shape."""
+    a = port.rng_normals(900 + n, m * n).reshape(m, n)
+    a[:, 3] = 0.0  # a zero column: its reflector is skipped (linalg.hpp:51)
+    qp, rp = port.thin_qr(a)
+    qr, rr = ref.thin_qr(a)
+    assert np.array_equal(qp, qr) and np.array_equal(rp, rr)
+
+
+@pytest.mark.parametrize("dims,mode", [((64, 48, 40), 0), ((64, 48, 40), 1), ((64, 48, 40), 2),
+                                       ((9, 8, 7, 300), 3), ((3, 5000, 4), 1)])
+def test_threaded_ttm_bit_identical_to_reference(port, ref, dims, mode):
+    x = port.rng_normals(77, int(np.prod(dims))).reshape(dims)
+    b = port.rng_normals(78, 11 * dims[mode]).reshape(11, dims[mode])
+    assert np.array_equal(port.ttm(x, b, mode), ref.ttm(x, b, mode))
+
+
+def test_threaded_solve_bit_identical_to_reference(port, ref):
+    """A 4th-order BRE run whose Z (R^3 = 4096 rows) and TTMs take the
+    threaded paths: the trace and the factors equal the reference's bit for
+    bit."""
+    x = port.synth_baseline(0, (20, 18, 17, 16), 16, 1e-3, 31337)
+    a = port.solve(x, 16, 5, extrapolate=True, seed=7)
+    b = ref.solve(x, 16, 5, extrapolate=True, seed=7)
+    assert [t["fitness"] for t in a.trace] == [t["fitness"] for t in b.trace]
+    for fa, fb in zip(a.factors, b.factors):
+        assert np.array_equal(fa, fb)
