@@ -346,3 +346,30 @@ def test_tall_z_fourth_order_vs_oracle(ctx, port):
     o = port.solve(x, 32, 8, extrapolate=True, seed=META["init_seed"])
     compare(g, o, factor_tol=1e-9)
     assert any(t.beta_used != 0.0 for t in g.trace)  # the history path runs too
+
+
+# ---------------------------------------------------------------- C5 (north star config 5)
+@pytest.mark.parametrize("k", [3, 4, 5, 12])
+def test_c5_proxy_teacher_forced(port, k):
+    """BASELINE config 5's device path -- fourth order, R = 64: the tall
+    multi-kernel Z-QR of Z = 262144 x 64 (zqr_rows/apply/fin<64>),
+    vgemm<64>, finish_cluster<64>, the 3-cycle branch reuse -- at the 64^4
+    proxy of the 256^4 tensor (Z and every R-sized operand keep their C5
+    size).  The device's state after sweep k -> one oracle sweep (the
+    reference's Householder thin_qr on that Z, linalg.hpp:39-99) vs the
+    device's sweep k+1, both uninterrupted and resumed from the state.  k =
+    3, 4, 5 cover the three phases of the cycle (dim_tree.hpp:411-422); k =
+    12 runs with the Q0 history in use.  Fitness, factors and lambda <= 1e-10
+    relative; integer flops, root counts, update order and beta identical."""
+    from tools.teacher_forced import CONFIGS, TRUTH_SEED, run
+    kind, _, rank, rho = CONFIGS["c5"]
+    r = run(kind, (64, 64, 64, 64), rank, rho, TRUTH_SEED["c5"], k, port=port)
+    for name in ("continued", "resumed"):
+        g = r[name]
+        assert g["iteration"] == g["oracle_iteration"] == k + 1
+        assert g["flops"] == g["oracle_flops"] and g["root_ttms"] == g["oracle_root_ttms"]
+        assert g["update_order"] == g["oracle_update_order"]
+        assert g["beta_used"] == g["oracle_beta_used"]
+        assert g["rel_fitness_err"] <= FIT_TOL, (name, g)
+        assert max(g["rel_factor_err"]) <= FACTOR_TOL, (name, g)
+        assert g["rel_lambda_err"] <= FACTOR_TOL, (name, g)
