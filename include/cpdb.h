@@ -156,6 +156,14 @@ int cpdb_tensor_set_device(cpdb_ctx* ctx, const double* device_ptr, const uint64
  * on (seed, dims, rank) only, not on the shard layout. */
 int cpdb_tensor_synth(cpdb_ctx* ctx, int32_t kind, const uint64_t* dims, uint32_t order,
                       uint64_t rank, double rho, uint64_t seed);
+/* The truth factors cpdb_tensor_synth builds X from (sum I_k x R doubles,
+ * mode after mode, lambda = 1): X_clean = reconstruct(factors) (kruskal.hpp:54-67). */
+int cpdb_tensor_synth_truth(cpdb_ctx* ctx, int32_t kind, const uint64_t* dims, uint32_t order,
+                            uint64_t rank, uint64_t seed, double* factors);
+/* Of the context's last cpdb_tensor_synth: out[0] = ||X_clean||^2 and out[1] =
+ * ||E||^2 of the unscaled noise draw (global over the ranks; 0 when rho = 0).
+ * X = X_clean + rho sqrt(out[0] / out[1]) E. */
+int cpdb_tensor_synth_norms(cpdb_ctx* ctx, double* out);
 int cpdb_tensor_get(cpdb_ctx* ctx, double* host);
 /* .cpdt tensor files (io.hpp:93-121: "CPDT", u8 version 1, u8 order, u64
  * extents, f64 values little-endian, row-major).  load streams the payload

@@ -1385,6 +1385,45 @@ int cpdo_solve(const double* x, const uint64_t* dims, uint32_t order, const cpdo
     return rc;
 }
 
+/* kruskal.hpp:54-67 reconstruct: A_0 diag(lambda) times the ascending
+ * Khatri-Rao of the other factors (gemm_bt loop order, detail::scale_columns
+ * applied to A_0 first). */
+int cpdo_reconstruct(const uint64_t* dims, uint32_t order, uint64_t R, const double* lambda,
+                     const double* factors, double* out) {
+    if (order < 1 || order > CPDO_MAX_ORDER) return fail(CPDO_INVALID_ARGUMENT, "reconstruct: order");
+    const double* f[CPDO_MAX_ORDER];
+    const double* p = factors;
+    for (uint32_t k = 0; k < order; ++k) {
+        f[k] = p;
+        p += dims[k] * R;
+    }
+    uint64_t krows = 1;
+    const double* mats[CPDO_MAX_ORDER];
+    uint64_t mrows[CPDO_MAX_ORDER];
+    for (uint32_t k = 1; k < order; ++k) {
+        mats[k - 1] = f[k];
+        mrows[k - 1] = dims[k];
+        krows *= dims[k];
+    }
+    double* kr = (double*)xcalloc(krows * R, sizeof(double));
+    if (order > 1)
+        cpdo_khatri_rao(mats, mrows, order - 1, R, kr);
+    else
+        for (uint64_t j = 0; j < R; ++j) kr[j] = 1.0;
+    double* a0 = (double*)xcalloc(dims[0] * R, sizeof(double));
+    for (uint64_t i = 0; i < dims[0]; ++i)
+        for (uint64_t j = 0; j < R; ++j) a0[i * R + j] = f[0][i * R + j] * lambda[j];
+    for (uint64_t i = 0; i < dims[0]; ++i)
+        for (uint64_t j = 0; j < krows; ++j) {
+            double acc = 0.0;
+            for (uint64_t q = 0; q < R; ++q) acc += a0[i * R + q] * kr[j * R + q];
+            out[i * krows + j] = acc;
+        }
+    free(a0);
+    free(kr);
+    return CPDO_OK;
+}
+
 /* BASELINE synthetic construction (definition in oracle/ref_runner.cpp,
  * cpdref_synth_baseline); reconstruct per kruskal.hpp:54-67 (A_0 times the
  * ascending Khatri-Rao of the other factors, gemm_bt loop order). */

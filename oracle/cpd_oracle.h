@@ -91,6 +91,10 @@ int cpdo_solve(const double* x, const uint64_t* dims, uint32_t order, const cpdo
                double* out_factors, double* factors_per_sweep, double* lambda_per_sweep,
                cpdo_q0_observer observer, void* observer_user);
 
+/* kruskal.hpp:54-67 reconstruct (factors: sum I_k x R, mode after mode) */
+int cpdo_reconstruct(const uint64_t* dims, uint32_t order, uint64_t rank, const double* lambda,
+                     const double* factors, double* out);
+
 /* BASELINE synthetic construction, same definition as cpdref_synth_baseline */
 int cpdo_synth_baseline(int32_t kind, const uint64_t* dims, uint32_t order, uint64_t rank,
                         double rho, uint64_t seed, double* out, double* truth_factors);

@@ -468,6 +468,19 @@ class Oracle:
                                                 _dp(s_last), C.byref(fit), C.byref(raw)))
         return fit.value, raw.value
 
+    def reconstruct(self, factors, lam=None) -> np.ndarray:
+        """kruskal.hpp:54-67 reconstruct."""
+        dims = [int(f.shape[0]) for f in factors]
+        rank = int(factors[0].shape[1])
+        lam = np.ones(rank) if lam is None else np.ascontiguousarray(lam, dtype=np.float64)
+        flat = np.ascontiguousarray(np.concatenate([np.ascontiguousarray(f).ravel()
+                                                    for f in factors]))
+        out = np.empty(dims)
+        d = _u64(dims)
+        self._check(self._f("reconstruct")(d.ctypes.data_as(_U64P), C.c_uint32(len(dims)),
+                                           C.c_uint64(rank), _dp(lam), _dp(flat), _dp(out)))
+        return out
+
     def synth_baseline(self, kind: int, dims, rank: int, rho: float, seed: int,
                        want_truth: bool = False):
         d = _u64(dims)

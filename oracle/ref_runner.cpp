@@ -561,6 +561,25 @@ int cpdref_solve(const double* x, const uint64_t* dims, uint32_t order, const cp
     });
 }
 
+// kruskal.hpp:54-67 reconstruct through the reference itself
+int cpdref_reconstruct(const uint64_t* dims, uint32_t order, uint64_t rank, const double* lambda,
+                       const double* factors, double* out) {
+    return guarded([&] {
+        const cpd::Shape shape = make_shape(dims, order);
+        cpd::KruskalModel m;
+        m.lambda.assign(lambda, lambda + rank);
+        const double* p = factors;
+        for (uint32_t k = 0; k < order; ++k) {
+            cpd::Matrix f(dims[k], rank);
+            std::memcpy(f.data(), p, dims[k] * rank * sizeof(double));
+            p += dims[k] * rank;
+            m.factors.push_back(std::move(f));
+        }
+        const cpd::DenseTensor xt = cpd::reconstruct(m, shape);
+        std::memcpy(out, xt.data(), xt.size() * sizeof(double));
+    });
+}
+
 // BASELINE.json synthetic construction.
 // kind 0: i.i.d. N(0,1) factors drawn mode by mode, row-major.
 // kind 1: per mode a shared g ~ N(0,1)^I, then per column j: U ~ U(0,1),

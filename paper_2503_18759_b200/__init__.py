@@ -197,6 +197,23 @@ class Context:
         _raise(_lib().cpdb_tensor_synth(self._h, kind, _up(d), len(d), rank, rho, seed))
         self.dims = [int(v) for v in d]
 
+    def synth_truth(self, kind: int, dims: Sequence[int], rank: int, seed: int) -> List[np.ndarray]:
+        """The truth factors synth_tensor builds X from (lambda = 1)."""
+        d = _u64(dims)
+        flat = np.empty(sum(int(v) * rank for v in dims))
+        _raise(_lib().cpdb_tensor_synth_truth(self._h, kind, _up(d), len(d), rank, seed, _p(flat)))
+        out, off = [], 0
+        for v in dims:
+            out.append(flat[off:off + int(v) * rank].reshape(int(v), rank).copy())
+            off += int(v) * rank
+        return out
+
+    def synth_norms(self):
+        """(||X_clean||^2, ||E||^2) of the last synth_tensor (global over ranks)."""
+        out = np.zeros(2)
+        _raise(_lib().cpdb_tensor_synth_norms(self._h, _p(out)))
+        return float(out[0]), float(out[1])
+
     def load_tensor(self, path: str):
         """Stream a .cpdt file (io.hpp:93-121) straight into HBM; a sharded
         context reads only its mode-0 slab."""
@@ -796,6 +813,13 @@ def retained_keys(s: Schedule, iteration: int, block: int) -> List[int]:
                                      s.num_iterations(), s.cycle_start, s.cycle_length, iteration,
                                      block, keys, 256, C.byref(n)))
     return [int(keys[i]) for i in range(n.value)]
+
+
+def shard_rows(extent0: int, rank: int, world: int) -> Tuple[int, int]:
+    """(begin, count) of the leading-mode rows `rank` owns (host only)."""
+    b, n = C.c_uint64(), C.c_uint64()
+    _raise(_lib().cpdb_shard_rows(extent0, rank, world, C.byref(b), C.byref(n)))
+    return int(b.value), int(n.value)
 
 
 def cpdt_info(path: str) -> List[int]:

@@ -105,6 +105,9 @@ SIGNATURES = {
     "cpdb_tensor_set_device": (C.c_int, [CTX, C.c_void_p, U64P, C.c_uint32]),
     "cpdb_tensor_synth": (C.c_int, [CTX, C.c_int32, U64P, C.c_uint32, C.c_uint64, C.c_double,
                                     C.c_uint64]),
+    "cpdb_tensor_synth_truth": (C.c_int, [CTX, C.c_int32, U64P, C.c_uint32, C.c_uint64,
+                                          C.c_uint64, P]),
+    "cpdb_tensor_synth_norms": (C.c_int, [CTX, P]),
     "cpdb_tensor_get": (C.c_int, [CTX, P]),
     "cpdb_create_local_group": (C.c_int, [C.c_int, C.c_int, C.POINTER(CTX)]),
     "cpdb_tensor_load_cpdt": (C.c_int, [CTX, C.c_char_p]),

@@ -350,8 +350,41 @@ int cpdb_tensor_synth(cpdb_ctx* c, int32_t kind, const uint64_t* dims, uint32_t 
         CPDB_CK(cpdb::synth_pass2(x, c->dims.data(), order, rank, seed, c->row_begin, c->rows,
                                   scal, rho, c->stream));
         c->launches += 4;
+        CPDB_CK(cudaMemcpyAsync(c->synth_norms, scal, 2 * sizeof(double), cudaMemcpyDeviceToHost,
+                                c->stream));
         CPDB_CK(cudaStreamSynchronize(c->stream));
+        if (rho <= 0.0) c->synth_norms[1] = 0.0;
         c->x = x;
+    });
+}
+
+int cpdb_tensor_synth_truth(cpdb_ctx* c, int32_t kind, const uint64_t* dims, uint32_t order,
+                            uint64_t rank, uint64_t seed, double* factors) {
+    return guarded([&] {
+        use_device(c);
+        if (kind != 0 && kind != 1) fail(CPDB_INVALID_ARGUMENT, "synth: unknown kind");
+        if (rank == 0) fail(CPDB_INVALID_ARGUMENT, "synth: rank must be >= 1");
+        if (!factors) fail(CPDB_INVALID_ARGUMENT, "synth_truth: null output");
+        const std::vector<uint64_t> d = dims_of(dims, order);
+        uint64_t nf = 0;
+        for (uint64_t e : d) nf += e * rank;
+        cpdb::DevBuf fb, ddims;
+        double* f = fb.ensure(nf);
+        double* dd = ddims.ensure(order);
+        CPDB_CK(cudaMemcpyAsync(dd, d.data(), order * sizeof(uint64_t), cudaMemcpyHostToDevice,
+                                c->stream));
+        CPDB_CK(cpdb::synth_factors(f, reinterpret_cast<const uint64_t*>(dd), order, rank, kind,
+                                    seed, c->stream));
+        c->launches += 1;
+        download(c, factors, f, nf);
+    });
+}
+
+int cpdb_tensor_synth_norms(cpdb_ctx* c, double* out) {
+    return guarded([&] {
+        if (!out) fail(CPDB_INVALID_ARGUMENT, "synth_norms: null output");
+        out[0] = c->synth_norms[0];
+        out[1] = c->synth_norms[1];
     });
 }
 

@@ -206,5 +206,8 @@ cudaError_t synth_pass2(double* x, const uint64_t* dims_host, uint32_t order, ui
                         uint64_t seed, uint64_t row_begin, uint64_t row_count, const double* scal,
                         double rho, cudaStream_t s);
 size_t synth_partials_doubles();
+// the truth factors alone (sum I_k x R doubles, mode after mode)
+cudaError_t synth_factors(double* factors, const uint64_t* dims_dev, uint32_t order,
+                          uint64_t rank, int32_t kind, uint64_t seed, cudaStream_t s);
 
 }  // namespace cpdb

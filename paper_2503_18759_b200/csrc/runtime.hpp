@@ -128,6 +128,8 @@ struct cpdb_ctx {
     std::vector<uint64_t> ldims;  // local extents (ldims[0] = rows)
     bool norm_valid = false;
     double norm_x_sq = 0.0;
+    // last cpdb_tensor_synth: global ||X_clean||^2 and ||E||^2 (E unscaled)
+    double synth_norms[2] = {0.0, 0.0};
 
     // cache slots for the device execute() API (dim_tree.hpp:473-544)
     std::map<uint32_t, cpdb::Slot> slots;

@@ -124,7 +124,11 @@ def test_cp_als_trajectories(ctx, ref, dims, rank, kind):
     x = ref.synth_baseline(kind, dims, rank, 1e-2, 777 + rank)
     g = cpd.cp_als(x, als_cfg(rank, 25, seed=9), ctx=ctx)
     o = ref.cp_als(x, rank, 25, seed=9)
-    compare(g, o, fit_tol=1e-10 if kind == 0 else 1e-9, factor_tol=1e-9 if kind == 0 else 1e-7)
+    # measured (tools/parity_floor.py --als-only, profiles/r02_parity_floor_als.jsonl):
+    # fit <= 5.2e-13; factors <= 4.7e-14 (kind 0); the ill-conditioned kind-1
+    # case's factors differ by 1.2e-10 where the reference moves by 6.9e-11
+    # under a 1e-15 perturbation of X, so its factor bar is 4x that floor
+    compare(g, o, factor_tol=1e-10 if kind == 0 else 3e-10)
 
 
 @pytest.mark.parametrize("dims,rank", [((12, 11, 10), 4), ((7, 6, 5, 4), 3)])
@@ -134,7 +138,7 @@ def test_cp_als_random_tensors(ctx, ref, dims, rank):
     x = np.random.default_rng(sum(dims)).standard_normal(dims)
     g = cpd.cp_als(x, als_cfg(rank, 15, seed=31), ctx=ctx)
     o = ref.cp_als(x, rank, 15, seed=31)
-    compare(g, o, fit_tol=1e-8, factor_tol=1e-6)
+    compare(g, o)  # measured: fit 5.3e-15, factors 7.7e-16
     for i in range(1, len(g.trace)):  # solver_test.cpp:131-136
         assert g.trace[i].fitness >= g.trace[i - 1].fitness - 1e-9
 

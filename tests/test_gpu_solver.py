@@ -51,8 +51,10 @@ def test_small_trajectories(ctx, port, dims, rank, variant):
     else:
         g = cpd.cp_als_qr(x, cfg_of(rank, 12, seed=3, strategy=variant), ctx=ctx)
         o = port.solve(x, rank, 12, extrapolate=False, strategy=variant, seed=3)
-    # random (non-low-rank) tensors converge slowly: compare at 1e-9 of fitness
-    compare(g, o, fit_tol=1e-9, factor_tol=1e-8)
+    # measured (tools/parity_floor.py, profiles/r02_parity_floor.jsonl): fit
+    # <= 1.9e-14, factors <= 8e-15, the oracle's own 1e-15-perturbation floor
+    # is the same order -- the north-star bar holds with 4 digits to spare
+    compare(g, o)
 
 
 def test_c1_full_config(ctx, port, golden):
@@ -77,7 +79,8 @@ def test_c4_ill_conditioned_reduced(ctx, port):
     x = port.synth_baseline(1, (48, 48, 48), 20, 1e-4, META["truth_seeds"]["c4"])
     g = cpd.als_qr_bre(x, cfg_of(20, 60, seed=META["init_seed"]), ctx=ctx)
     o = port.solve(x, 20, 60, extrapolate=True, seed=META["init_seed"])
-    compare(g, o, factor_tol=1e-8)
+    # measured: fit 1.5e-11 (oracle floor 1.3e-11), factors 1.1e-12
+    compare(g, o)
 
 
 def test_c3_shape_4th_order_reduced(ctx, port):
@@ -293,7 +296,7 @@ def test_rank_edges_vs_oracle(ctx, port, dims, rank):
     else:
         g = cpd.als_qr_bre(x, cfg_of(rank, 6, seed=5), ctx=ctx)
         o = port.solve(x, rank, 6, extrapolate=True, seed=5)
-    compare(g, o, fit_tol=1e-9, factor_tol=1e-8)
+    compare(g, o)  # measured: fit <= 1.3e-14, factors <= 4.2e-15
 
 
 @pytest.mark.parametrize("early", ["1", "0"])
@@ -311,7 +314,7 @@ def test_schedule_variants_match_oracle(ctx, port, monkeypatch, early, overlap_s
     x = port.synth_baseline(0, (64, 64, 64), 16, 1e-3, META["truth_seeds"]["c2"])
     g = cpd.als_qr_bre(x, cfg_of(16, 24, seed=META["init_seed"]), ctx=ctx)
     o = port.solve(x, 16, 24, extrapolate=True, seed=META["init_seed"])
-    compare(g, o, factor_tol=1e-9)
+    compare(g, o)  # measured: fit 9.4e-12, factors 2.6e-16
     g2 = cpd.als_qr_bre(x, cfg_of(16, 24, seed=META["init_seed"]), ctx=ctx)
     assert [t.fitness for t in g2.trace] == [t.fitness for t in g.trace]
     for a, b in zip(g.model.factors, g2.model.factors):
@@ -328,12 +331,16 @@ def test_stop_test_undoes_speculative_update(ctx, port, monkeypatch, speculate, 
     import paper_2503_18759_b200 as cpd
     monkeypatch.setenv("CPDB_SPECULATE", speculate)
     x = port.synth_baseline(0, dims, 3, 1e-2, 20250011)
-    # threshold = the oracle's own fitness at sweep 10: the run stops mid-way
-    thr = port.solve(x, 3, 10, extrapolate=True, seed=5).trace[-1]["fitness"]
+    # threshold midway between the oracle's fitness at sweeps k-1 and k (the
+    # last sweep <= 10 that still gains > 1e-9): the run stops at sweep k
+    # whatever the last bits of either side's fitness
+    f = [t["fitness"] for t in port.solve(x, 3, 10, extrapolate=True, seed=5).trace]
+    k = max(i + 1 for i in range(2, 10) if f[i] - f[i - 1] > 1e-9)
+    thr = 0.5 * (f[k - 2] + f[k - 1])
     o = port.solve(x, 3, 40, extrapolate=True, seed=5, fitness_threshold=thr)
-    assert 2 < len(o.trace) <= 10
+    assert len(o.trace) == k
     g = cpd.als_qr_bre(x, cfg_of(3, 40, seed=5, fitness_threshold=thr), ctx=ctx)
-    compare(g, o, factor_tol=1e-9)
+    compare(g, o)
 
 
 def test_tall_z_fourth_order_vs_oracle(ctx, port):
@@ -344,7 +351,7 @@ def test_tall_z_fourth_order_vs_oracle(ctx, port):
     x = port.synth_baseline(0, dims, 32, 1e-3, META["truth_seeds"]["c5"])
     g = cpd.als_qr_bre(x, cfg_of(32, 8, seed=META["init_seed"]), ctx=ctx)
     o = port.solve(x, 32, 8, extrapolate=True, seed=META["init_seed"])
-    compare(g, o, factor_tol=1e-9)
+    compare(g, o)  # measured: fit 1.5e-13, factors 1.7e-14
     assert any(t.beta_used != 0.0 for t in g.trace)  # the history path runs too
 
 
@@ -373,3 +380,36 @@ def test_c5_proxy_teacher_forced(port, k):
         assert g["rel_fitness_err"] <= FIT_TOL, (name, g)
         assert max(g["rel_factor_err"]) <= FACTOR_TOL, (name, g)
         assert g["rel_lambda_err"] <= FACTOR_TOL, (name, g)
+
+
+# ---------------------------------------------------------------- full-length BASELINE parity
+FULL_LENGTH = {  # (kind, dims, rank, rho, sweeps): BASELINE.json configs 2, 3, 4
+    "c2": (0, (512, 512, 512), 32, 1e-3, 100),
+    "c3": (0, (128, 128, 128, 128), 16, 1e-2, 100),
+    "c4": (1, (256, 256, 256), 20, 1e-4, 500),
+}
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("name", ["c2", "c3", "c4"])
+def test_full_length_parity(port, name):
+    """Every sweep of BASELINE configs 2-4 at full size and full sweep count,
+    device vs the oracle (the C restatement, bit-identical to the reference:
+    tests/test_oracle.py) on the same device-generated tensor: fitness and
+    final factors / lambda <= 1e-10 relative on every sweep, identical trace
+    length, update order, integer flops / root counts and beta-activation
+    sweep (solver_test.cpp:168-180).  Measured round 1 on the
+    reference itself: C2 1.7e-13, C3 4.0e-11, C4 5.1e-11 (its own 1e-15
+    perturbation floor 1.7e-11)."""
+    import paper_2503_18759_b200 as cpd
+    kind, dims, rank, rho, sweeps = FULL_LENGTH[name]
+    ctx = cpd.Context(0)
+    ctx.synth_tensor(kind, list(dims), rank, rho, META["truth_seeds"][name])
+    x = ctx.get_tensor(list(dims))
+    g = ctx.solve(cfg_of(rank, sweeps, seed=META["init_seed"]), extrapolate=True)
+    o = port.solve(x, rank, sweeps, extrapolate=True, seed=META["init_seed"])
+    compare(g, o)
+    fb = [t.iteration for t in g.trace if t.beta_used != 0.0]
+    ob = [t["iteration"] for t in o.trace if t["beta_used"] != 0.0]
+    assert fb[:1] == ob[:1] and len(fb) == len(ob)
+    ctx.close()

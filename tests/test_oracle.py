@@ -197,3 +197,15 @@ def test_threaded_solve_bit_identical_to_reference(port, ref):
     assert [t["fitness"] for t in a.trace] == [t["fitness"] for t in b.trace]
     for fa, fb in zip(a.factors, b.factors):
         assert np.array_equal(fa, fb)
+
+
+@pytest.mark.parametrize("dims,rank", [((9, 8, 7), 3), ((7, 6, 5, 4), 5), ((11,), 2), ((5, 40), 4)])
+def test_reconstruct_bit_identical_to_reference(port, ref, dims, rank):
+    """kruskal.hpp:54-67: the port's reconstruct (checker of the device
+    generator's truth factors) equals the reference's bit for bit, lambda
+    included; and synth_baseline(rho = 0) is reconstruct(truth)."""
+    fs = [port.rng_normals(50 + k, d * rank).reshape(d, rank) for k, d in enumerate(dims)]
+    lam = port.rng_normals(99, rank)
+    assert np.array_equal(port.reconstruct(fs, lam), ref.reconstruct(fs, lam))
+    x, truth = ref.synth_baseline(0, dims, rank, 0.0, 123, want_truth=True)
+    assert np.array_equal(port.reconstruct(truth), x)
