@@ -214,7 +214,9 @@ def run_reference(args, c, rank, world):
         "impl": "reference", "metric": METRIC, "value": rate, "unit": "sweeps/s",
         "n_gpus": args.gpus, "steps": k, "warmup": 1, "ms_per_step": 1e3 / rate,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic (reference generator, BASELINE construction)",
+        "data": "synthetic (reference generator cpd::Rng, BASELINE construction; the device "
+                "arm's counter-based generator draws other values of the same distribution: "
+                "throughput-neutral)",
         "config": {"workload": workload_name(args.config, c), "dims": list(c["dims"]),
                    "rank": c["rank"]},
         "cpu_baseline": {"value": rate, "unit": "sweeps/s", "cores": 1, "kind": kind,
@@ -279,8 +281,8 @@ def main():
     dt = allmax(world, dt)
     value = K / dt
     d = {k: p1[k] - p0[k] for k in ("root_ttms", "root_ttm_ms", "root_ttm_flops",
-                                     "root_ttm_bytes", "branch_ttm_ms", "comm_ms",
-                                     "kernel_launches")}
+                                     "root_ttm_bytes", "branch_ttm_ms", "mode_update_ms",
+                                     "comm_ms", "kernel_launches")}
     # ---- the root TTM kernel alone (roofline): same config, overlap off ------
     # In the timed run the sweep's root TTM shares the GPU with the preceding
     # update (low-priority stream), so its launch-to-end time is not the
@@ -330,6 +332,10 @@ def main():
     roof["fp64_tflops"] = f_launch / t_launch / 1e12
     roof["hbm_gbs"] = b_launch / t_launch / 1e9
     roof["roofline_frac"] = (max(f_launch / (p64 * 1e12), b_launch / (hbm * 1e9))) / t_launch
+    # the same launches inside the timed run (sharing the GPU with the update
+    # the root overlaps): launch-to-end time on its stream
+    roof["frac_in_timed_run"] = (max(f_launch / (p64 * 1e12), b_launch / (hbm * 1e9))
+                                 / (overlapped_ms * 1e-3))
 
     # ---- e2e through the C ABI with host buffers ---------------------------------
     e2e = None
@@ -358,7 +364,8 @@ def main():
         cfg2 = cpd.SolverConfig(rank=c["rank"], max_iterations=K, seed=INIT_SEED)
         barrier(world)
         t0 = time.perf_counter()
-        ctx2.set_tensor(xh, dims)
+        ctx2.set_tensor(xh, dims)  # synchronous H2D from pinned memory
+        t_h2d = time.perf_counter() - t0
         s2 = ctx2.session(cfg2, extrapolate=True)
         r2 = s2.run(K)
         m2 = s2.end()
@@ -369,9 +376,11 @@ def main():
         h2d = xh.size * 8
         d2h = (sum(f.size for f in m2.factors) + m2.lam.size) * 8 + len(r2) * 128
         e2e = {"value": K / et, "unit": "sweeps/s", "h2d_bytes_per_step": h2d / K,
-               "d2h_bytes_per_step": d2h / K,
-               "note": "one job: H2D of X (pinned) + setup + K sweeps + D2H of the model, "
-                       "bytes amortised over the K sweeps"}
+               "d2h_bytes_per_step": d2h / K, "h2d_ms": t_h2d * 1e3,
+               "h2d_gbs": h2d / t_h2d / 1e9,
+               "rest_ms": (et - t_h2d) * 1e3,
+               "note": "one job: H2D of X (pinned; h2d_ms of it) + setup + K sweeps + D2H of "
+                       "the model, bytes amortised over the K sweeps"}
 
     # ---- CPU baseline: the reference itself, bounded sample ---------------------
     cpu = None
@@ -403,11 +412,20 @@ def main():
             "e2e": e2e,
             "clocks": clocks.summary(),
             "gpu_launches": int(d["kernel_launches"]),
-            "breakdown_ms_per_step": {
+            # device time per step summed by kernel class (CUDA events per
+            # launch).  Classes run concurrently on several streams (the root
+            # under the previous update, Z-QR beside the chain), so the sum
+            # exceeds the wall time by the overlap: concurrency = sum / wall.
+            # mode_update (Z-QR, V-GEMM, finisher) is 0 unless CPDB_TIME_TAILS=1
+            # (its events cost ~5% of the sweep rate); profiles/ has its share.
+            "kernel_ms_per_step": {
                 "root_ttm": d["root_ttm_ms"] / K, "branch_ttm": d["branch_ttm_ms"] / K,
-                "comm": d["comm_ms"] / K,
-                "mode_update_other": (dt * 1e3 - d["root_ttm_ms"] - d["branch_ttm_ms"]
-                                      - d["comm_ms"]) / K},
+                "mode_update": d["mode_update_ms"] / K, "comm": d["comm_ms"] / K,
+                "sum": (d["root_ttm_ms"] + d["branch_ttm_ms"] + d["mode_update_ms"]
+                        + d["comm_ms"]) / K,
+                "wall": dt / K * 1e3,
+                "concurrency": (d["root_ttm_ms"] + d["branch_ttm_ms"] + d["mode_update_ms"]
+                                + d["comm_ms"]) / (dt * 1e3)},
             "final_fitness": rows[-1].fitness,
         }
         print(json.dumps(line), flush=True)

@@ -114,7 +114,9 @@ typedef struct {
     double root_ttm_flops;    /* algorithmic 2*|Y|*I_c summed over timed launches  */
     double root_ttm_bytes;    /* algorithmic 8*(|X| + |Y| + I_c*R) summed          */
     double branch_ttm_ms;     /* non-root TTM steps                                */
-    double mode_update_ms;    /* Z-QR, V-GEMM, solve, normalise, factor QR, fit    */
+    double mode_update_ms;    /* Z-QR, V-GEMM and finisher kernels (solve,
+                                 normalise, factor QR, fit), summed; timed only
+                                 with CPDB_TIME_TAILS=1, else 0                   */
     double comm_ms;           /* NCCL reductions (sharded contexts)                */
     uint64_t kernel_launches; /* device kernels launched by the solve              */
 } cpdb_profile;
@@ -288,6 +290,53 @@ int cpdb_leading_flop_coefficient(uint32_t order, int32_t strategy, uint64_t* co
 int cpdb_shard_plan(uint32_t order, int32_t strategy, uint64_t iterations, const uint64_t* dims,
                     uint64_t rank, int world, int32_t* flags, uint64_t* payload, uint64_t cap,
                     uint64_t* n_steps);
+
+/* The reduction strategy of the sharded session (csrc/shard.cpp).  A TTM
+ * contracting the shard mode of its source yields per-rank partial sums:
+ *   EAGER    all-reduce them at once (replicated afterwards);
+ *   SCATTER  reduce-scatter them onto another free mode (sharded afterwards,
+ *            downstream TTMs stay divided over the ranks);
+ *   LAZY     keep them partial down the chain and all-reduce V (I_n x R);
+ *   AUTO     per step, the cheapest of the three by the cost model over the
+ *            step's consumer tree (FP64 rate, NCCL bus bandwidth, latency).
+ * V of a sharded Y(n) is all-gathered (its rows), of a partial one all-reduced. */
+#define CPDB_SHARD_EAGER 0
+#define CPDB_SHARD_SCATTER 1
+#define CPDB_SHARD_LAZY 2
+#define CPDB_SHARD_AUTO 3
+#define CPDB_LAYOUT_REPLICATED 0
+#define CPDB_LAYOUT_SHARDED 1
+#define CPDB_LAYOUT_PARTIAL 2
+#define CPDB_RED_NONE 0
+#define CPDB_RED_ALLREDUCE 1
+#define CPDB_RED_SCATTER 2
+#define CPDB_V_NONE 0
+#define CPDB_V_GATHER 1
+#define CPDB_V_ALLREDUCE 2
+typedef struct {
+    int32_t src_layout, src_mode;  /* layout of the step's source (mode: the split one) */
+    int32_t out_layout, out_mode;  /* layout of its stored output                     */
+    int32_t reduction;             /* CPDB_RED_* applied to the step's output          */
+    int32_t scatter_mode;          /* CPDB_RED_SCATTER: the free mode scattered onto   */
+    uint64_t words;                /* doubles reduced (global partial size)            */
+} cpdb_shard_step;
+typedef struct {
+    double tflops;     /* FP64 rate of the TTMs per GPU (default 30)                 */
+    double bus_gbs;    /* NCCL bus bandwidth (default 700, NVLink 5 / NVSwitch)      */
+    double latency_s;  /* per collective (default 20e-6)                             */
+} cpdb_shard_cost;
+/* steps: one record per scheduled step (same order as cpdb_schedule_build);
+ * vop / vwords: per mode update, V's collective and its size; est[0] / est[1]:
+ * the model's per-rank compute / communication seconds for the whole plan.
+ * cost may be NULL (defaults). */
+int cpdb_shard_plan_ex(uint32_t order, int32_t strategy, uint64_t iterations,
+                       const uint64_t* dims, uint64_t rank, int world, int32_t policy,
+                       const cpdb_shard_cost* cost, cpdb_shard_step* steps, uint64_t cap_steps,
+                       uint64_t* n_steps, int32_t* vop, uint64_t* vwords, uint64_t cap_updates,
+                       uint64_t* n_updates, double* est);
+/* The policy a context's sessions use (default AUTO; env CPDB_SHARD_POLICY
+ * = eager|scatter|lazy|auto overrides at context creation). */
+int cpdb_set_shard_policy(cpdb_ctx* ctx, int32_t policy, const cpdb_shard_cost* cost);
 
 /* ---- device-resident execute() (dim_tree.hpp:473-544) ------------------------- */
 /* One scheduled TTM on the device: reads X (source == CPDB_ROOT_KEY) or the

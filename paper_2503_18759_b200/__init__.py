@@ -197,6 +197,11 @@ class Context:
         _raise(_lib().cpdb_tensor_synth(self._h, kind, _up(d), len(d), rank, rho, seed))
         self.dims = [int(v) for v in d]
 
+    def set_shard_policy(self, policy="auto", cost: Optional[dict] = None):
+        """Reduction strategy of this context's sharded sessions (shard_plan_ex)."""
+        pol = SHARD_POLICIES[policy] if isinstance(policy, str) else int(policy)
+        _raise(_lib().cpdb_set_shard_policy(self._h, pol, _shard_cost(cost)))
+
     def synth_truth(self, kind: int, dims: Sequence[int], rank: int, seed: int) -> List[np.ndarray]:
         """The truth factors synth_tensor builds X from (lambda = 1)."""
         d = _u64(dims)
@@ -858,6 +863,53 @@ def shard_plan(order: int, strategy, iterations: int, dims: Sequence[int], rank:
                                   flags.ctypes.data_as(C.POINTER(C.c_int32)), _up(payload),
                                   n.value, C.byref(n)))
     return flags, payload
+
+
+SHARD_POLICIES = {"eager": 0, "scatter": 1, "lazy": 2, "auto": 3}
+LAYOUTS = {0: "replicated", 1: "sharded", 2: "partial"}
+REDUCTIONS = {0: None, 1: "allreduce", 2: "scatter"}
+V_OPS = {0: None, 1: "gather", 2: "allreduce"}
+
+
+def _shard_cost(cost):
+    if cost is None:
+        return None
+    c = _cpdb.ShardCost(float(cost.get("tflops", 0.0)), float(cost.get("bus_gbs", 0.0)),
+                        float(cost.get("latency_s", -1.0)))
+    return C.byref(c)
+
+
+def shard_plan_ex(order: int, strategy, iterations: int, dims: Sequence[int], rank: int,
+                  world: int, policy="auto", cost: Optional[dict] = None) -> dict:
+    """The sharded session's layouts and reductions (csrc/shard.cpp,
+    cpdb_shard_plan_ex): per scheduled step {src, out: (layout, mode),
+    reduction, scatter_mode, words}; per mode update the V collective and its
+    size; the cost model's per-rank compute / communication seconds."""
+    d = _u64(dims)
+    pol = SHARD_POLICIES[policy] if isinstance(policy, str) else int(policy)
+    ns, nu = C.c_uint64(), C.c_uint64()
+    cst = _shard_cost(cost)
+    _raise(_lib().cpdb_shard_plan_ex(order, _strategy(strategy), iterations, _up(d), rank, world,
+                                     pol, cst, None, 0, C.byref(ns), None, None, 0, C.byref(nu),
+                                     None))
+    steps = (_cpdb.ShardStep * max(ns.value, 1))()
+    vop = np.zeros(max(nu.value, 1), dtype=np.int32)
+    vw = np.zeros(max(nu.value, 1), dtype=np.uint64)
+    est = np.zeros(2)
+    _raise(_lib().cpdb_shard_plan_ex(order, _strategy(strategy), iterations, _up(d), rank, world,
+                                     pol, cst, steps, ns.value, C.byref(ns),
+                                     vop.ctypes.data_as(C.POINTER(C.c_int32)), _up(vw), nu.value,
+                                     C.byref(nu), _p(est)))
+    out = []
+    for i in range(ns.value):
+        s_ = steps[i]
+        out.append({"src": (LAYOUTS[s_.src_layout], s_.src_mode),
+                    "out": (LAYOUTS[s_.out_layout], s_.out_mode),
+                    "reduction": REDUCTIONS[s_.reduction], "scatter_mode": s_.scatter_mode,
+                    "words": int(s_.words)})
+    return {"steps": out, "v_ops": [V_OPS[int(v)] for v in vop[:nu.value]],
+            "v_words": [int(v) for v in vw[:nu.value]],
+            "est_compute_s": float(est[0]), "est_comm_s": float(est[1])}
 
 
 def closed_form_cost(order: int, strategy, dims: Sequence[int], rank: int) -> int:

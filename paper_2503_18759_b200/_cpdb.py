@@ -92,6 +92,16 @@ I64P = C.POINTER(C.c_int64)
 CTX = C.c_void_p
 
 # name -> (restype, argtypes)
+class ShardStep(C.Structure):
+    _fields_ = [("src_layout", C.c_int32), ("src_mode", C.c_int32), ("out_layout", C.c_int32),
+                ("out_mode", C.c_int32), ("reduction", C.c_int32), ("scatter_mode", C.c_int32),
+                ("words", C.c_uint64)]
+
+
+class ShardCost(C.Structure):
+    _fields_ = [("tflops", C.c_double), ("bus_gbs", C.c_double), ("latency_s", C.c_double)]
+
+
 SIGNATURES = {
     "cpdb_version": (C.c_char_p, []),
     "cpdb_last_error": (C.c_char_p, []),
@@ -109,6 +119,11 @@ SIGNATURES = {
                                           C.c_uint64, P]),
     "cpdb_tensor_synth_norms": (C.c_int, [CTX, P]),
     "cpdb_tensor_get": (C.c_int, [CTX, P]),
+    "cpdb_shard_plan_ex": (C.c_int, [C.c_uint32, C.c_int32, C.c_uint64, U64P, C.c_uint64, C.c_int,
+                                     C.c_int32, C.POINTER(ShardCost), C.POINTER(ShardStep),
+                                     C.c_uint64, U64P, C.POINTER(C.c_int32), U64P, C.c_uint64,
+                                     U64P, P]),
+    "cpdb_set_shard_policy": (C.c_int, [CTX, C.c_int32, C.POINTER(ShardCost)]),
     "cpdb_create_local_group": (C.c_int, [C.c_int, C.c_int, C.POINTER(CTX)]),
     "cpdb_tensor_load_cpdt": (C.c_int, [CTX, C.c_char_p]),
     "cpdb_tensor_save_cpdt": (C.c_int, [CTX, C.c_char_p]),

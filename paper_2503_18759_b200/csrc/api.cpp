@@ -99,6 +99,14 @@ void init_ctx(cpdb_ctx* c, int device) {
     CPDB_CK(cudaStreamCreateWithPriority(&c->zq, cudaStreamNonBlocking, greatest));
     // a TTM chain that must yield SMs to a concurrent multi-kernel Z-QR
     CPDB_CK(cudaStreamCreateWithPriority(&c->mid, cudaStreamNonBlocking, below));
+    // the last update of a sweep while the next sweep's first update runs
+    // beside it (Session::run): below that update's chain, above the root
+    const int below2 = below < least ? (below + 1 < least ? below + 1 : below) : below;
+    CPDB_CK(cudaStreamCreateWithPriority(&c->tailq, cudaStreamNonBlocking, below2));
+    if (const char* sp = std::getenv("CPDB_SHARD_POLICY")) {
+        const std::string v(sp);
+        c->shard_policy = v == "eager" ? 0 : v == "scatter" ? 1 : v == "lazy" ? 2 : 3;
+    }
     CPDB_CK(cudaMalloc(&c->dstatus, 64));
     CPDB_CK(cudaMemset(c->dstatus, 0, 64));
     CPDB_CK(cudaMallocHost(&c->pinned, 64 * sizeof(double)));
@@ -881,6 +889,66 @@ int cpdb_shard_plan(uint32_t order, int32_t strategy, uint64_t iterations, const
                     ++i;
                 }
         *n_steps = i;
+    });
+}
+
+int cpdb_shard_plan_ex(uint32_t order, int32_t strategy, uint64_t iterations,
+                       const uint64_t* dims, uint64_t rank, int world, int32_t policy,
+                       const cpdb_shard_cost* cost, cpdb_shard_step* steps, uint64_t cap_steps,
+                       uint64_t* n_steps, int32_t* vop, uint64_t* vwords, uint64_t cap_updates,
+                       uint64_t* n_updates, double* est) {
+    return guarded([&] {
+        if (strategy < 0 || strategy > 2) fail(CPDB_INVALID_ARGUMENT, "unknown strategy");
+        if (policy < 0 || policy > 3) fail(CPDB_INVALID_ARGUMENT, "shard_plan: unknown policy");
+        if (world < 1) fail(CPDB_INVALID_ARGUMENT, "shard_plan: world must be >= 1");
+        if (dims == nullptr) fail(CPDB_INVALID_ARGUMENT, "shard_plan: null dims");
+        if (rank == 0) fail(CPDB_INVALID_ARGUMENT, "shard_plan: rank must be >= 1");
+        const cpdb::Plan p =
+            cpdb::build_plan(order, static_cast<cpdb::Strategy>(strategy), iterations);
+        cpdb::ShardCost cp;
+        if (cost) {
+            if (cost->tflops > 0) cp.tflops = cost->tflops;
+            if (cost->bus_gbs > 0) cp.bus_gbs = cost->bus_gbs;
+            if (cost->latency_s >= 0) cp.latency_s = cost->latency_s;
+        }
+        const cpdb::ShardPlan sp =
+            cpdb::plan_shards(p, std::vector<uint64_t>(dims, dims + order), rank, world,
+                              static_cast<cpdb::ShardPolicy>(policy), cp);
+        uint64_t i = 0, u = 0;
+        for (size_t sw = 0; sw < sp.steps.size(); ++sw)
+            for (size_t b = 0; b < sp.steps[sw].size(); ++b) {
+                for (const cpdb::StepShard& st : sp.steps[sw][b]) {
+                    if (steps && i < cap_steps)
+                        steps[i] = cpdb_shard_step{st.src.kind, st.src.mode, st.out.kind,
+                                                   st.out.mode, st.red, st.scatter, st.words};
+                    ++i;
+                }
+                const cpdb::UpdateShard& us = sp.updates[sw][b];
+                if (u < cap_updates) {
+                    if (vop) vop[u] = us.vop;
+                    if (vwords) vwords[u] = us.vwords;
+                }
+                ++u;
+            }
+        if (n_steps) *n_steps = i;
+        if (n_updates) *n_updates = u;
+        if (est) {
+            est[0] = sp.est_compute_s;
+            est[1] = sp.est_comm_s;
+        }
+    });
+}
+
+int cpdb_set_shard_policy(cpdb_ctx* c, int32_t policy, const cpdb_shard_cost* cost) {
+    return guarded([&] {
+        if (!c) fail(CPDB_INVALID_ARGUMENT, "null context");
+        if (policy < 0 || policy > 3) fail(CPDB_INVALID_ARGUMENT, "unknown shard policy");
+        c->shard_policy = policy;
+        if (cost) {
+            if (cost->tflops > 0) c->shard_cost.tflops = cost->tflops;
+            if (cost->bus_gbs > 0) c->shard_cost.bus_gbs = cost->bus_gbs;
+            if (cost->latency_s >= 0) c->shard_cost.latency_s = cost->latency_s;
+        }
     });
 }
 

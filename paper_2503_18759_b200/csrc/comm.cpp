@@ -23,10 +23,15 @@ const Nccl& nccl() {
         table.CommDestroy = reinterpret_cast<decltype(table.CommDestroy)>(sym("ncclCommDestroy"));
         table.AllReduce = reinterpret_cast<decltype(table.AllReduce)>(sym("ncclAllReduce"));
         table.AllGather = reinterpret_cast<decltype(table.AllGather)>(sym("ncclAllGather"));
+        table.ReduceScatter =
+            reinterpret_cast<decltype(table.ReduceScatter)>(sym("ncclReduceScatter"));
+        table.GroupStart = reinterpret_cast<decltype(table.GroupStart)>(sym("ncclGroupStart"));
+        table.GroupEnd = reinterpret_cast<decltype(table.GroupEnd)>(sym("ncclGroupEnd"));
         table.GetErrorString =
             reinterpret_cast<decltype(table.GetErrorString)>(sym("ncclGetErrorString"));
         table.ok = table.GetUniqueId && table.CommInitRank && table.CommDestroy &&
-                   table.AllReduce && table.AllGather && table.GetErrorString;
+                   table.AllReduce && table.AllGather && table.ReduceScatter &&
+                   table.GroupStart && table.GroupEnd && table.GetErrorString;
         if (!table.ok) table.why = "libnccl.so.2 lacks a required symbol";
     });
     return table;

@@ -182,6 +182,11 @@ cudaError_t launch_zqr_multi(const ZqrArgs& a, cudaStream_t s, int sms);
 cudaError_t reduce_splits(const double* part, uint32_t nsplit, uint64_t n, double* out,
                           cudaStream_t s);
 // out[e] = sum_{r < world} slots[r*stride + e]  (fixed order; in-process rank groups)
+// reduce-scatter through the in-process group's slots: this rank's chunk
+// (rows [rank*chunk, (rank+1)*chunk) of every outer block) summed over ranks
+cudaError_t sum_slots_scatter(const double* slots, uint64_t stride, uint32_t world,
+                              uint64_t outer, uint64_t block, uint64_t chunk, uint32_t rank,
+                              double* out, cudaStream_t s);
 cudaError_t sum_slots(const double* slots, uint64_t stride, uint32_t world, uint64_t n,
                       double* out, cudaStream_t s);
 

@@ -235,6 +235,36 @@ void allgather(cpdb_ctx* c, double* dev_full, size_t per_rank) {
     if (r != ncclSuccess) fail(CPDB_NCCL_ERROR, std::string("ncclAllGather: ") + N.GetErrorString(r));
 }
 
+void reduce_scatter(cpdb_ctx* c, const double* src, uint64_t outer, uint64_t block,
+                    double* dst) {
+    const uint64_t chunk = block / uint64_t(c->world);
+    if (c->world <= 1) {
+        CPDB_CK(cudaMemcpyAsync(dst, src, outer * block * sizeof(double),
+                                cudaMemcpyDeviceToDevice, c->stream));
+        return;
+    }
+    if (c->group) {
+        LocalGroup& g = *c->group;
+        group_publish(c, src, outer * block);
+        CPDB_CK(sum_slots_scatter(g.slots, g.cap, uint32_t(g.world), outer, block, chunk,
+                                  uint32_t(c->rank), dst, c->stream));
+        CPDB_CK(cudaStreamSynchronize(c->stream));
+        g.barrier();
+        return;
+    }
+    // one reduce-scatter per outer slice (each slice is contiguous with the
+    // scattered mode outermost), batched into one NCCL group
+    const Nccl& N = nccl();
+    ncclResult_t r = N.GroupStart();
+    for (uint64_t o = 0; o < outer && r == ncclSuccess; ++o)
+        r = N.ReduceScatter(src + o * block, dst + o * chunk, chunk, ncclDouble, ncclSum,
+                            static_cast<ncclComm_t>(c->comm), c->stream);
+    const ncclResult_t r2 = N.GroupEnd();
+    if (r == ncclSuccess) r = r2;
+    if (r != ncclSuccess)
+        fail(CPDB_NCCL_ERROR, std::string("ncclReduceScatter: ") + N.GetErrorString(r));
+}
+
 double ctx_norm_sq(cpdb_ctx* c) {
     require_tensor(c);
     if (c->norm_valid) return c->norm_x_sq;
@@ -318,4 +348,5 @@ cpdb_ctx::~cpdb_ctx() {
     if (mid) cudaStreamDestroy(mid);
     if (aux) cudaStreamDestroy(aux);
     if (zq) cudaStreamDestroy(zq);
+    if (tailq) cudaStreamDestroy(tailq);
 }

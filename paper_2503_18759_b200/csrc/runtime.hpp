@@ -73,12 +73,13 @@ struct Slot {
     bool valid = false;
     std::vector<uint64_t> dims;    // local extents
     std::vector<uint64_t> stamps;  // 0 = mode not absorbed
-    bool sharded = false;          // leading mode free and split across ranks
+    bool sharded = false;          // split across ranks along a free mode (lay.mode)
+    ShardLayout lay;               // replicated / split / partial sums (shard.cpp)
 };
 
 struct Timer {
     cudaEvent_t a = nullptr, b = nullptr;
-    int kind = 0;  // 0 root ttm, 1 branch ttm, 2 comm
+    int kind = 0;  // 0 root ttm, 1 branch ttm, 2 comm, 3 mode-update kernel
     double flops = 0, bytes = 0;
 };
 
@@ -114,12 +115,15 @@ struct cpdb_ctx {
     cudaStream_t mid = nullptr;   // below stream/side: TTM chain beside a multi-kernel Z-QR
     cudaStream_t aux = nullptr;   // speculative next-sweep update beside the last one
     cudaStream_t zq = nullptr;    // the sweep-boundary Z-QR (not behind any chain)
+    cudaStream_t tailq = nullptr;  // a sweep's last update beside the next sweep's first
 
     // sharding: leading mode split in contiguous slabs
     int rank = 0, world = 1;
     void* comm = nullptr;  // ncclComm_t
     std::shared_ptr<cpdb::LocalGroup> group;  // in-process ranks (tests)
     uint64_t row_begin = 0, rows = 0;
+    int32_t shard_policy = 3;          // CPDB_SHARD_* (shard.cpp), default auto
+    cpdb::ShardCost shard_cost;
 
     // X
     const double* x = nullptr;
@@ -155,6 +159,10 @@ void require_tensor(cpdb_ctx* c);
 double ctx_norm_sq(cpdb_ctx* c);
 void allreduce_sum(cpdb_ctx* c, double* dev, size_t n);
 void allgather(cpdb_ctx* c, double* dev_full, size_t per_rank);
+// src: `outer` contiguous blocks of `block` doubles, each the full extent of
+// the scattered mode (outermost within the block); dst: this rank's
+// block/world-sized chunk of every block, summed over the ranks
+void reduce_scatter(cpdb_ctx* c, const double* src, uint64_t outer, uint64_t block, double* dst);
 
 // The device-resident run_qr (solvers.hpp:215-336).
 void solve(cpdb_ctx* c, const cpdb_config& cfg, cpdb_state* state, cpdb_trace_row* trace,

@@ -98,4 +98,40 @@ inline int32_t shard_flags(ModeSet source, uint32_t contract, ModeSet produces, 
     return f;
 }
 
+// ---- sharding planner (shard.cpp): layouts, reductions, cost model ---------
+enum ShardLayKind : int32_t { kLayRep = 0, kLayShard = 1, kLayPartial = 2 };
+struct ShardLayout {
+    int32_t kind = kLayRep;
+    int32_t mode = -1;  // kLayShard: the split free mode
+    bool operator==(const ShardLayout& o) const { return kind == o.kind && mode == o.mode; }
+    bool operator!=(const ShardLayout& o) const { return !(*this == o); }
+};
+enum ShardRed : int32_t { kRedNone = 0, kRedAllReduce = 1, kRedScatter = 2 };
+enum ShardVOp : int32_t { kVNone = 0, kVGather = 1, kVAllReduce = 2 };
+enum ShardPolicy : int32_t { kPolicyEager = 0, kPolicyScatter = 1, kPolicyLazy = 2, kPolicyAuto = 3 };
+struct StepShard {
+    ShardLayout src;      // layout of the step's source (X: sharded along mode 0)
+    ShardLayout out;      // layout of the stored output (after the reduction)
+    int32_t red = kRedNone;
+    int32_t scatter = -1;  // kRedScatter: the free mode the partial is scattered onto
+    uint64_t words = 0;    // doubles of the reduced partial (global size)
+};
+struct UpdateShard {
+    ShardLayout yn;        // layout of Y(n) at the V-GEMM
+    int32_t vop = kVNone;  // V's collective
+    uint64_t vwords = 0;   // I_n x R
+};
+struct ShardCost {
+    double tflops = 30.0;      // FP64 DMMA rate of the TTMs / V-GEMM (per GPU)
+    double bus_gbs = 700.0;    // NCCL bus bandwidth over NVLink 5 / NVSwitch
+    double latency_s = 20e-6;  // per collective
+};
+struct ShardPlan {
+    std::vector<std::vector<std::vector<StepShard>>> steps;  // [sweep][update][step]
+    std::vector<std::vector<UpdateShard>> updates;           // [sweep][update]
+    double est_compute_s = 0.0, est_comm_s = 0.0;            // per rank, whole plan
+};
+ShardPlan plan_shards(const Plan& p, const std::vector<uint64_t>& dims, uint64_t R, int world,
+                      ShardPolicy pol, const ShardCost& cp);
+
 }  // namespace cpdb

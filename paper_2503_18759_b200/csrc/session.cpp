@@ -136,6 +136,7 @@ Session::~Session() {
     if (c && c->mid) cudaStreamSynchronize(c->mid);
     if (c && c->aux) cudaStreamSynchronize(c->aux);
     if (c && c->zq) cudaStreamSynchronize(c->zq);
+    if (c && c->tailq) cudaStreamSynchronize(c->tailq);
     if (ev_fin) cudaEventDestroy(ev_fin);
     if (pf.ev) cudaEventDestroy(pf.ev);
     if (t_start) cudaEventDestroy(t_start);
@@ -143,6 +144,7 @@ Session::~Session() {
     if (ev_zqr) cudaEventDestroy(ev_zqr);
     if (ev_zq) cudaEventDestroy(ev_zq);
     if (ev_aux) cudaEventDestroy(ev_aux);
+    if (ev_tail) cudaEventDestroy(ev_tail);
     for (cudaEvent_t e : ev_fac)
         if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : ev_v)
@@ -169,7 +171,7 @@ void Session::tl_end(cudaEvent_t a, cudaStream_t st, const char* label) {
     cudaEvent_t b;
     CPDB_CK(cudaEventCreate(&b));
     CPDB_CK(cudaEventRecord(b, st));
-    const int sid = st == side ? 1 : st == c->lo ? 2 : st == c->mid ? 3 : st == c->aux ? 4 : st == c->zq ? 5 : 0;
+    const int sid = st == side ? 1 : st == c->lo ? 2 : st == c->mid ? 3 : st == c->aux ? 4 : st == c->zq ? 5 : st == c->tailq ? 6 : 0;
     marks.push_back(Mark{label, sid, tl_sweep, tl_mode, a, b});
 }
 
@@ -206,6 +208,7 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
             hb.name(c->mid, "mid");
             hb.name(c->aux, "aux");
             hb.name(c->zq, "zq");
+            hb.name(c->tailq, "tailq");
             hb.name(nullptr, "legacy");
         }
         fpath = std::getenv("CPDB_FINGERPRINT");
@@ -249,6 +252,20 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         fail(e.code, e.what);
     }
     sharded = c->world > 1;
+    if (sharded) {
+        // layouts, reductions and V collectives of every step (shard.cpp)
+        splan = plan_shards(plan, c->dims, R, c->world,
+                            static_cast<ShardPolicy>(c->shard_policy), c->shard_cost);
+        need_local.assign(order, false);
+        qp_local.resize(order);
+        for (const auto& sw : splan.steps)
+            for (const auto& up : sw)
+                for (const StepShard& st : up)
+                    if (st.src.kind == kLayShard) need_local[uint32_t(st.src.mode)] = true;
+        for (uint32_t m = 0; m < order; ++m)
+            if (need_local[m] && c->dims[m] % uint64_t(c->world) != 0)
+                fail(CPDB_LOGIC_ERROR, "shard plan splits a mode that does not divide");
+    }
     s = c->stream;
     side = c->side;
     zrows = 1;
@@ -292,6 +309,10 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         dep_events = chain_side && !(ef && ef[0] == '0');
         const char* ce = std::getenv("CPDB_CHAIN_EVENTS");
         chain_events = dep_events && !(ce && ce[0] == '0');
+        const char* lt = std::getenv("CPDB_LOW_TAIL");
+        low_tail = !(lt && lt[0] == '0');
+        const char* sh = std::getenv("CPDB_SELF_HIST");
+        self_hist = !(sh && sh[0] == '0');
         const char* sp = std::getenv("CPDB_SPECULATE");
         speculate = !(sp && sp[0] == '0');
         const char* zy = std::getenv("CPDB_ZQR_YIELD");
@@ -365,9 +386,10 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     versions.assign(order, 1);
     CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
     for (uint32_t k = 0; k < order; ++k) qr_factor(k);
-    pack_local0();
+    for (uint32_t k = 0; k < order; ++k) pack_local(k);
     CPDB_CK(cudaEventCreateWithFlags(&ev_zq, cudaEventDisableTiming));
     CPDB_CK(cudaEventCreateWithFlags(&ev_aux, cudaEventDisableTiming));
+    CPDB_CK(cudaEventCreateWithFlags(&ev_tail, cudaEventDisableTiming));
     for (uint32_t k = 0; k < order; ++k) {
         CPDB_CK(cudaEventCreateWithFlags(&ev_fac[k], cudaEventDisableTiming));
         CPDB_CK(cudaEventRecord(ev_fac[k], s));
@@ -430,23 +452,55 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     if (done > 0) {
         for (uint32_t key : retained_keys(plan, done - 1, order - 1)) {
             if (cache.count(key)) continue;
+            // the layout the plan gave the slot when it last produced it
+            ShardLayout want{};
+            if (sharded) {
+                bool found = false;
+                for (uint64_t sw = done; sw-- > 0 && !found;)
+                    for (uint32_t b = order; b-- > 0 && !found;) {
+                        const Update& u = plan.sweeps[sw].updates[b];
+                        for (size_t j = u.steps.size(); j-- > 0;)
+                            if (u.steps[j].produces == key && u.steps[j].produces != (1u << u.mode)) {
+                                want = splan.steps[sw][b][j].out;
+                                found = true;
+                                break;
+                            }
+                    }
+            }
             std::vector<uint64_t> d = c->ldims;
             const double* cur = c->x;
             ModeSet cur_set = plan.root();
+            ShardLayout lay = sharded ? ShardLayout{kLayShard, 0} : ShardLayout{};
             DevBuf tmp[2];
             int w = 0;
             for (uint32_t k = order; k-- > 0;) {
                 if (key & (1u << k)) continue;
+                const ModeSet next = cur_set & ~(1u << k);
+                // X is split along mode 0, which is contracted last: partial
+                // sums at the end only, then brought to the slot's layout
+                StepShard sh{lay, lay, kRedNone, -1, 0};
+                if (lay.kind == kLayShard && uint32_t(lay.mode) == k) {
+                    sh.out = want;
+                    if (want.kind == kLayRep) sh.red = kRedAllReduce;
+                    if (want.kind == kLayShard) {
+                        sh.red = kRedScatter;
+                        sh.scatter = want.mode;
+                    }
+                }
                 std::vector<uint64_t> nd = d;
                 nd[k] = R;
+                if (sh.red == kRedScatter) nd[uint32_t(sh.scatter)] /= uint64_t(c->world);
                 double* out = tmp[w].ensure(numel(nd));
-                const ModeSet next = cur_set & ~(1u << k);
-                ttm_step(cur, d, shard_flags(cur_set, k, next, order, sharded), k, out, false);
+                ttm_step(cur, d, sharded ? &sh : nullptr, k, out, false);
                 cur_set = next;
                 cur = out;
                 d = nd;
+                lay = sh.out;
                 w ^= 1;
             }
+            if (sharded && lay != want)
+                fail(CPDB_LOGIC_ERROR, "resume: cannot rebuild " + set_name(key, order) +
+                                           " in its planned layout");
             Slot& sl = cache[key];
             sl.buf.ensure(numel(d));
             CPDB_CK(cudaMemcpyAsync(sl.buf.p, cur, numel(d) * sizeof(double),
@@ -454,7 +508,8 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
             acc(s, "cache_rebuild_copy", {rg(cur, numel(d))}, {rg(sl.buf.p, numel(d))});
             sl.valid = true;
             sl.dims = d;
-            sl.sharded = set_sharded(key, sharded);
+            sl.lay = lay;
+            sl.sharded = lay.kind == kLayShard;
             sl.stamps.assign(order, 0);
             for (uint32_t k = 0; k < order; ++k)
                 if (!(key & (1u << k))) sl.stamps[k] = versions[k];
@@ -466,7 +521,8 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     // Y_(n) per mode and update parity (consecutive updates of the same mode
     // -- the sweep boundary -- may be in flight together)
     ybuf.resize(2 * order);
-    for (uint32_t n = 0; n < 2 * order; ++n) ybuf[n].ensure(numel(local_dims_of(1u << (n / 2))));
+    for (uint32_t n = 0; n < 2 * order; ++n)
+        ybuf[n].ensure(numel(dims_in(1u << (n / 2), ShardLayout{})));
     // every cache slot the plan will use, allocated now: a first use inside
     // the sweeps would put a cudaMalloc (device-wide sync; C5: 8.6 GB slots)
     // in the middle of the run
@@ -474,10 +530,18 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         const uint64_t span = std::min<uint64_t>(
             plan.sweeps.size(), plan.cycle_start + 2 * std::max<uint64_t>(plan.cycle_length, 1) + 1);
         for (uint64_t sw = 0; sw < span; ++sw)
-            for (const Update& u : plan.sweeps[sw].updates)
-                for (const Step& st : u.steps)
-                    if (st.produces != (1u << u.mode))
-                        cache[st.produces].buf.ensure(numel(local_dims_of(st.produces)));
+            for (uint32_t b = 0; b < plan.sweeps[sw].updates.size(); ++b) {
+                const Update& u = plan.sweeps[sw].updates[b];
+                for (size_t j = 0; j < u.steps.size(); ++j) {
+                    const Step& st = u.steps[j];
+                    if (st.produces == (1u << u.mode)) continue;
+                    // sharded: the slot's size in the layout the plan gives it
+                    // (the largest over the productions in the span)
+                    cache[st.produces].buf.ensure(numel(
+                        sharded ? dims_in(st.produces, splan.steps[sw][b][j].out)
+                                : local_dims_of(st.produces)));
+                }
+            }
         if (prefetch_enabled) {
             uint64_t mx = 0;
             for (uint32_t k = 0; k < order; ++k) {
@@ -519,25 +583,69 @@ void Session::qr_factor(uint32_t k) {
     c->launches += 1;
 }
 
-// Sharded runs contract the leading mode with this rank's rows of Q_0 only;
-// they get their own packed copy (no row-alignment constraint).
-void Session::pack_local0() {
-    if (!sharded) return;
-    qp0_local.ensure(uint64_t(ttm_kpad(c->rows)) * Rp);
-    CPDB_CK(pack_q(fb[0].q.p + c->row_begin * R, qp0_local.p, uint32_t(c->rows), R, s));
+// Sharded runs contract a split mode m with this rank's rows of Q_m only;
+// they get their own packed copy (no row-alignment constraint), refreshed
+// after every update of m.
+void Session::pack_local(uint32_t m) {
+    if (!sharded || !need_local[m]) return;
+    const uint64_t rows = shard_rows_of(m);
+    qp_local[m].ensure(uint64_t(ttm_kpad(rows)) * Rp);
+    CPDB_CK(pack_q(fb[m].q.p + uint64_t(c->rank) * rows * R, qp_local[m].p, uint32_t(rows), R,
+                   s));
     c->launches += 1;
 }
 
-void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32_t flags,
+// CUDA-event pair around a mode-update kernel (Z-QR, V-GEMM, finisher):
+// cpdb_profile.mode_update_ms, with CPDB_TIME_TAILS=1 only (the extra events
+// break the programmatic launch overlap of the tail: C2 -5% sweeps/s).
+Timer Session::tail_timer_begin(cudaStream_t st) {
+    static const bool on = [] {
+        const char* e = std::getenv("CPDB_TIME_TAILS");
+        return e && e[0] == '1';
+    }();
+    Timer t;
+    if (c->timing && on) {
+        t.a = events.get();
+        t.b = events.get();
+        t.kind = 3;
+        CPDB_CK(cudaEventRecord(t.a, st));
+    }
+    return t;
+}
+
+void Session::tail_timer_end(Timer& t, cudaStream_t st) {
+    if (!t.a) return;
+    CPDB_CK(cudaEventRecord(t.b, st));
+    timers.push_back(t);
+}
+
+uint64_t Session::shard_rows_of(uint32_t m) const { return c->dims[m] / uint64_t(c->world); }
+
+// Extents a tensor over free set `key` has on this rank in layout L (free
+// modes I_k, or I_k / world for the split one; contracted modes R).
+std::vector<uint64_t> Session::dims_in(uint32_t key, const ShardLayout& L) const {
+    std::vector<uint64_t> d(order);
+    for (uint32_t k = 0; k < order; ++k)
+        d[k] = !(key & (1u << k))                            ? uint64_t(R)
+               : (L.kind == kLayShard && uint32_t(L.mode) == k) ? shard_rows_of(k)
+                                                                 : c->dims[k];
+    return d;
+}
+
+void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, const StepShard* sh,
                        uint32_t k, double* dst, bool is_root, cudaStream_t st, bool prefetch,
                        bool no_pdl, int sms) {
     if (!st) st = s;
     const double* q = fb[k].q.p;
     const double* qp = fb[k].qp.p;
-    if (k == 0 && (flags & kSrcSharded)) {
-        q += c->row_begin * R;
-        qp = qp0_local.p;
+    if (sh && sh->src.kind == kLayShard && uint32_t(sh->src.mode) == k) {
+        // contracting the split mode: this rank's rows of Q_k -> a partial sum
+        q += uint64_t(c->rank) * shard_rows_of(k) * R;
+        qp = qp_local[k].p;
     }
+    // a reduce-scatter needs the whole partial first
+    double* raw = dst;
+    if (sh && sh->red == kRedScatter) raw = rs_tmp.ensure(numel(sd) / sd[k] * R);
     Timer t;
     if (c->timing) {
         t.a = events.get();
@@ -548,11 +656,11 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32
     cudaEvent_t tla = tl_begin(st);
     fp(st, prefetch ? "root_prefetch" : is_root ? "root_ttm" : "branch_ttm", "in_before",
        {rg(src, numel(sd)), rg(qp, uint64_t(ttm_kpad(sd[k])) * Rp)});
-    run_ttm(c, src, sd, k, q, qp, R, dst, st, prefetch || yield_now, no_pdl, sms,
+    run_ttm(c, src, sd, k, q, qp, R, raw, st, prefetch || yield_now, no_pdl, sms,
             prefetch ? pf.tpc : 0);
     acc(st, prefetch ? "root_prefetch" : is_root ? "root_ttm" : "branch_ttm",
           {rg(src, numel(sd)), rg(qp, uint64_t(ttm_kpad(sd[k])) * Rp)},
-          {rg(dst, numel(sd) / sd[k] * R)});
+          {rg(raw, numel(sd) / sd[k] * R)});
     tl_end(tla, st, prefetch ? "root_prefetch" : is_root ? "root" : "branch");
     if (c->timing) {
         CPDB_CK(cudaEventRecord(t.b, st));
@@ -562,7 +670,7 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32
         t.bytes = 8.0 * (double(nin) + double(nout) + double(sd[k]) * R);
         timers.push_back(t);
     }
-    if (flags & kAllReduce) {
+    if (sh && sh->red != kRedNone) {
         Timer tc;
         if (c->timing) {
             tc.a = events.get();
@@ -570,7 +678,18 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, int32
             tc.kind = 2;
             CPDB_CK(cudaEventRecord(tc.a, s));
         }
-        allreduce_sum(c, dst, numel(sd) / sd[k] * R);
+        std::vector<uint64_t> od = sd;
+        od[k] = R;
+        if (sh->red == kRedAllReduce) {
+            allreduce_sum(c, dst, numel(od));
+        } else {
+            // blocks: everything from the scattered mode inward (contiguous,
+            // that mode outermost), one per index of the modes before it
+            const uint32_t m = uint32_t(sh->scatter);
+            uint64_t outer = 1;
+            for (uint32_t j = 0; j < m; ++j) outer *= od[j];
+            reduce_scatter(c, raw, outer, numel(od) / outer, dst);
+        }
         if (c->timing) {
             CPDB_CK(cudaEventRecord(tc.b, s));
             timers.push_back(tc);
@@ -641,7 +760,7 @@ void Session::prefetch_root(uint64_t sweep, uint32_t b, cudaStream_t after) {
 void Session::launch_prefetch() {
     if (!pf.active || pf.launched) return;
     CPDB_CK(cudaStreamWaitEvent(c->lo, ev_fin, 0));
-    ttm_step(c->x, c->ldims, 0, pf.cm, pre.p, true, c->lo, true, true);
+    ttm_step(c->x, c->ldims, nullptr, pf.cm, pre.p, true, c->lo, true, true);
     CPDB_CK(cudaEventRecord(pf.ev, c->lo));
     pf.launched = true;
 }
@@ -747,6 +866,9 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     // form below (its Z-QR launches programmatically right behind the
     // finisher, measured faster when it has to wait for that finisher anyway).
     early = dep_events && last_mode == int(n);
+    // same deterministic kernel on the same R_k (k != n) as the previous
+    // update of mode n: its Q0 (the history, solvers.hpp:265) is this Q0
+    zb[zpar].hist_is_self = last_mode == int(n) && has_hist[n] && self_hist;
     // (the sweep-boundary Z-QR on its own stream, not behind the previous
     // chain on `side`)
     cudaStream_t zs = early ? c->zq : chain_side ? s : side;
@@ -762,8 +884,10 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         z.ts = reinterpret_cast<unsigned long long*>(zts.ensure(32));
         CPDB_CK(cudaMemsetAsync(z.ts, 0, 32 * sizeof(double), zs));
     }
-    const cudaStream_t ts =
-        early ? c->mid : chain_side ? (zqr_yield ? c->mid : side) : s;
+    const cudaStream_t ts = tail_override ? tail_override
+                            : early       ? c->mid
+                            : chain_side  ? (zqr_yield ? c->mid : side)
+                                          : s;
     if (early) {
         for (uint32_t k = 0; k < order; ++k)
             if (k != n) CPDB_CK(cudaStreamWaitEvent(zs, ev_fac[k], 0));
@@ -813,7 +937,11 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     fp(zs, "zqr", "in_before",
        {rg(z.rmats[0], R * R), rg(z.rmats[1], order > 2 ? R * R : 0),
         rg(z.rmats[2], order > 3 ? R * R : 0), rg(z.rmats[3], order > 4 ? R * R : 0)});
-    CPDB_CK(launch_zqr(z, zs, c->sms));
+    {
+        Timer tt = tail_timer_begin(zs);
+        CPDB_CK(launch_zqr(z, zs, c->sms));
+        tail_timer_end(tt, zs);
+    }
     acc(zs, "zqr",
           {rg(z.rmats[0], R * R), rg(z.rmats[1], order > 2 ? R * R : 0),
            rg(z.rmats[2], order > 3 ? R * R : 0), rg(z.rmats[3], order > 4 ? R * R : 0)},
@@ -854,7 +982,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
         const double* src;
         std::vector<uint64_t> sd;
         std::vector<uint64_t> stamp(order, 0);
-        const int32_t flags = shard_flags(st.source, st.contract, st.produces, n, sharded);
+        const StepShard* sh = sharded ? &splan.steps[sweep - 1][b][si] : nullptr;
         if (st.source == root) {
             src = c->x;
             sd = c->ldims;
@@ -870,11 +998,12 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
             src = it->second.buf.p;
             sd = it->second.dims;
             stamp = it->second.stamps;
-            if (it->second.sharded != bool(flags & kSrcSharded))
+            if (sh && it->second.lay != sh->src)
                 fail(CPDB_LOGIC_ERROR, "execute: shard layout of " + set_name(st.source, order));
         }
         std::vector<uint64_t> od = sd;
         od[st.contract] = R;
+        if (sh && sh->red == kRedScatter) od[uint32_t(sh->scatter)] /= uint64_t(c->world);
         if (si == 0 && pf.active && pf.sweep == sweep && pf.block == b) {
             // issued early by prefetch_root: adopt its buffer as the slot
             launch_prefetch();
@@ -893,7 +1022,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
                 chain_waited |= 1u << st.contract;
                 after_wait = true;
             }
-            ttm_step(src, sd, flags, st.contract, dst, st.source == root, ts, false,
+            ttm_step(src, sd, sh, st.contract, dst, st.source == root, ts, false,
                      after_wait, budget(sweep, b));
             after_wait = false;
             if (dep_events && st.produces != (1u << n))
@@ -911,7 +1040,8 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
             sl.valid = true;
             sl.dims = od;
             sl.stamps = stamp;
-            sl.sharded = (flags & kOutSharded) != 0;
+            sl.lay = sh ? sh->out : ShardLayout{};
+            sl.sharded = sl.lay.kind == kLayShard;
         }
     }
     const std::vector<ModeSet> keep = retained_keys(plan, sweep - 1, b);
@@ -939,12 +1069,16 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     if (use_ex) beta_used = beta;
 
     // 5. V = Y_(n) Q0_hat (+ the unextrapolated V for the fitness, :277-284)
-    const std::vector<uint64_t> yd = local_dims_of(1u << n);
+    const UpdateShard* ush = sharded ? &splan.updates[sweep - 1][b] : nullptr;
+    const std::vector<uint64_t> yd =
+        sharded ? dims_in(1u << n, ush->yn) : local_dims_of(1u << n);
     VgemmArgs v{};
     v.y = ybuf[2 * n + zpar].p;
     ZBuf& zcur = zb[zpar];
     v.q0 = zcur.q0.p;
-    v.hist = maybe_ex ? hist[n].p : nullptr;
+    // (at the sweep boundary the history is this update's own Q0, bit for
+    // bit: the V-GEMM need not wait for the previous update's Z-QR)
+    v.hist = maybe_ex ? (zcur.hist_is_self ? zcur.q0.p : hist[n].p) : nullptr;
     v.beta = beta;
     v.alpha = cfg.alpha;
     v.extrap = maybe_ex ? 1 : 0;
@@ -967,15 +1101,18 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     v.vfitpart = v.dual ? vfitpart[zpar].ensure(part) : nullptr;
     // split-K partials -> V (this rank's rows; sharded mode-0 updates gather
     // the full V on every rank)
-    const bool gather = (shard_flags(0, 0, 1u << n, n, sharded) & kGatherV) != 0;
-    const uint64_t off = gather ? c->row_begin * R : 0;
+    // V's collective: this rank's rows of a split Y(n) are gathered, the
+    // partial V of a partial Y(n) is all-reduced
+    const bool gather = ush && ush->vop == kVGather;
+    const bool vsum = ush && ush->vop == kVAllReduce;
+    const uint64_t off = gather ? uint64_t(c->rank) * yd[n] * R : 0;
     v.v_out = vf.p + off;
     v.vfit_out = v.dual ? vff.p + off : nullptr;
     CPDB_CK(cudaStreamWaitEvent(bs, ev_zqr, 0));
     if (dep_events) CPDB_CK(cudaStreamWaitEvent(bs, ev_zq, 0));  // Q0, R0 ready
     // the history Q0 comes from the previous update of this mode's Z-QR, which
     // nothing else orders before this V-GEMM once the fronts are event-driven
-    if (maybe_ex) CPDB_CK(cudaStreamWaitEvent(bs, ev_hist[n], 0));
+    if (maybe_ex && !zcur.hist_is_self) CPDB_CK(cudaStreamWaitEvent(bs, ev_hist[n], 0));
     tl_sweep = sweep;
     tl_mode = n;
     hb.cur_sweep = sweep;
@@ -987,12 +1124,17 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
         const char* e = std::getenv("CPDB_VSPLIT_MAX");
         return e ? uint32_t(std::atoi(e)) : 16u;
     }();
-    v.max_split = (vsplit_max > 0 && !gather && finish_sums_splits(v.I, R)) ? vsplit_max : 0;
+    v.max_split = (vsplit_max > 0 && !gather && !vsum && finish_sums_splits(v.I, R)) ? vsplit_max
+                                                                                        : 0;
     const int vsms = budget(sweep, b);
     fp(bs, "vgemm", "in_before",
        {rg(v.y, numel(yd)), rg(v.q0, zrows * R), rg(v.hist, v.extrap ? zrows * R : 0),
         rg(v.gate, v.gate ? 4 : 0)});
-    CPDB_CK(launch_vgemm(v, bs, vsms > 0 ? vsms : c->sms));
+    {
+        Timer tt = tail_timer_begin(bs);
+        CPDB_CK(launch_vgemm(v, bs, vsms > 0 ? vsms : c->sms));
+        tail_timer_end(tt, bs);
+    }
     acc(bs, "vgemm",
           {rg(v.y, numel(yd)), rg(v.q0, zrows * R), rg(v.hist, v.extrap ? zrows * R : 0),
            rg(v.gate, v.gate ? 4 : 0)},
@@ -1004,7 +1146,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     if (dep_events) CPDB_CK(cudaEventRecord(ev_v[2 * n + zpar], bs));  // ybuf consumed
     // the cluster finisher sums the split-K partials itself (no reduction
     // launch on the chain); gathered (sharded mode-0) V needs them reduced
-    const bool fused = vsplit_max > 0 && !v.reduced && !gather && v.nsplit <= 64 &&
+    const bool fused = vsplit_max > 0 && !v.reduced && !gather && !vsum && v.nsplit <= 64 &&
                        finish_sums_splits(v.I, R);
     if (!v.reduced && !fused) {
         tla = tl_begin(bs);
@@ -1021,6 +1163,10 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     if (gather) {
         allgather(c, vf.p, v.I * R);
         if (v.dual) allgather(c, vff.p, v.I * R);
+    }
+    if (vsum) {
+        allreduce_sum(c, vf.p, v.I * R);
+        if (v.dual) allreduce_sum(c, vff.p, v.I * R);
     }
     // 6-9. A_hat, lambda, factor QR, fitness (solvers.hpp:272-292)
     FinishArgs f{};
@@ -1054,7 +1200,11 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
         fp(bs, "finish", "in_before",
            {rg(f.vpart, vin), rg(f.vfitpart, f.dual ? vin : 0), rg(f.r0, R * R)});
     }
-    CPDB_CK(launch_finish(f, bs));
+    {
+        Timer tt = tail_timer_begin(bs);
+        CPDB_CK(launch_finish(f, bs));
+        tail_timer_end(tt, bs);
+    }
     {
         const uint64_t vin = uint64_t(f.nsplit) * f.I * R;
         acc(bs, "finish", {rg(f.vpart, vin), rg(f.vfitpart, f.dual ? vin : 0), rg(f.r0, R * R)},
@@ -1075,7 +1225,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
             std::fprintf(stderr, " %d:%.2f", k, ts[k] ? (ts[k] - ts[0]) * 1e-3 : -1.0);
         std::fprintf(stderr, "\n");
     }
-    if (n == 0) pack_local0();
+    pack_local(n);
     if (dep_events) {
         CPDB_CK(cudaEventRecord(ev_fac[n], bs));       // A_n, Q_n, R_n final
         CPDB_CK(cudaEventRecord(ev_zread[zpar], bs));  // Q0 / R0 / history consumed
@@ -1104,17 +1254,30 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         // is then sticky for the whole run instead of reset per sweep)
         if (!front_issued && !dep_events)
             CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
+        // the next sweep's first update will run beside this sweep's last one
+        // (below): the last one then yields to it
+        const bool tail_low = low_tail && dep_events && speculate && !sharded &&
+                              observer == nullptr && fps == nullptr && lps == nullptr &&
+                              (!extrap || has_beta) && rows_out + 1 < nsweeps &&
+                              done + 1 < last_sweep;
         for (uint32_t b = 0; b < order; ++b) {
+            const bool low = tail_low && b == order - 1;
             if (b == 0 && front_issued) {
                 front_issued = false;  // issued ahead of the previous sweep's host sync
             } else if (b == 1 && front1_issued) {
                 front1_issued = false;
             } else {
+                if (low) tail_override = c->tailq;
                 mode_update_front(sweep, b, observer, user);
+                tail_override = nullptr;
             }
             if (b == 0 && spec.issued) {
                 spec.issued = false;  // issued (whole) ahead of the previous sweep's host sync
                 beta_used = spec.beta_used;
+            } else if (low) {
+                mode_update_back(sweep, b, beta_used, c->tailq);
+                CPDB_CK(cudaEventRecord(ev_tail, c->tailq));
+                CPDB_CK(cudaStreamWaitEvent(s, ev_tail, 0));
             } else {
                 mode_update_back(sweep, b, beta_used);
             }
@@ -1213,6 +1376,8 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
                 c->prof.root_ttm_bytes += t.bytes;
             } else if (t.kind == 1) {
                 c->prof.branch_ttm_ms += tm;
+            } else if (t.kind == 3) {
+                c->prof.mode_update_ms += tm;
             } else {
                 c->prof.comm_ms += tm;
             }
@@ -1270,8 +1435,6 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         std::fprintf(stderr, "cpdb hbcheck: %llu sweeps checked, %llu violations\n",
                      (unsigned long long)(done - first_sweep), (unsigned long long)hb.violations);
     c->prof.sweeps = done - first_sweep;
-    c->prof.mode_update_ms =
-        c->prof.solve_ms - c->prof.root_ttm_ms - c->prof.branch_ttm_ms - c->prof.comm_ms;
     c->prof.kernel_launches = c->launches - launches0;
     return rows_out;
 }

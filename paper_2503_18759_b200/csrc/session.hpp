@@ -46,7 +46,14 @@ struct Session {
     // (the next sweep's first, before the host has read this sweep's fitness)
     // can be undone by swapping back when the stop test fires.
     std::vector<FactorBufs> fb_alt;
-    DevBuf lam, lam_alt, qp0_local, tsbuf, zts;
+    DevBuf lam, lam_alt, tsbuf, zts;
+    // sharded runs: the layout / reduction plan of every step
+    // (shard.cpp), this rank's packed rows of each split Q_m, and the whole
+    // partial of a step whose output is reduce-scattered
+    ShardPlan splan;
+    std::vector<bool> need_local;
+    std::vector<DevBuf> qp_local;
+    DevBuf rs_tmp;
     DevBuf gate;  // {has_beta, beta, has_prev, prev_fitness} on the device (beta_gate)
     // the next sweep's first update issued before the host read this sweep's
     // fitness (Session::run); what undoing it needs
@@ -58,11 +65,23 @@ struct Session {
         double beta_used = 0.0;  // its trace contribution, once the host knows the gate
     } spec;
     bool speculate = false;  // CPDB_SPECULATE=0 turns it off
+    bool self_hist = true;   // CPDB_SELF_HIST=0: always wait for the history's own Z-QR
+    // The sweep's last update while the next sweep's first update runs beside
+    // it (beta frozen): off the critical path (it only yields this sweep's
+    // fitness), so its chain, V-GEMM and finisher go on c->tailq, below the
+    // next update's kernels (CPDB_LOW_TAIL=0: off)
+    bool low_tail = true;
+    cudaStream_t tail_override = nullptr;
+    cudaEvent_t ev_tail = nullptr;
     DevBuf fscratch[2], vpart[2], vfitpart[2], vfull[2], vfitfull[2], vout, fitbuf;
     // Z-QR outputs, double-buffered so the next update's Z-QR can run while
     // this update's V-GEMM / finisher still read Q0 and R0
     struct ZBuf {
         DevBuf q0, q1, r0, work;
+        // the previous update was of the same mode (sweep boundary): no R_k
+        // it reads changed since that update's Z-QR, so its Q0 -- this
+        // mode's extrapolation history -- equals this Z-QR's Q0 bit for bit
+        bool hist_is_self = false;
     } zb[2];
     int zpar = 0;  // parity of the update in flight (set by the front, used by the back)
     // Dependency events of the event-driven schedule (dep_events): the
@@ -176,8 +195,10 @@ struct Session {
 private:
     std::vector<uint64_t> local_dims_of(uint32_t key) const;
     void qr_factor(uint32_t k);
-    void pack_local0();
-    void ttm_step(const double* src, const std::vector<uint64_t>& sd, int32_t flags,
+    void pack_local(uint32_t m);
+    uint64_t shard_rows_of(uint32_t m) const;
+    std::vector<uint64_t> dims_in(uint32_t key, const ShardLayout& L) const;
+    void ttm_step(const double* src, const std::vector<uint64_t>& sd, const StepShard* sh,
                   uint32_t k, double* dst, bool is_root, cudaStream_t st = nullptr,
                   bool prefetch = false, bool no_pdl = false, int sms = 0);
     void prefetch_root(uint64_t sweep, uint32_t b, cudaStream_t after);
@@ -189,6 +210,8 @@ private:
     void mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cudaStream_t bs = nullptr,
                           bool host_beta = false);
     void undo_speculative_update();
+    Timer tail_timer_begin(cudaStream_t st);
+    void tail_timer_end(Timer& t, cudaStream_t st);
 };
 
 }  // namespace cpdb

@@ -588,6 +588,33 @@ cudaError_t sum_slots(const double* slots, uint64_t stride, uint32_t world, uint
     return cudaGetLastError();
 }
 
+namespace {
+// dst[o * chunk + j] = sum_r slots[r * stride + o * block + rank * chunk + j]
+__global__ void sum_slots_scatter_kernel(const double* slots, uint64_t stride, uint32_t world,
+                                         uint64_t outer, uint64_t block, uint64_t chunk,
+                                         uint32_t rank, double* out) {
+    const uint64_t n = outer * chunk;
+    for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < n;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        const uint64_t o = e / chunk, j = e % chunk;
+        const uint64_t src = o * block + uint64_t(rank) * chunk + j;
+        double v = 0.0;
+        for (uint32_t r = 0; r < world; ++r) v += slots[r * stride + src];
+        out[e] = v;
+    }
+}
+}  // namespace
+
+cudaError_t sum_slots_scatter(const double* slots, uint64_t stride, uint32_t world,
+                              uint64_t outer, uint64_t block, uint64_t chunk, uint32_t rank,
+                              double* out, cudaStream_t s) {
+    const uint64_t n = outer * chunk;
+    const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, 1024));
+    sum_slots_scatter_kernel<<<std::max(grid, 1u), 256, 0, s>>>(slots, stride, world, outer,
+                                                                block, chunk, rank, out);
+    return cudaGetLastError();
+}
+
 uint32_t vgemm_max_split() { return 296; }
 
 namespace {

@@ -291,7 +291,9 @@ cudaError_t launch_v2(const TtmArgs& a, cudaStream_t s, int sms) {
         const cuuint64_t strides[3] = {a.inner * 8, 64, a.K * a.inner * 8};
         cuuint32_t box[4];
         if (gpo >= uint64_t(C::G)) {
-            if (gpo % C::G != 0) return cudaErrorNotSupported;  // a tile would straddle two o
+            // a tile would straddle two o (outer == 1: the last tile's
+            // columns past the end are zero-filled and not stored)
+            if (gpo % C::G != 0 && a.outer != 1) return cudaErrorNotSupported;
             box[0] = 8; box[1] = BK; box[2] = C::G; box[3] = 1;
         } else {
             if (C::G % gpo != 0) return cudaErrorNotSupported;
@@ -302,6 +304,7 @@ cudaError_t launch_v2(const TtmArgs& a, cudaStream_t s, int sms) {
                 box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     } else {
+        if (C::BJ > 256 && C::BJ % 256 != 0) return cudaErrorNotSupported;  // partial box
         const cuuint64_t dims[3] = {4, a.outer, a.K / 4};
         const cuuint64_t strides[2] = {a.K * 8, 32};
         const cuuint32_t box[3] = {4, cuuint32_t(C::BJ <= 256 ? C::BJ : 256),
@@ -378,33 +381,61 @@ uint64_t tiles_with(const TtmArgs& a, int cb, int nc) {
     return (cols + per - 1) / per;
 }
 
-// Pick the widest tile (CB0, CB0/2, CB0/4) that still fills the GPU: score =
-// SM utilisation of the last wave x a per-CB efficiency (narrower tiles
-// re-load Q fragments more often per DMMA).  Branch TTMs on the R-sized
-// intermediates are small (C2: 64 tiles at CB 4), so they drop to CB 2.
+// Whether a tile of nc*cb 8-column groups fits the kGroups box rule (a tile
+// never straddles two o unless there is only one).
+template <int LAYOUT>
+bool tile_ok(const TtmArgs& a, int cb, int nc) {
+    // kRows boxes carry at most 256 rows: wider tiles take whole boxes
+    if (LAYOUT != kGroups) return nc * cb * 8 <= 256 || (nc * cb * 8) % 256 == 0;
+    const uint64_t g = uint64_t(nc) * cb, gpo = a.inner / 8;
+    return gpo >= g ? (gpo % g == 0 || a.outer == 1) : (g % gpo == 0);
+}
+
+// Pick the tile (CB0, CB0/2, CB0/4 column blocks per warp; 8 or 7 consumer
+// warps) that best fills the GPU: score = SM utilisation of the last wave x
+// a per-CB efficiency (narrower tiles re-load Q fragments more often per
+// DMMA).  Branch TTMs on the R-sized intermediates are small (C2: 16384 rows
+// -> 64 tiles at CB 4, 128 at CB 2 = 86% of 148 SMs); 7 consumer warps make
+// 112-row tiles, 147 of them (99%).
 template <int RB, int CB0, int BK, int ST, int LAYOUT>
 cudaError_t launch_adaptive(const TtmArgs& a, cudaStream_t s, int sms) {
-    constexpr int NC = 8;
-    int best = CB0;
+    int best = CB0, best_nc = 8;
     double best_score = -1.0;
-    for (int cb = CB0; cb >= 1 && cb >= CB0 / 4; cb /= 2) {
-        const uint64_t t = tiles_with<LAYOUT>(a, cb, NC);
-        const double waves = std::ceil(double(t) / sms);
-        const double util = double(t) / (waves * sms);
-        const double eff = cb == CB0 ? 1.0 : (cb == CB0 / 2 ? 0.9 : 0.7);
-        const double score = util * eff;
-        if (score > best_score + 1e-9) {
-            best_score = score;
-            best = cb;
+    static const bool nc7 = [] {
+        const char* e = std::getenv("CPDB_TTM_NC7");
+        return !(e && e[0] == '0');
+    }();
+    for (int nc = 8; nc >= (nc7 ? 7 : 8); --nc)
+        for (int cb = CB0; cb >= 1 && cb >= CB0 / 4; cb /= 2) {
+            if (!tile_ok<LAYOUT>(a, cb, nc)) continue;
+            const uint64_t t = tiles_with<LAYOUT>(a, cb, nc);
+            const double waves = std::ceil(double(t) / sms);
+            const double util = double(t) / (waves * sms);
+            const double eff = (cb == CB0 ? 1.0 : (cb == CB0 / 2 ? 0.9 : 0.7)) *
+                               (nc == 8 ? 1.0 : 0.97);
+            const double score = util * eff;
+            if (score > best_score + 1e-9) {
+                best_score = score;
+                best = cb;
+                best_nc = nc;
+            }
         }
+    if (best_nc == 7) {
+        if constexpr (CB0 >= 4) {
+            if (best == CB0 / 4) return launch_v2<RB, CB0 / 4, BK, ST, 7, LAYOUT>(a, s, sms);
+        }
+        if constexpr (CB0 >= 2) {
+            if (best == CB0 / 2) return launch_v2<RB, CB0 / 2, BK, ST, 7, LAYOUT>(a, s, sms);
+        }
+        return launch_v2<RB, CB0, BK, ST, 7, LAYOUT>(a, s, sms);
     }
     if constexpr (CB0 >= 4) {
-        if (best == CB0 / 4) return launch_v2<RB, CB0 / 4, BK, ST, NC, LAYOUT>(a, s, sms);
+        if (best == CB0 / 4) return launch_v2<RB, CB0 / 4, BK, ST, 8, LAYOUT>(a, s, sms);
     }
     if constexpr (CB0 >= 2) {
-        if (best == CB0 / 2) return launch_v2<RB, CB0 / 2, BK, ST, NC, LAYOUT>(a, s, sms);
+        if (best == CB0 / 2) return launch_v2<RB, CB0 / 2, BK, ST, 8, LAYOUT>(a, s, sms);
     }
-    return launch_v2<RB, CB0, BK, ST, NC, LAYOUT>(a, s, sms);
+    return launch_v2<RB, CB0, BK, ST, 8, LAYOUT>(a, s, sms);
 }
 
 template <int LAYOUT>

@@ -33,6 +33,7 @@ def run_ranks(ctxs, fn):
     return out
 
 
+@pytest.mark.parametrize("policy", ["eager", "scatter", "lazy", "auto"])
 @pytest.mark.parametrize("dims,rank,world,variant", [
     ((16, 12, 10), 3, 2, "bre"),
     ((24, 20, 16), 5, 4, "bre"),
@@ -41,8 +42,12 @@ def run_ranks(ctxs, fn):
     ((12, 10, 8, 6), 3, 2, "dim-tree"),
     ((128, 96, 64), 16, 4, "bre"),
     ((32, 24, 24, 20), 8, 8, "bre"),
+    ((16, 16, 16, 16), 64 // 4, 4, "bre"),
 ])
-def test_sharded_matches_unsharded(ctx, port, dims, rank, world, variant):
+def test_sharded_matches_unsharded(ctx, port, dims, rank, world, variant, policy):
+    """Every reduction strategy of the sharded session (csrc/shard.cpp: eager
+    all-reduce, reduce-scatter onto a free mode, lazy reduction at V, and the
+    cost model's per-step choice) gives the unsharded trajectory."""
     import paper_2503_18759_b200 as cpd
     x = port.synth_baseline(0, dims, rank, 1e-2, 20250003)
     strategy = "branch-reuse" if variant == "bre" else variant
@@ -52,8 +57,11 @@ def test_sharded_matches_unsharded(ctx, port, dims, rank, world, variant):
     ref = ctx.solve(cfg, extrapolate=ext)
     rows = dims[0] // world
     group = cpd.Context.local_group(0, world)
+    # slow modelled links make "auto" mix all three strategies on these sizes
+    cost = {"bus_gbs": 0.05} if policy == "auto" else None
 
     def rank_run(r, c):
+        c.set_shard_policy(policy, cost)
         c.set_tensor(np.ascontiguousarray(x[r * rows:(r + 1) * rows]), dims)
         return c.solve(cfg, extrapolate=ext)
 
@@ -132,5 +140,40 @@ def test_sharded_stop_test_undoes_speculative_update(ctx, port, dims, world):
         for fa, fb in zip(g.model.factors, ref.model.factors):
             assert np.linalg.norm(fa - fb) <= 1e-10 * np.linalg.norm(fb)
         assert np.linalg.norm(g.model.lam - ref.model.lam) <= 1e-10 * np.linalg.norm(ref.model.lam)
+    for c in group:
+        c.close()
+
+
+@pytest.mark.parametrize("policy", ["eager", "scatter", "lazy", "auto"])
+@pytest.mark.parametrize("k", [3, 4, 5])
+def test_sharded_resume_rebuilds_planned_layouts(ctx, port, policy, k):
+    """A sharded session resumed from a sweep-boundary state rebuilds every
+    retained intermediate in the layout the plan gave it (split, replicated
+    or partial sums) and continues the unsharded trajectory."""
+    import paper_2503_18759_b200 as cpd
+    dims, rank, world = (16, 12, 8, 8), 4, 4
+    x = port.synth_baseline(0, dims, rank, 1e-2, 20250021)
+    cfg = cpd.SolverConfig(rank=rank, max_iterations=k + 3, seed=7)
+    ctx.set_tensor(x)
+    ref = ctx.solve(cfg, extrapolate=True)
+    first = ctx.solve(cpd.SolverConfig(rank=rank, max_iterations=k, seed=7), extrapolate=True)
+    rows = dims[0] // world
+    group = cpd.Context.local_group(0, world)
+    cost = {"bus_gbs": 0.05} if policy == "auto" else None
+
+    def rank_run(r, c):
+        c.set_shard_policy(policy, cost)
+        c.set_tensor(np.ascontiguousarray(x[r * rows:(r + 1) * rows]), dims)
+        return c.solve(cpd.SolverConfig(rank=rank, max_iterations=3, seed=7), extrapolate=True,
+                       state=first.state)
+
+    res = run_ranks(group, rank_run)
+    for g in res:
+        assert len(g.trace) == 3
+        for a, b in zip(g.trace, ref.trace[k:]):
+            assert a.iteration == b.iteration and a.flops == b.flops
+            assert abs(a.fitness - b.fitness) <= 1e-10 * b.fitness
+        for fa, fb in zip(g.model.factors, ref.model.factors):
+            assert np.linalg.norm(fa - fb) <= 1e-10 * np.linalg.norm(fb)
     for c in group:
         c.close()

@@ -165,3 +165,149 @@ def test_sharded_chain_gloo_world2(order, strategy):
     while not errq.empty():
         errs.append(errq.get())
     assert all(p.exitcode == 0 for p in procs), errs
+
+
+# ---------------------------------------------------------------- reduction strategies
+POLICIES = ["eager", "scatter", "lazy", "auto"]
+
+
+def _slab(t, mode, rank, world):
+    n = t.shape[mode] // world
+    return np.take(t, np.arange(rank * n, (rank + 1) * n), axis=mode)
+
+
+def _rank_main_ex(rank, world, port, order, strategy, sweeps, policy, dims, errq):
+    """Execute cpdb_shard_plan_ex's layouts with numpy TTMs and gloo
+    collectives: partial sums all-reduced, reduce-scattered (all-reduce +
+    this rank's slab of the scatter mode) or carried on; V of a sharded Y(n)
+    gathered, of a partial one all-reduced.  Every V must equal the
+    unsharded run's."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        R = 3
+        rng = np.random.default_rng(17)
+        x = rng.standard_normal(dims)
+        qs = [np.linalg.qr(rng.standard_normal((d, R)))[0] for d in dims]
+        q0 = rng.standard_normal((R ** (order - 1), R))
+        sched = cpd.build_schedule(order, strategy, sweeps)
+        plan = cpd.shard_plan_ex(order, strategy, sweeps, dims, R, world, policy,
+                                 cost={"bus_gbs": 0.05})  # slow links: every strategy shows up
+        root = (1 << order) - 1
+        xl = _slab(x, 0, rank, world)
+        cache = {}
+        i = u = 0
+
+        def allreduce(a):
+            t = torch.from_numpy(np.ascontiguousarray(a))
+            dist.all_reduce(t)
+            return t.numpy()
+
+        for it in range(sweeps):
+            for up in sched.iteration(it):
+                for st in up.steps:
+                    rec = plan["steps"][i]
+                    i += 1
+                    src, lay = (xl, ("sharded", 0)) if st.source == root else cache[st.source]
+                    assert rec["src"] == lay, (it, up.mode, rec, lay)
+                    c = st.contract_mode
+                    q = qs[c]
+                    if lay == ("sharded", c):
+                        q = _slab(q, 0, rank, world)
+                    out = ttm(src, q, c)
+                    if rec["reduction"] == "allreduce":
+                        out = allreduce(out)
+                    elif rec["reduction"] == "scatter":
+                        out = _slab(allreduce(out), rec["scatter_mode"], rank, world)
+                    out_lay = rec["out"]
+                    if st.produces == (1 << up.mode):
+                        yn, ylay = out, out_lay
+                    else:
+                        cache[st.produces] = (out, out_lay)
+                vop = plan["v_ops"][u]
+                u += 1
+                n = up.mode
+                unf = np.moveaxis(yn, n, 0).reshape(yn.shape[n], -1)
+                v = unf @ q0
+                if vop == "gather":
+                    assert ylay == ("sharded", n)
+                    parts = [torch.zeros_like(torch.from_numpy(v)) for _ in range(world)]
+                    dist.all_gather(parts, torch.from_numpy(np.ascontiguousarray(v)))
+                    v = np.concatenate([p.numpy() for p in parts], axis=0)
+                elif vop == "allreduce":
+                    assert ylay[0] == "partial"
+                    v = allreduce(v)
+                else:
+                    assert ylay[0] == "replicated"
+                want = x
+                for k in range(order):
+                    if k != n:
+                        want = ttm(want, qs[k], k)
+                vw = np.moveaxis(want, n, 0).reshape(want.shape[n], -1) @ q0
+                np.testing.assert_allclose(v, vw, rtol=1e-12, atol=1e-12)
+                qs[n] = np.linalg.qr(np.random.default_rng(100 * it + n).standard_normal(
+                    (dims[n], R)))[0]
+                cache = {k: v_ for k, v_ in cache.items() if k >> n & 1}
+        assert i == len(plan["steps"]) and u == len(plan["v_ops"])
+    except Exception as e:  # surfaced to the parent
+        errq.put(f"rank {rank}: {e!r}")
+        raise
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("policy", POLICIES)
+@pytest.mark.parametrize("order,strategy", [(3, "branch-reuse"), (4, "branch-reuse"),
+                                            (4, "dim-tree")])
+def test_reduction_strategies_gloo_world2(order, strategy, policy):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    errq = ctx.Queue()
+    port = _free_port()
+    dims = [8, 6, 4, 4][:order]
+    procs = [ctx.Process(target=_rank_main_ex,
+                         args=(r, 2, port, order, strategy, 5, policy, dims, errq))
+             for r in range(2)]
+    for p in procs:
+        p.start()
+    for p in procs:
+        p.join(240)
+    errs = []
+    while not errq.empty():
+        errs.append(errq.get())
+    assert all(p.exitcode == 0 for p in procs), errs
+
+
+def test_strategy_rules_and_costs_c5():
+    """Row e of SURVEY.md 8 for config 5 (256^4, R 64, mode-1 shards): the
+    per-sweep exchange of each strategy against the survey's table, and the
+    cost model's choice.  Eager all-reduces 8.59 GB + 2.15 GB in the sweep
+    whose root contracts mode 1; reduce-scatter moves the same partials once
+    (half the bytes) and keeps the downstream TTMs divided; lazy exchanges
+    only V (I_n x R per update) but replicates the downstream work; auto is
+    never worse than any fixed strategy under its own model."""
+    dims, R = (256,) * 4, 64
+    tot = {}
+    for pol in POLICIES:
+        r = cpd.shard_plan_ex(4, "branch-reuse", 12, dims, R, 8, pol)
+        tot[pol] = r["est_compute_s"] + r["est_comm_s"]
+        for s in r["steps"]:
+            if s["reduction"] == "scatter":
+                assert s["out"] == ("sharded", s["scatter_mode"]) and s["scatter_mode"] != 0
+            if s["src"] == ("sharded", 0) and s["reduction"] is None:
+                assert s["out"][0] in ("sharded", "partial")
+        if pol == "eager":
+            assert max(s["words"] for s in r["steps"]) * 8 == 64 * 256 ** 3 * 8
+            assert all(s["out"][0] != "partial" for s in r["steps"])
+        if pol == "lazy":
+            assert all(s["reduction"] is None for s in r["steps"])
+            assert set(r["v_ops"]) <= {"gather", "allreduce", None}
+    assert tot["auto"] <= min(tot[p] for p in ("eager", "scatter", "lazy")) + 1e-12
+    assert tot["auto"] < tot["eager"]
+    # one rank: nothing is sharded, reduced or exchanged
+    r1 = cpd.shard_plan_ex(4, "branch-reuse", 6, dims, R, 1, "auto")
+    assert all(s["reduction"] is None and s["out"][0] == "replicated" for s in r1["steps"])
+    assert r1["est_comm_s"] == 0.0

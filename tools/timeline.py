@@ -37,7 +37,7 @@ s = ctx.session(cpd.SolverConfig(rank=c["rank"], max_iterations=a.warmup + a.swe
                                  seed=bench.INIT_SEED), extrapolate=True)
 rows = s.run(a.warmup + a.sweeps)
 s.close()
-names = {0: "main", 1: "side", 2: "lo", 3: "mid", 4: "aux", 5: "zq"}
+names = {0: "main", 1: "side", 2: "lo", 3: "mid", 4: "aux", 5: "zq", 6: "tail"}
 recs = []
 for line in open(path):
     lab, st, sw, mode, t0, t1 = line.strip().split(",")
