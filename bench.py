@@ -154,6 +154,9 @@ def init_dist():
     if world > 1:
         import torch.distributed as dist
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        # NCCL's communicator set-up lines (rank / nranks per comm) in the log
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("gloo", rank=rank, world_size=world)
     return rank, world, local
 
@@ -404,7 +407,11 @@ def main():
             "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (device generator, BASELINE construction)",
             "config": {"workload": workload_name(args.config, c), "dims": dims,
-                       "rank": c["rank"], "parallelism": f"mode-1 shards x{world}",
+                       "rank": c["rank"],
+                       "parallelism": f"mode-1 shards x{world}" + (
+                           f", reductions: {os.environ.get('CPDB_SHARD_POLICY', 'auto')} "
+                           "(eager all-reduce / reduce-scatter / lazy at V, per step)"
+                           if world > 1 else ""),
                        "l2": f"X = {np.prod(dims) * 8 / 1e9:.2f} GB > 126 MB L2: every sweep "
                              f"streams X from HBM, no flush needed"},
             "roofline": roof,

@@ -311,6 +311,15 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         chain_events = dep_events && !(ce && ce[0] == '0');
         const char* lt = std::getenv("CPDB_LOW_TAIL");
         low_tail = !(lt && lt[0] == '0');
+        // the low tail's TTM chain and V-GEMM take this many SMs (stream
+        // priority alone does not keep its grids, launched first, from
+        // interleaving with the next sweep's first update)
+        const char* tsm = std::getenv("CPDB_TAIL_SMS");
+        tail_sms = tsm ? std::atoi(tsm) : 40;
+        {
+            const double xe = double(numel(c->ldims));
+            long_root = std::max(2.0 * xe * R / 31.5e12, 8.0 * xe / 6.0e12) >= 150e-6;
+        }
         const char* sh = std::getenv("CPDB_SELF_HIST");
         self_hist = !(sh && sh[0] == '0');
         const char* sp = std::getenv("CPDB_SPECULATE");
@@ -1023,7 +1032,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
                 after_wait = true;
             }
             ttm_step(src, sd, sh, st.contract, dst, st.source == root, ts, false,
-                     after_wait, budget(sweep, b));
+                     after_wait, tail_override ? tail_sms : budget(sweep, b));
             after_wait = false;
             if (dep_events && st.produces != (1u << n))
                 CPDB_CK(cudaEventRecord(ready_event(st.produces), ts));
@@ -1126,7 +1135,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     }();
     v.max_split = (vsplit_max > 0 && !gather && !vsum && finish_sums_splits(v.I, R)) ? vsplit_max
                                                                                         : 0;
-    const int vsms = budget(sweep, b);
+    const int vsms = bs == c->tailq && tail_sms > 0 ? tail_sms : budget(sweep, b);
     fp(bs, "vgemm", "in_before",
        {rg(v.y, numel(yd)), rg(v.q0, zrows * R), rg(v.hist, v.extrap ? zrows * R : 0),
         rg(v.gate, v.gate ? 4 : 0)});
@@ -1256,7 +1265,9 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
             CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
         // the next sweep's first update will run beside this sweep's last one
         // (below): the last one then yields to it
-        const bool tail_low = low_tail && dep_events && speculate && !sharded &&
+        // (long roots only: with a short root (C4) the last update is on the
+        // critical path again -- measured C4 -4%, C2 +2.7%)
+        const bool tail_low = low_tail && long_root && dep_events && speculate && !sharded &&
                               observer == nullptr && fps == nullptr && lps == nullptr &&
                               (!extrap || has_beta) && rows_out + 1 < nsweeps &&
                               done + 1 < last_sweep;

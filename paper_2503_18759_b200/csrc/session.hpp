@@ -71,6 +71,8 @@ struct Session {
     // fitness), so its chain, V-GEMM and finisher go on c->tailq, below the
     // next update's kernels (CPDB_LOW_TAIL=0: off)
     bool low_tail = true;
+    bool long_root = false;  // the root TTM takes >= 150 us (estimate)
+    int tail_sms = 40;       // CPDB_TAIL_SMS: SM budget of the low tail's TTMs / V-GEMM
     cudaStream_t tail_override = nullptr;
     cudaEvent_t ev_tail = nullptr;
     DevBuf fscratch[2], vpart[2], vfitpart[2], vfull[2], vfitfull[2], vout, fitbuf;

@@ -401,9 +401,12 @@ template <int RB, int CB0, int BK, int ST, int LAYOUT>
 cudaError_t launch_adaptive(const TtmArgs& a, cudaStream_t s, int sms) {
     int best = CB0, best_nc = 8;
     double best_score = -1.0;
+    // opt-in (CPDB_TTM_NC7=1): measured at C2, 147-CTA branch TTMs leave no
+    // SMs for the concurrent 8-CTA cluster kernels and lose 1.2% sweeps/s
+    // against 128-CTA ones
     static const bool nc7 = [] {
         const char* e = std::getenv("CPDB_TTM_NC7");
-        return !(e && e[0] == '0');
+        return e && e[0] == '1';
     }();
     for (int nc = 8; nc >= (nc7 ? 7 : 8); --nc)
         for (int cb = CB0; cb >= 1 && cb >= CB0 / 4; cb /= 2) {

@@ -151,12 +151,16 @@ def test_sharded_resume_rebuilds_planned_layouts(ctx, port, policy, k):
     retained intermediate in the layout the plan gave it (split, replicated
     or partial sums) and continues the unsharded trajectory."""
     import paper_2503_18759_b200 as cpd
+    from test_gpu_solver import port_init
     dims, rank, world = (16, 12, 8, 8), 4, 4
     x = port.synth_baseline(0, dims, rank, 1e-2, 20250021)
+    init = cpd.SweepState(0, np.ones(rank), port_init(port, dims, rank, 7))
     cfg = cpd.SolverConfig(rank=rank, max_iterations=k + 3, seed=7)
     ctx.set_tensor(x)
-    ref = ctx.solve(cfg, extrapolate=True)
-    first = ctx.solve(cpd.SolverConfig(rank=rank, max_iterations=k, seed=7), extrapolate=True)
+    ref = ctx.solve(cfg, extrapolate=True, state=init)
+    first = ctx.solve(cpd.SolverConfig(rank=rank, max_iterations=k, seed=7), extrapolate=True,
+                      state=init)
+    assert first.state.sweeps_done == k
     rows = dims[0] // world
     group = cpd.Context.local_group(0, world)
     cost = {"bus_gbs": 0.05} if policy == "auto" else None
