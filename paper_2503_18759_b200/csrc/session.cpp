@@ -315,7 +315,7 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         // priority alone does not keep its grids, launched first, from
         // interleaving with the next sweep's first update)
         const char* tsm = std::getenv("CPDB_TAIL_SMS");
-        tail_sms = tsm ? std::atoi(tsm) : 40;
+        tail_sms = tsm ? std::atoi(tsm) : 80;
         {
             const double xe = double(numel(c->ldims));
             long_root = std::max(2.0 * xe * R / 31.5e12, 8.0 * xe / 6.0e12) >= 150e-6;
@@ -393,7 +393,11 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     if (extrap)
         for (DevBuf& b : vfitpart) b.ensure(size_t(vgemm_max_split()) * maxI * R);
     versions.assign(order, 1);
-    CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
+    CPDB_CK(cudaMemsetAsync(c->dstatus, 0, 5 * sizeof(int), s));
+    {
+        const char* fe = std::getenv("CPDB_FAULT_SWEEP");
+        fault_sweep = fe ? std::strtoull(fe, nullptr, 10) : 0;
+    }
     for (uint32_t k = 0; k < order; ++k) qr_factor(k);
     for (uint32_t k = 0; k < order; ++k) pack_local(k);
     CPDB_CK(cudaEventCreateWithFlags(&ev_zq, cudaEventDisableTiming));
@@ -583,7 +587,7 @@ void Session::qr_factor(uint32_t k) {
     f.r_out = fb[k].r.p;
     f.lambda = lam.p;
     f.scratch = fscratch[0].p;
-    f.status = c->dstatus;
+    f.status = status_word(done + 1);  // reported with the first sweep
     f.v_out = vout.p;
     CPDB_CK(launch_finish(f, s));
     acc(s, "qr_factor", {rg(f.a_out, f.I * R)},
@@ -862,7 +866,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     z.q0 = zcur.q0.p;
     z.r0 = zcur.r0.p;
     z.work = zcur.work.p;
-    z.status = c->dstatus;
+    z.status = status_word(sweep);
     // Z-QR depends only on R_k (k != n), final since the previous update's
     // finisher, and overlaps the TTM chain on a second stream.  Unsharded, the
     // Z-QR follows the finisher on the main stream (programmatic launch: its
@@ -1197,7 +1201,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     f.fitness = last ? 1 : 0;
     f.norm_x_sq = nx2;
     f.fit_out = fitbuf.p;
-    f.status = c->dstatus;
+    f.status = status_word(sweep);
     static const bool trace_phases = std::getenv("CPDB_PHASE_TRACE") != nullptr;
     if (trace_phases) {
         f.ts = reinterpret_cast<unsigned long long*>(tsbuf.ensure(32));
@@ -1223,6 +1227,8 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     }
     tl_end(tla, bs, "finish");
     c->launches += 1;
+    if (fault_sweep == sweep && b == 0)  // test hook: a breakdown in this update
+        CPDB_CK(cudaMemsetAsync(status_word(sweep), 2, 1, bs));
     fb[n].swap(fb_alt[n]);  // the new factor state (the old one stays for undo)
     lam.swap(lam_alt);
     if (trace_phases) {
@@ -1259,15 +1265,14 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         const uint64_t sweep = done + 1;
         const Sweep& sw = plan.sweeps[sweep - 1];
         double beta_used = 0.0;
-        // (event-driven fronts run ahead of the stream order: the status word
-        // is then sticky for the whole run instead of reset per sweep)
-        if (!front_issued && !dep_events)
-            CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
         // the next sweep's first update will run beside this sweep's last one
         // (below): the last one then yields to it
         // (long roots only: with a short root (C4) the last update is on the
         // critical path again -- measured C4 -4%, C2 +2.7%)
-        const bool tail_low = low_tail && long_root && dep_events && speculate && !sharded &&
+        // (third order only: a fourth-order sweep's last update carries the
+        // heavy TTMs itself -- C5 -13% with it budgeted, C3 flat)
+        const bool tail_low = low_tail && long_root && order == 3 && dep_events && speculate &&
+                              !sharded &&
                               observer == nullptr && fps == nullptr && lps == nullptr &&
                               (!extrap || has_beta) && rows_out + 1 < nsweeps &&
                               done + 1 < last_sweep;
@@ -1304,7 +1309,8 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         CPDB_CK(cudaEventRecord(e_end, s));
         CPDB_CK(cudaMemcpyAsync(c->pinned, fitbuf.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
         acc(s, "fitness_d2h", {rg(fitbuf.p, 2)}, {});
-        CPDB_CK(cudaMemcpyAsync(c->pinned + 2, c->dstatus, sizeof(int), cudaMemcpyDeviceToHost, s));
+        CPDB_CK(cudaMemcpyAsync(c->pinned + 2, status_word(sweep), sizeof(int),
+                                cudaMemcpyDeviceToHost, s));
         cudaEvent_t e_fit = events.get();
         CPDB_CK(cudaEventRecord(e_fit, s));
         const Cost at_end = total;
@@ -1314,7 +1320,6 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         // host waits for this sweep's fitness (wasted only if it converges).
         const bool more = rows_out + 1 < nsweeps && done + 1 < last_sweep;
         if (more && observer == nullptr && fps == nullptr) {
-            if (!dep_events) CPDB_CK(cudaMemsetAsync(c->dstatus, 0, sizeof(int), s));
             mode_update_front(sweep + 1, 0, nullptr, nullptr);
             front_issued = true;
             // ... and, with the beta decision taken on the device, its V-GEMM
@@ -1361,6 +1366,13 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         CPDB_CK(cudaEventSynchronize(e_fit));
         int status;
         std::memcpy(&status, c->pinned + 2, sizeof(int));
+        // the word is free again for sweep + 4, whose first kernels the host
+        // issues only after it has synchronised on sweep + 2's fitness, i.e.
+        // after this clear (no device-side wait needed).  The next sweep's
+        // speculative work has its own word, so a breakdown in an update the
+        // reference never runs -- undone when the stop test fires -- is never
+        // reported.
+        CPDB_CK(cudaMemsetAsync(status_word(sweep), 0, sizeof(int), s));
         if (status) {
             if ((status & 0xFF) == 1)
                 fail(CPDB_SINGULAR_TRIANGULAR,
@@ -1466,6 +1478,9 @@ void Session::undo_speculative_update() {
     --versions[n];
     last_mode = spec.prev_last_mode;
     spec.issued = false;
+    // whatever the undone update reported is moot
+    CPDB_CK(cudaMemsetAsync(status_word(done + 1), 0, sizeof(int), s));
+    CPDB_CK(cudaStreamSynchronize(s));
 }
 
 // ---------------------------------------------------------------- results

@@ -72,8 +72,13 @@ struct Session {
     // next update's kernels (CPDB_LOW_TAIL=0: off)
     bool low_tail = true;
     bool long_root = false;  // the root TTM takes >= 150 us (estimate)
-    int tail_sms = 40;       // CPDB_TAIL_SMS: SM budget of the low tail's TTMs / V-GEMM
+    int tail_sms = 80;       // CPDB_TAIL_SMS: SM budget of the low tail's TTMs / V-GEMM
     cudaStream_t tail_override = nullptr;
+    // Device status words (Cholesky breakdown / singular R0), a ring of four:
+    // a sweep's kernels write word 1 + (sweep & 3), the host reads it when it
+    // consumes that sweep and then clears it (Session::run)
+    int* status_word(uint64_t sweep) const { return c->dstatus + 1 + (sweep & 3); }
+    uint64_t fault_sweep = 0;  // CPDB_FAULT_SWEEP=k: test hook, a breakdown in sweep k's first update
     cudaEvent_t ev_tail = nullptr;
     DevBuf fscratch[2], vpart[2], vfitpart[2], vfull[2], vfitfull[2], vout, fitbuf;
     // Z-QR outputs, double-buffered so the next update's Z-QR can run while

@@ -15,6 +15,7 @@
 // Small Z (C1-C4) runs as one 8-CTA cluster kernel (cluster.cu); this file is
 // the multi-kernel path for tall Z (C5: 262144 x 64).
 #include <algorithm>
+#include <cstdlib>
 
 #include "kernels.hpp"
 #include "rowalg.cuh"
@@ -26,29 +27,63 @@ constexpr int kNT = 512;
 constexpr int kTile = 256;      // Z rows staged per tile (fewer when R is large)
 constexpr int kMaxParts = 296;  // G2 partials (one per CTA)
 
-// work layout (doubles): [U1 | G2 -> U2 | partials of G2 ...]
+// work layout (doubles): [U1 | G2 -> U2 | W1 = U1^-1 | W2 = U2^-1 | partials of G2 ...]
+constexpr int kPartOff = 4;  // partials start at kPartOff * R * R
+// W = U^-1 for upper-triangular U (R x R, stride R, R <= 64, in shared
+// memory): rows of W from the last up, W[i][j] = -(sum_{k=i+1..j} U[i][k]
+// W[k][j]) / U[i][i], the columns j of a row in parallel, NT/64 threads per
+// column summing fixed strided subsets combined by a fixed shuffle butterfly
+// (deterministic); w: R x R shared scratch, dinv: R shared.  The result is
+// written to `out` (global, stride R).
+template <int NT>
+__device__ void upper_inverse(const double* u, int R, double* w, double* dinv, double* out) {
+    constexpr int TPC = NT / 64;
+    for (int e = threadIdx.x; e < R * R; e += NT) w[e] = 0.0;
+    for (int i = threadIdx.x; i < R; i += NT) dinv[i] = 1.0 / u[i * R + i];
+    __syncthreads();
+    const int j = threadIdx.x / TPC, sub = threadIdx.x % TPC;
+#pragma unroll 1
+    for (int i = R - 1; i >= 0; --i) {
+        double acc = 0.0;
+        if (j < R && j > i)
+#pragma unroll 1
+            for (int k = i + 1 + sub; k <= j; k += TPC) acc = fma(u[i * R + k], w[k * R + j], acc);
+#pragma unroll
+        for (int o = TPC / 2; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (sub == 0 && j < R && j >= i) w[i * R + j] = j == i ? dinv[i] : -acc * dinv[i];
+        __syncthreads();
+    }
+    for (int e = threadIdx.x; e < R * R; e += NT) out[e] = w[e];
+}
+
 template <int RM>
 __global__ void __launch_bounds__(kNT) zqr_prep_kernel(ZqrArgs a) {
     extern __shared__ double sm[];
     const int R = a.R, nm = a.nm;
     double* g = sm;
+    // G1 = Hadamard_k R_k^T R_k: each R_k staged (behind g's R x R, the
+    // inverse's scratch later) and its Gram on DMMA (gram_dmma), the last
+    // mode's first
+    double* stage = g + R * R;
+    double* gk = stage + R * R;
 #pragma unroll 1
-    for (int e = threadIdx.x; e < R * R; e += kNT) {
-        const int p = e / R, q = e % R;
-        const int lo = p < q ? p : q, hi = p < q ? q : p;
-        double h = 1.0;
-        for (int t = nm - 1; t >= 0; --t) {
-            const double* m = a.rmats[t];
-            double s = 0.0;
-            for (int k = 0; k <= lo; ++k) s = fma(m[k * R + lo], m[k * R + hi], s);
-            h = (t == nm - 1) ? s : h * s;
-        }
-        g[e] = h;
+    for (int t = nm - 1; t >= 0; --t) {
+        __syncthreads();
+#pragma unroll 1
+        for (int e = threadIdx.x; e < R * R; e += kNT) stage[e] = a.rmats[t][e];
+        __syncthreads();
+        gram_dmma<kNT>(stage, R, R, R, gk, R);
+        __syncthreads();
+#pragma unroll 1
+        for (int e = threadIdx.x; e < R * R; e += kNT) g[e] = t == nm - 1 ? gk[e] : g[e] * gk[e];
     }
     __syncthreads();
     if (!chol<kNT, RM>(g, R, R) && threadIdx.x == 0) *a.status = 2;
 #pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) a.work[e] = g[e];
+    __syncthreads();
+    // W1 = U1^-1 (the GEMM form of Q1 = Z U1^-1)
+    upper_inverse<kNT>(g, R, g + R * R, g + 2 * R * R, a.work + 2 * R * R);
 }
 
 // Q1 = Z U1^-1 tile by tile; per-CTA partial G2 = Q1^T Q1 on DMMA.
@@ -109,15 +144,176 @@ __global__ void __launch_bounds__(kNT) zqr_rows_kernel(ZqrArgs a, int tile_rows)
         gram_dmma<kNT>(tile, ld, rows, R, part, R, true);
     }
     __syncthreads();
-    double* out = a.work + 2 * R * R + size_t(blockIdx.x) * R * R;
+    double* out = a.work + kPartOff * R * R + size_t(blockIdx.x) * R * R;
 #pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) out[e] = part[e];
+}
+
+// Q1 = Z W1 on the FP64 tensor cores (W1 = U1^-1 from zqr_prep), tile by
+// tile of kGT rows: the tile of Z is built in shared memory from the rows of
+// the R_k (the fastest digit's R_k staged, the slower ones read through L2),
+// multiplied by the staged W1 (DMMA m8n8k4, warp w owns rows 8w..8w+7), Q1
+// stored, and the tile's Gram added to this CTA's G2 partial (DMMA, fixed
+// order).  Replaces the row-by-row register substitution (zqr_rows_kernel,
+// CPDB_ZQR_GEMM=0; C5: 0.62 ms per update).
+constexpr int kGT = 128;  // rows per tile (16 warps x 8)
+template <int RM>
+struct ZgSmem {
+    static constexpr int LD = RM + 4;  // padded rows: conflict-free fragments
+    static constexpr size_t doubles(int R) {
+        return size_t(RM) * LD + size_t(kGT) * LD + 2 * size_t(R) * R +
+               size_t(kGT / R + 2) * R;
+    }
+};
+
+template <int RM>
+__global__ void __launch_bounds__(kNT) zqr_rows_gemm_kernel(ZqrArgs a) {
+    constexpr int LD = ZgSmem<RM>::LD, NB = RM / 8;
+    extern __shared__ double sm[];
+    const int R = a.R, nm = a.nm;
+    double* w1 = sm;                // RM x LD
+    double* zt = w1 + RM * LD;      // kGT x LD: Z tile, then Q1 tile
+    double* fast = zt + kGT * LD;   // R x R: the fastest digit's R_k
+    double* part = fast + R * R;    // R x R: this CTA's G2 partial
+    double* slow = part + R * R;    // (kGT / R + 2) x R: products of the slower digits' rows
+    const double* wsrc = a.work + 2 * R * R;
+#pragma unroll 1
+    for (int e = threadIdx.x; e < RM * RM; e += kNT) {
+        const int i = e / RM, j = e % RM;
+        w1[i * LD + j] = (i < R && j < R) ? wsrc[i * R + j] : 0.0;
+    }
+#pragma unroll 1
+    for (int e = threadIdx.x; e < R * R; e += kNT) {
+        fast[e] = a.rmats[nm - 1][e];
+        part[e] = 0.0;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m = lane >> 2, kq = lane & 3;
+    const uint64_t ntiles = (a.zrows + kGT - 1) / kGT;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint64_t row0 = t * kGT;
+        const int rows = int(min(uint64_t(kGT), a.zrows - row0));
+        __syncthreads();  // the previous tile's Gram is done with zt / slow
+        // Z row t = R_{nm-1}[t % R] * P[t / R], P[q] = the product of the
+        // slower digits' rows of q (the next slower first): one product per
+        // group of R consecutive rows, then one multiply per element
+        const uint32_t g0 = uint32_t(row0) / uint32_t(R);
+        const int ng = int((uint32_t(row0) + uint32_t(rows) - 1) / uint32_t(R) - g0) + 1;
+#pragma unroll 1
+        for (int e = threadIdx.x; e < ng * R; e += kNT) {
+            const int gi = e / R, c = e % R;
+            uint32_t rem = g0 + uint32_t(gi);
+            double v = 1.0;
+#pragma unroll 1
+            for (int k = nm - 2; k >= 0; --k) {
+                const uint32_t qt = rem / uint32_t(R);
+                const double m = a.rmats[k][int(rem - qt * uint32_t(R)) * R + c];
+                v = (k == nm - 2) ? m : v * m;
+                rem = qt;
+            }
+            slow[e] = v;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int e = threadIdx.x; e < kGT * RM; e += kNT) {
+            const int r = e / RM, c = e % RM;
+            double v = 0.0;
+            if (r < rows && c < R) {
+                const uint32_t t = uint32_t(row0) + uint32_t(r);
+                const uint32_t q = t / uint32_t(R);
+                v = fast[int(t - q * uint32_t(R)) * R + c] * slow[int(q - g0) * R + c];
+            }
+            zt[r * LD + c] = v;
+        }
+        __syncthreads();
+        double acc[NB][2];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
+#pragma unroll
+        for (int k4 = 0; k4 < RM / 4; ++k4) {
+            const double av = zt[(warp * 8 + m) * LD + 4 * k4 + kq];
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+                dmma(acc[b][0], acc[b][1], av, w1[(4 * k4 + kq) * LD + b * 8 + m]);
+        }
+        __syncthreads();  // every warp done reading the Z tile
+        {
+            const int r = warp * 8 + m;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                const int c = b * 8 + 2 * kq;
+                zt[r * LD + c] = acc[b][0];
+                zt[r * LD + c + 1] = acc[b][1];
+                if (r < rows) {
+                    double* q = a.q1 + (row0 + r) * R;
+                    if (c < R) q[c] = acc[b][0];
+                    if (c + 1 < R) q[c + 1] = acc[b][1];
+                }
+            }
+        }
+        __syncthreads();
+        gram_dmma<kNT>(zt, LD, rows, R, part, R, true);
+    }
+    __syncthreads();
+    double* out = a.work + kPartOff * R * R + size_t(blockIdx.x) * R * R;
+#pragma unroll 1
+    for (int e = threadIdx.x; e < R * R; e += kNT) out[e] = part[e];
+}
+
+// Q0 = Q1 W2 (W2 = U2^-1, near the identity) on DMMA, kGT rows per tile.
+template <int RM>
+__global__ void __launch_bounds__(kNT, 2) zqr_apply_gemm_kernel(ZqrArgs a) {
+    constexpr int LD = ZgSmem<RM>::LD, NB = RM / 8;
+    extern __shared__ double sm[];
+    const int R = a.R;
+    double* w2 = sm;            // RM x LD
+    double* qt = w2 + RM * LD;  // kGT x LD
+    const double* wsrc = a.work + 3 * R * R;
+#pragma unroll 1
+    for (int e = threadIdx.x; e < RM * RM; e += kNT) {
+        const int i = e / RM, j = e % RM;
+        w2[i * LD + j] = (i < R && j < R) ? wsrc[i * R + j] : 0.0;
+    }
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m = lane >> 2, kq = lane & 3;
+    const uint64_t ntiles = (a.zrows + kGT - 1) / kGT;
+    for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const uint64_t row0 = t * kGT;
+        const int rows = int(min(uint64_t(kGT), a.zrows - row0));
+        __syncthreads();
+#pragma unroll
+        for (int e = threadIdx.x; e < kGT * RM; e += kNT) {
+            const int r = e / RM, c = e % RM;
+            qt[r * LD + c] = (r < rows && c < R) ? __ldcs(a.q1 + (row0 + r) * R + c) : 0.0;
+        }
+        __syncthreads();
+        double acc[NB][2];
+#pragma unroll
+        for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
+#pragma unroll
+        for (int k4 = 0; k4 < RM / 4; ++k4) {
+            const double av = qt[(warp * 8 + m) * LD + 4 * k4 + kq];
+#pragma unroll
+            for (int b = 0; b < NB; ++b)
+                dmma(acc[b][0], acc[b][1], av, w2[(4 * k4 + kq) * LD + b * 8 + m]);
+        }
+        const int r = warp * 8 + m;
+        if (r < rows) {
+            double* q = a.q0 + (row0 + r) * R;
+#pragma unroll
+            for (int b = 0; b < NB; ++b) {
+                const int c = b * 8 + 2 * kq;
+                if (c < R) q[c] = acc[b][0];
+                if (c + 1 < R) q[c + 1] = acc[b][1];
+            }
+        }
+    }
 }
 
 __global__ void __launch_bounds__(kNT) zqr_reduce_kernel(ZqrArgs a, int nparts) {
     const int R2 = a.R * a.R;
     for (int e = blockIdx.x * kNT + threadIdx.x; e < R2; e += gridDim.x * kNT) {
-        const double* p = a.work + 2 * R2 + e;
+        const double* p = a.work + kPartOff * R2 + e;
         double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
         int b = 0;
         for (; b + 3 < nparts; b += 4) {
@@ -156,6 +352,9 @@ __global__ void __launch_bounds__(kNT) zqr_fin_kernel(ZqrArgs a) {
         a.r0[e] = i <= j ? s : 0.0;
         a.work[R * R + e] = g[e];  // U2
     }
+    __syncthreads();
+    // W2 = U2^-1 (the GEMM apply); g + 2R^2 .. is the series' scratch, free now
+    upper_inverse<kNT>(g, R, g + 2 * R * R, g + 3 * R * R, a.work + 3 * R * R);
 }
 
 // Q0 = Q1 U2^-1, one lane group per row
@@ -193,24 +392,53 @@ cudaError_t run_multi(const ZqrArgs& a, cudaStream_t s, int sms) {
     cudaError_t e = cudaFuncSetAttribute(zqr_rows_kernel<RM>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     if (e != cudaSuccess) return e;
-    zqr_prep_kernel<RM><<<1, kNT, size_t(R) * R * sizeof(double), s>>>(a);
-    const uint64_t ntiles = (a.zrows + tile - 1) / tile;
-    const int grid = int(std::min<uint64_t>(ntiles, uint64_t(std::min(2 * sms, kMaxParts))));
-    zqr_rows_kernel<RM><<<grid, kNT, rows_smem, s>>>(a, tile);
+    static const bool gemm = [] {
+        const char* v = std::getenv("CPDB_ZQR_GEMM");
+        return !(v && v[0] == '0');
+    }();
+    const size_t psm = (3 * size_t(R) * R + R) * sizeof(double);
+    e = cudaFuncSetAttribute(zqr_prep_kernel<RM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int((3 * size_t(RM) * RM + RM) * sizeof(double)));
+    if (e != cudaSuccess) return e;
+    zqr_prep_kernel<RM><<<1, kNT, psm, s>>>(a);
+    int grid;
+    if (gemm) {
+        const size_t gsm = ZgSmem<RM>::doubles(R) * sizeof(double);
+        e = cudaFuncSetAttribute(zqr_rows_gemm_kernel<RM>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(gsm));
+        if (e != cudaSuccess) return e;
+        const uint64_t ntiles = (a.zrows + kGT - 1) / kGT;
+        grid = int(std::min<uint64_t>(ntiles, uint64_t(std::min(sms, kMaxParts))));
+        zqr_rows_gemm_kernel<RM><<<grid, kNT, gsm, s>>>(a);
+    } else {
+        const uint64_t ntiles = (a.zrows + tile - 1) / tile;
+        grid = int(std::min<uint64_t>(ntiles, uint64_t(std::min(2 * sms, kMaxParts))));
+        zqr_rows_kernel<RM><<<grid, kNT, rows_smem, s>>>(a, tile);
+    }
     zqr_reduce_kernel<<<(R * R + kNT - 1) / kNT, kNT, 0, s>>>(a, grid);
     e = cudaFuncSetAttribute(zqr_fin_kernel<RM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(4 * RM * RM * sizeof(double)));
     if (e != cudaSuccess) return e;
     zqr_fin_kernel<RM><<<1, kNT, 4 * size_t(R) * R * sizeof(double), s>>>(a);
-    const uint64_t groups = (a.zrows + (kNT / LaneRow<RM>::T) - 1) / (kNT / LaneRow<RM>::T);
-    const int agrid = int(std::min<uint64_t>(groups, uint64_t(4 * sms)));
-    zqr_apply_kernel<RM><<<agrid, kNT, 0, s>>>(a);
+    if (gemm) {
+        const size_t asm_ = size_t(RM + kGT) * ZgSmem<RM>::LD * sizeof(double);
+        e = cudaFuncSetAttribute(zqr_apply_gemm_kernel<RM>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, int(asm_));
+        if (e != cudaSuccess) return e;
+        const uint64_t ntiles = (a.zrows + kGT - 1) / kGT;
+        const int agrid = int(std::min<uint64_t>(ntiles, uint64_t(2 * sms)));  // 2 per SM
+        zqr_apply_gemm_kernel<RM><<<agrid, kNT, asm_, s>>>(a);
+    } else {
+        const uint64_t groups = (a.zrows + (kNT / LaneRow<RM>::T) - 1) / (kNT / LaneRow<RM>::T);
+        const int agrid = int(std::min<uint64_t>(groups, uint64_t(4 * sms)));
+        zqr_apply_kernel<RM><<<agrid, kNT, 0, s>>>(a);
+    }
     return cudaGetLastError();
 }
 
 }  // namespace
 
-size_t zqr_work_doubles(uint32_t R) { return size_t(2 + kMaxParts) * R * R; }
+size_t zqr_work_doubles(uint32_t R) { return size_t(kPartOff + kMaxParts) * R * R; }
 
 cudaError_t launch_zqr(const ZqrArgs& a, cudaStream_t s, int sms) {
     if (zqr_cluster_fits(a.zrows, a.R, a.nm)) return launch_zqr_cluster(a, s);

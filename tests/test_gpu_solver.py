@@ -413,3 +413,26 @@ def test_full_length_parity(port, name):
     ob = [t["iteration"] for t in o.trace if t["beta_used"] != 0.0]
     assert fb[:1] == ob[:1] and len(fb) == len(ob)
     ctx.close()
+
+
+@pytest.mark.parametrize("dims", [(40, 36, 32), (20, 18, 16, 14)])
+def test_breakdown_in_undone_update_is_not_reported(ctx, port, monkeypatch, dims):
+    """The next sweep's first update runs speculatively before the host reads
+    this sweep's fitness; its status word is its own (one per sweep parity).
+    A breakdown there (CPDB_FAULT_SWEEP injects one) after the stop test
+    fired is discarded with the undone update -- the converged model comes
+    back -- while the same breakdown in a sweep that is consumed raises, as
+    the reference would (linalg.hpp:199-203)."""
+    import paper_2503_18759_b200 as cpd
+    x = port.synth_baseline(0, dims, 3, 1e-2, 20250011)
+    f = [t["fitness"] for t in port.solve(x, 3, 10, extrapolate=True, seed=5).trace]
+    k = max(i + 1 for i in range(2, 10) if f[i] - f[i - 1] > 1e-9)
+    thr = 0.5 * (f[k - 2] + f[k - 1])
+    o = port.solve(x, 3, 40, extrapolate=True, seed=5, fitness_threshold=thr)
+    assert len(o.trace) == k
+    monkeypatch.setenv("CPDB_FAULT_SWEEP", str(k + 1))
+    g = cpd.als_qr_bre(x, cfg_of(3, 40, seed=5, fitness_threshold=thr), ctx=ctx)
+    compare(g, o)
+    monkeypatch.setenv("CPDB_FAULT_SWEEP", str(k - 1))
+    with pytest.raises(cpd.SingularTriangularError):
+        cpd.als_qr_bre(x, cfg_of(3, 40, seed=5, fitness_threshold=thr), ctx=ctx)
