@@ -283,6 +283,208 @@ __device__ __forceinline__ void vgemm_tile(const VgemmArgs& a, uint64_t i0, uint
     }
 }
 
+// ---------------------------------------------------------------- wide V-GEMM
+// Tall-K V = Y_(n) P for R in (32, 64] (C5: I 256, K = R^3 = 262144): one CTA
+// per K-chunk holds up to 256 rows of V (128 for the dual form), so P (Q0,
+// extrapolated on the fly) is read once per chunk instead of once per 64-row
+// block.  16 warps; warp w owns a 32-row x 32-column block of V (32 x 16 of
+// V and of Vfit for the dual form): per 4-k step 4 A + 4 B fragment loads
+// feed 16 DMMAs.  Y
+// tiles (16 k) stream in through cp.async into a 3-stage ring; P (and F =
+// Q0 for the dual form) go through registers because the extrapolation
+// P = Q0 + beta (Q0 - alpha H) is applied on the way (the same expression
+// as the reference, solvers.hpp:75-86).  Y layouts: J % 16 == 0 (a 16-k tile
+// is 16 consecutive j of one o: rows i contiguous in k, smem [i][k]) or
+// J == 1 (k = o: 16 rows of I contiguous i, smem [k][i]); other shapes use
+// vgemm_dmma_kernel.  Split-K partials are summed by reduce_splits.
+constexpr int kWT = 512, kWK = 16, kWStages = 3;
+constexpr int kWLdA = kWK + 4;    // smem [i][k] row stride (J % 16 == 0)
+constexpr int kWLdP = 64 + 4;     // P / F tile [k][c]
+template <bool DUAL>
+struct WideCfg {
+    static constexpr int WI = DUAL ? 128 : 256;  // rows of V per CTA
+    static constexpr int LdB = WI + 4;           // smem [k][i] row stride (J == 1)
+    static constexpr int YS = WI * kWLdA > kWK * LdB ? WI * kWLdA : kWK * LdB;  // doubles / Y stage
+    static constexpr size_t smem() {
+        return (size_t(kWStages) * YS + size_t(kWStages) * kWK * kWLdP * (DUAL ? 2 : 1)) *
+               sizeof(double);
+    }
+};
+
+__device__ __forceinline__ void cp_async16(void* dst, const void* src, bool valid) {
+    const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(dst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(d), "l"(src),
+                 "r"(valid ? 16 : 0)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <bool DUAL>
+__global__ void __launch_bounds__(kWT, 1) vgemm_wide_kernel(VgemmArgs a, uint64_t kchunk) {
+    constexpr int kWI = WideCfg<DUAL>::WI, kWLdB = WideCfg<DUAL>::LdB, kWYS = WideCfg<DUAL>::YS;
+    extern __shared__ __align__(16) double wsm[];
+    double* ys = wsm;                           // kWStages x kWYS
+    double* ps = ys + kWStages * kWYS;          // kWStages x 16 x kWLdP
+    double* fs = ps + kWStages * kWK * kWLdP;   // (DUAL) kWStages x 16 x kWLdP
+    const int R = int(a.R);
+    const uint64_t I = a.I, J = a.J;
+    const uint64_t K = a.O * a.J;
+    const uint64_t i0 = uint64_t(blockIdx.y) * kWI;
+    const uint64_t kb = uint64_t(blockIdx.x) * kchunk;
+    const uint64_t ke = min(K, kb + kchunk);
+    const int ntile = int((ke - kb + kWK - 1) / kWK);
+    const bool jrun = J != 1;  // J % 16 == 0 (host-checked)
+    const bool ex = extrap_on(a);
+    const double beta = extrap_beta(a);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int m = lane >> 2, kq = lane & 3;
+    // warp tile: rows rw0.., cols cw0..
+    constexpr int WR = 32, WC = DUAL ? 16 : 32;
+    constexpr int RBW = WR / 8, CBW = WC / 8;
+    const int rw0 = (warp % (kWI / WR)) * WR, cw0 = (warp / (kWI / WR)) * WC;
+
+    // issue the loads of tile t into stage st (Y by cp.async; P/F to registers)
+    auto load_y = [&](int t, int st) {
+        const uint64_t k0 = kb + uint64_t(t) * kWK;
+        double* dst = ys + st * kWYS;
+        if (jrun) {
+            // 256 rows x 16 k = 256 x 8 chunks of 16 B
+            const uint64_t o = k0 / J, j0 = k0 - o * J;
+#pragma unroll
+            for (int u = 0; u < (kWI * kWK / 2) / kWT; ++u) {
+                const int e = threadIdx.x + u * kWT;
+                const int r = e >> 3, c2 = (e & 7) * 2;
+                const uint64_t i = i0 + r;
+                const bool ok = i < I && k0 + c2 < ke;
+                const double* src = a.y + ((o * I + (ok ? i : 0)) * J + j0 + (ok ? c2 : 0));
+                cp_async16(dst + r * kWLdA + c2, src, ok);
+            }
+        } else {
+            // 16 k x 256 rows: J == 1, row o of Y is I contiguous i
+#pragma unroll
+            for (int u = 0; u < (kWI * kWK / 2) / kWT; ++u) {
+                const int e = threadIdx.x + u * kWT;
+                const int kk = e / (kWI / 2), r2 = (e % (kWI / 2)) * 2;
+                const uint64_t i = i0 + r2;
+                const bool ok = k0 + kk < ke && i + 1 < I + 1 && i < I;
+                const double* src = a.y + ((ok ? k0 + kk : 0) * I + (ok ? i : 0));
+                cp_async16(dst + kk * kWLdB + r2, src, ok);
+            }
+        }
+    };
+    constexpr int PPT = (kWK * 64 + kWT - 1) / kWT;  // 2 P elements per thread
+    auto load_p = [&](int t, double (&pr)[PPT], double (&fr)[PPT]) {
+        const uint64_t k0 = kb + uint64_t(t) * kWK;
+#pragma unroll
+        for (int u = 0; u < PPT; ++u) {
+            const int e = threadIdx.x + u * kWT;
+            const int kk = e >> 6, c = e & 63;
+            const uint64_t k = k0 + kk;
+            double q = 0.0, p = 0.0;
+            if (k < ke && c < R) {
+                q = __ldg(a.q0 + k * R + c);
+                p = ex ? q + beta * (q - a.alpha * __ldg(a.hist + k * R + c)) : q;
+            }
+            pr[u] = p;
+            fr[u] = q;
+        }
+    };
+    auto stash_p = [&](int st, const double (&pr)[PPT], const double (&fr)[PPT]) {
+#pragma unroll
+        for (int u = 0; u < PPT; ++u) {
+            const int e = threadIdx.x + u * kWT;
+            const int kk = e >> 6, c = e & 63;
+            ps[(st * kWK + kk) * kWLdP + c] = pr[u];
+            if (DUAL) fs[(st * kWK + kk) * kWLdP + c] = fr[u];
+        }
+    };
+
+    double acc[RBW][CBW][2], accf[DUAL ? RBW : 1][DUAL ? CBW : 1][2];
+#pragma unroll
+    for (int x = 0; x < RBW; ++x)
+#pragma unroll
+        for (int y = 0; y < CBW; ++y) {
+            acc[x][y][0] = acc[x][y][1] = 0.0;
+            if (DUAL) accf[x][y][0] = accf[x][y][1] = 0.0;
+        }
+
+    double pr[PPT], fr[PPT];
+    // prologue: stages 0 .. kWStages-2
+#pragma unroll
+    for (int t = 0; t < kWStages - 1; ++t) {
+        if (t < ntile) {
+            load_y(t, t);
+            load_p(t, pr, fr);
+            stash_p(t, pr, fr);
+        }
+        cp_async_commit();
+    }
+    for (int t = 0; t < ntile; ++t) {
+        const int st = t % kWStages;
+        const int tn = t + kWStages - 1;
+        const bool more = tn < ntile;
+        if (more) load_p(tn, pr, fr);  // registers, in flight during the MMAs
+        cp_async_wait<kWStages - 2>();
+        __syncthreads();  // tile t landed; stage (t-1) % S free for reuse
+        if (more) load_y(tn, tn % kWStages);
+        cp_async_commit();
+        const double* y = ys + st * kWYS;
+        const double* p = ps + st * kWK * kWLdP;
+        const double* f = fs + st * kWK * kWLdP;
+#pragma unroll
+        for (int k4 = 0; k4 < kWK / 4; ++k4) {
+            double af[RBW];
+#pragma unroll
+            for (int x = 0; x < RBW; ++x) {
+                const int r = rw0 + x * 8 + m, kk = 4 * k4 + kq;
+                af[x] = jrun ? y[r * kWLdA + kk] : y[kk * kWLdB + r];
+            }
+#pragma unroll
+            for (int yb = 0; yb < CBW; ++yb) {
+                const int c = cw0 + yb * 8 + m, kk = 4 * k4 + kq;
+                const double bv = p[kk * kWLdP + c];
+#pragma unroll
+                for (int x = 0; x < RBW; ++x) dmma(acc[x][yb][0], acc[x][yb][1], af[x], bv);
+                if (DUAL) {
+                    const double fv = f[kk * kWLdP + c];
+#pragma unroll
+                    for (int x = 0; x < RBW; ++x) dmma(accf[x][yb][0], accf[x][yb][1], af[x], fv);
+                }
+            }
+        }
+        if (more) stash_p(tn % kWStages, pr, fr);  // its stage was last read at t - 1
+    }
+    cp_async_wait<0>();
+    // partials of this K-chunk
+    double* vp = a.vpart + uint64_t(blockIdx.x) * I * R;
+    double* fp = DUAL ? a.vfitpart + uint64_t(blockIdx.x) * I * R : nullptr;
+#pragma unroll
+    for (int x = 0; x < RBW; ++x) {
+        const uint64_t i = i0 + rw0 + x * 8 + m;
+        if (i >= I) continue;
+#pragma unroll
+        for (int yb = 0; yb < CBW; ++yb) {
+            const int c = cw0 + yb * 8 + 2 * kq;
+            if (c < R) {
+                vp[i * R + c] = acc[x][yb][0];
+                if (DUAL) fp[i * R + c] = accf[x][yb][0];
+            }
+            if (c + 1 < R) {
+                vp[i * R + c + 1] = acc[x][yb][1];
+                if (DUAL) fp[i * R + c + 1] = accf[x][yb][1];
+            }
+        }
+    }
+}
+
+size_t vgemm_wide_smem(bool dual) {
+    return dual ? WideCfg<true>::smem() : WideCfg<false>::smem();
+}
+
 template <int RM, bool DUAL>
 __global__ void __launch_bounds__(kDThreads)
 vgemm_dmma_kernel(VgemmArgs a, uint64_t kchunk) {
@@ -523,6 +725,29 @@ cudaError_t vgemm_run(VgemmArgs& a, cudaStream_t s, int sms) {
         a.nsplit = 1;
         a.reduced = 1;
         return cudaLaunchKernelEx(&c, vgemm_cluster_kernel<RM, DUAL>, a, kchunk);
+    }
+    // tall K, R in (32, 64]: the wide kernel (all rows per CTA, P read once)
+    static const bool wide_ok = [] {
+        const char* e = std::getenv("CPDB_VGEMM_WIDE");
+        return !(e && e[0] == '0');
+    }();
+    if (RM == 64 && a.R > 32 && wide_ok && (a.J % kWK == 0 || a.J == 1) && K >= (1ull << 16) &&
+        (a.I % 2 == 0)) {
+        const uint64_t iblocks = (a.I + WideCfg<DUAL>::WI - 1) / WideCfg<DUAL>::WI;
+        const uint64_t ktiles = (K + kWK - 1) / kWK;
+        uint64_t nsplit = std::max<uint64_t>(1, uint64_t(sms) / iblocks);
+        nsplit = std::min<uint64_t>({nsplit, ktiles, uint64_t(vgemm_max_split())});
+        const uint64_t kchunk = ((ktiles + nsplit - 1) / nsplit) * kWK;
+        nsplit = (K + kchunk - 1) / kchunk;
+        a.nsplit = uint32_t(nsplit);
+        const size_t smem = vgemm_wide_smem(DUAL);
+        cudaError_t e = cudaFuncSetAttribute(vgemm_wide_kernel<DUAL>,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(smem));
+        if (e != cudaSuccess) return e;
+        const dim3 grid{unsigned(nsplit), unsigned(iblocks), 1u};
+        vgemm_wide_kernel<DUAL><<<grid, kWT, smem, s>>>(a, kchunk);
+        return cudaGetLastError();
     }
     if (RM >= 8 && K < (1ull << 32)) {  // DMMA path
         const uint64_t iblocks = (a.I + kDM - 1) / kDM;
