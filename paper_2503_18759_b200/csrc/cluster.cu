@@ -172,7 +172,8 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
             }
             __syncthreads();
         }
-        const bool ok = chol<kNT, RM>(S.g, R, R);
+        // (rank 0's own Gram partial S.p is free after the reduction)
+        const bool ok = chol_first_pass<kNT, RM>(S.g, R, I, S.p) >= 0;
         if (threadIdx.x == 0) S.misc[2] = ok ? 0.0 : 1.0;
         CPDB_TS(5);
     }
@@ -377,7 +378,8 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
     }
     __syncthreads();
     CPDB_TS(1);
-    const bool ok1 = chol<kNT, RM>(S.g, R, R);
+    // (S.p, this rank's G2 partial later, is free here)
+    const bool ok1 = chol_first_pass<kNT, RM>(S.g, R, a.zrows, S.p) >= 0;
     if (!ok1 && rank == 0 && threadIdx.x == 0) *a.status = 2;
     stage_tri<RM>(S.g, R, R, S.u, S.dinv, kNT);  // U1 (kept in S.g too)
     __syncthreads();

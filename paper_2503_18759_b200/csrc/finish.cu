@@ -84,7 +84,7 @@ __global__ void __launch_bounds__(kNT) finish_single_kernel(FinishArgs a, int w_
         }
         __syncthreads();
     }
-    if (!chol<kNT, RM>(g, R, R)) {
+    if (chol_first_pass<kNT, RM>(g, R, I, g1) < 0) {
         if (threadIdx.x == 0) *a.status = 2;
         return;
     }

@@ -394,6 +394,33 @@ __device__ bool chol(double* g, int ld, int R) {
     }
 }
 
+// ---------------------------------------------------------------- first CholeskyQR pass
+// Cholesky of the first pass's Gram G (R x R, stride R) of an m x R matrix
+// with a shifted retry (shifted CholeskyQR, Fukaya-Kannan-Nakatsukasa-
+// Yamamoto-Yanagisawa 2020): when G is numerically indefinite (kappa of the
+// matrix beyond ~1e8, where the reference's Householder QR still works), G +
+// s I with s = 11 (m R + R (R + 1)) u tr(G) is factored instead.  The
+// second pass (near_identity_chol, or the pivoted chol when G2 is not close
+// to I) then restores the orthogonality, so the run continues where
+// CholeskyQR2 would stop.  copy: R x R scratch.  Block-uniform result: 0
+// plain, 1 shifted, -1 breakdown even with the shift.
+template <int NT, int RM>
+__device__ int chol_first_pass(double* g, int R, uint64_t m, double* copy) {
+#pragma unroll 1
+    for (int e = threadIdx.x; e < R * R; e += NT) copy[e] = g[e];
+    __syncthreads();
+    if (chol<NT, RM>(g, R, R)) return 0;
+    double tr = 0.0;
+    for (int i = 0; i < R; ++i) tr += copy[i * R + i];
+    const double sh =
+        11.0 * (double(m) * R + double(R) * (R + 1)) * 1.1102230246251565e-16 * tr;
+#pragma unroll 1
+    for (int e = threadIdx.x; e < R * R; e += NT)
+        g[e] = copy[e] + ((e / R == e % R) ? sh : 0.0);
+    __syncthreads();
+    return chol<NT, RM>(g, R, R) ? 1 : -1;
+}
+
 // ---------------------------------------------------------------- near-identity Cholesky
 // The second CholeskyQR pass factors G = Q1^T Q1 = I + E with |E| ~ kappa^2
 // eps (Q1 is already orthonormal to working accuracy).  Its Cholesky factor

@@ -78,7 +78,9 @@ __global__ void __launch_bounds__(kNT) zqr_prep_kernel(ZqrArgs a) {
         for (int e = threadIdx.x; e < R * R; e += kNT) g[e] = t == nm - 1 ? gk[e] : g[e] * gk[e];
     }
     __syncthreads();
-    if (!chol<kNT, RM>(g, R, R) && threadIdx.x == 0) *a.status = 2;
+    // (the staging area behind g is free: scratch of the shifted retry)
+    if (chol_first_pass<kNT, RM>(g, R, a.zrows, g + R * R) < 0 && threadIdx.x == 0)
+        *a.status = 2;
 #pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) a.work[e] = g[e];
     __syncthreads();
