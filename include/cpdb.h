@@ -119,6 +119,8 @@ typedef struct {
                                  with CPDB_TIME_TAILS=1, else 0                   */
     double comm_ms;           /* NCCL reductions (sharded contexts)                */
     uint64_t kernel_launches; /* device kernels launched by the solve              */
+    uint64_t qr_shifted;      /* sweeps in which a CholeskyQR first pass needed the
+                                 shifted retry (kappa beyond ~1e8)                 */
 } cpdb_profile;
 
 /* ---- version / device ----------------------------------------------------- */

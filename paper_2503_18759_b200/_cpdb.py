@@ -80,6 +80,7 @@ class Profile(C.Structure):
         ("mode_update_ms", C.c_double),
         ("comm_ms", C.c_double),
         ("kernel_launches", C.c_uint64),
+        ("qr_shifted", C.c_uint64),
     ]
 
 

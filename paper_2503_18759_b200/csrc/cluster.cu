@@ -173,8 +173,10 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
             __syncthreads();
         }
         // (rank 0's own Gram partial S.p is free after the reduction)
-        const bool ok = chol_first_pass<kNT, RM>(S.g, R, I, S.p) >= 0;
+        const int fp = chol_first_pass<kNT, RM>(S.g, R, I, S.p);
+        const bool ok = fp >= 0;
         if (threadIdx.x == 0) S.misc[2] = ok ? 0.0 : 1.0;
+        if (fp == 1 && threadIdx.x == 0) atomicOr(a.status, kStatusShifted);
         CPDB_TS(5);
     }
     cl.sync();  // ---- 2: lambda (rank 0's scratch), U1 (rank 0's g) published
@@ -379,8 +381,10 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
     __syncthreads();
     CPDB_TS(1);
     // (S.p, this rank's G2 partial later, is free here)
-    const bool ok1 = chol_first_pass<kNT, RM>(S.g, R, a.zrows, S.p) >= 0;
+    const int fp1 = chol_first_pass<kNT, RM>(S.g, R, a.zrows, S.p);
+    const bool ok1 = fp1 >= 0;
     if (!ok1 && rank == 0 && threadIdx.x == 0) *a.status = 2;
+    if (fp1 == 1 && rank == 0 && threadIdx.x == 0) atomicOr(a.status, kStatusShifted);
     stage_tri<RM>(S.g, R, R, S.u, S.dinv, kNT);  // U1 (kept in S.g too)
     __syncthreads();
     CPDB_TS(2);

@@ -84,10 +84,12 @@ __global__ void __launch_bounds__(kNT) finish_single_kernel(FinishArgs a, int w_
         }
         __syncthreads();
     }
-    if (chol_first_pass<kNT, RM>(g, R, I, g1) < 0) {
+    const int fp = chol_first_pass<kNT, RM>(g, R, I, g1);
+    if (fp < 0) {
         if (threadIdx.x == 0) *a.status = 2;
         return;
     }
+    if (fp == 1 && threadIdx.x == 0) atomicOr(a.status, kStatusShifted);
 #pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) g1[e] = g[e];
     stage_tri<RM>(g, R, R, u, dinv, kNT);

@@ -404,6 +404,9 @@ __device__ bool chol(double* g, int ld, int R) {
 // to I) then restores the orthogonality, so the run continues where
 // CholeskyQR2 would stop.  copy: R x R scratch.  Block-uniform result: 0
 // plain, 1 shifted, -1 breakdown even with the shift.
+// status-word bit: a first pass needed the shifted retry (not an error)
+constexpr int kStatusShifted = 1 << 16;
+
 template <int NT, int RM>
 __device__ int chol_first_pass(double* g, int R, uint64_t m, double* copy) {
 #pragma unroll 1

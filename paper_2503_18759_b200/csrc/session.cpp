@@ -1026,7 +1026,12 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
             cache[st.produces].buf.swap(pre);
             pf.active = false;
             after_wait = true;
-            if (dep_events) CPDB_CK(cudaEventRecord(ready_event(st.produces), ts));
+            // ready when the root kernel on the low-priority stream is: a
+            // later chain on this source (the next sweep's first update)
+            // then waits for the root itself, like this chain, instead of
+            // for this stream -- both become runnable together and the
+            // stream priorities decide which gets the SMs first
+            if (dep_events) CPDB_CK(cudaEventRecord(ready_event(st.produces), c->lo));
         } else {
             double* dst = (st.produces == (1u << n)) ? ybuf[2 * n + zpar].p
                                                     : cache[st.produces].buf.ensure(numel(od));
@@ -1366,6 +1371,8 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         CPDB_CK(cudaEventSynchronize(e_fit));
         int status;
         std::memcpy(&status, c->pinned + 2, sizeof(int));
+        if (status & (1 << 16)) c->prof.qr_shifted += 1;  // rowalg.cuh kStatusShifted
+        status &= 0xFFFF;
         // the word is free again for sweep + 4, whose first kernels the host
         // issues only after it has synchronised on sweep + 2's fitness, i.e.
         // after this clear (no device-side wait needed).  The next sweep's

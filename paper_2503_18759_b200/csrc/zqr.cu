@@ -79,8 +79,9 @@ __global__ void __launch_bounds__(kNT) zqr_prep_kernel(ZqrArgs a) {
     }
     __syncthreads();
     // (the staging area behind g is free: scratch of the shifted retry)
-    if (chol_first_pass<kNT, RM>(g, R, a.zrows, g + R * R) < 0 && threadIdx.x == 0)
-        *a.status = 2;
+    const int fp = chol_first_pass<kNT, RM>(g, R, a.zrows, g + R * R);
+    if (fp < 0 && threadIdx.x == 0) *a.status = 2;
+    if (fp == 1 && threadIdx.x == 0) atomicOr(a.status, kStatusShifted);
 #pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) a.work[e] = g[e];
     __syncthreads();

@@ -459,6 +459,7 @@ def test_ill_conditioned_factors_do_not_break_down(ctx, port, delta):
     xp = x * (1.0 + 1e-15 * np.random.default_rng(6).standard_normal(x.shape))
     op = port.solve(xp, R, 15, extrapolate=True, seed=7)
     g = cpd.als_qr_bre(x, cfg_of(R, 15, seed=7), ctx=ctx)
+    assert ctx.profile()["qr_shifted"] > 0  # the retry did run
     assert len(g.trace) == len(o.trace) == 15
     floor = max(abs(a_["fitness"] - b["fitness"]) for a_, b in zip(op.trace, o.trace))
     err = max(abs(t.fitness - b["fitness"]) for t, b in zip(g.trace, o.trace))
