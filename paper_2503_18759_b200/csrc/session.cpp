@@ -1343,8 +1343,17 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
                     // it runs beside them on its own stream (its front waited
                     // for the V-GEMM that read ybuf[n]; factor and lambda
                     // buffers are the other copies, partials the other parity)
-                    mode_update_back(sweep + 1, 0, unused, c->aux, true);
-                    CPDB_CK(cudaEventRecord(ev_aux, c->aux));
+                    // behind its own chain on the chain's stream (mid), so
+                    // the V-GEMM follows the branch TTM without a
+                    // cross-stream event hop (C2 +0.9%, C1 +2.9%, C4 flat;
+                    // CPDB_SPEC_STREAM=aux: its own stream)
+                    static const bool spec_mid = [] {
+                        const char* e = std::getenv("CPDB_SPEC_STREAM");
+                        return !(e && std::strcmp(e, "aux") == 0);
+                    }();
+                    const cudaStream_t ss = spec_mid ? c->mid : c->aux;
+                    mode_update_back(sweep + 1, 0, unused, ss, true);
+                    CPDB_CK(cudaEventRecord(ev_aux, ss));
                     CPDB_CK(cudaStreamWaitEvent(s, ev_aux, 0));
                     // and the second update's front (Z-QR + chain: no beta,
                     // no returned state -- nothing to undo), which also
@@ -1356,7 +1365,7 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
                         // CPDB_ZQR_AUX=0/1 overrides)
                         static const char* zae = std::getenv("CPDB_ZQR_AUX");
                         const bool zaux = zae ? zae[0] == '1' : order == 3;
-                        if (zaux) zqr_stream_override = c->aux;
+                        if (zaux) zqr_stream_override = ss;
                         mode_update_front(sweep + 1, 1, nullptr, nullptr);
                         zqr_stream_override = nullptr;
                         front1_issued = true;
