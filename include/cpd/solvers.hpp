@@ -226,6 +226,53 @@ inline SolveResult run_qr(const DenseTensor& x, const SolverConfig& cfg,
 
 }  // namespace detail
 
+namespace detail {
+
+// cp_als on a context whose tensor is already in HBM (cpdb_als_solve):
+// shared by cp_als and the command line (which streams X straight to HBM)
+inline SolveResult run_als_on_context(cpdb_ctx* ctx, const std::vector<std::size_t>& dims,
+                                      const SolverConfig& cfg, const double* init_f,
+                                      const double* init_l) {
+    cpdb_config c{};
+    c.rank = cfg.rank;
+    c.max_iterations = cfg.max_iterations;
+    c.fitness_threshold = cfg.fitness_threshold;
+    c.alpha = cfg.alpha;
+    c.activation_gap = cfg.activation_gap;
+    c.seed = cfg.seed;
+    std::size_t nfac = 0;
+    for (const std::size_t d : dims) nfac += d * cfg.rank;
+    std::vector<cpdb_trace_row> rows(cfg.max_iterations);
+    std::vector<double> lam(cfg.rank), fac(nfac);
+    uint64_t n = 0;
+    abi::check(cpdb_als_solve(ctx, &c, init_l, init_f, rows.data(), &n, lam.data(), fac.data()));
+    SolveResult out;
+    for (uint64_t i = 0; i < n; ++i) {
+        const cpdb_trace_row& r = rows[i];
+        TraceRow t;
+        t.iteration = std::size_t(r.iteration);
+        t.update_order.assign(r.update_order, r.update_order + r.order);
+        t.fitness = r.fitness;
+        t.raw_radicand = r.raw_radicand;
+        t.wall_seconds = r.wall_seconds;
+        t.root_ttm_count = r.root_ttm_count;
+        t.flops = r.flops;
+        t.beta_used = r.beta_used;
+        t.regularized = r.regularized != 0;
+        out.trace.push_back(std::move(t));
+    }
+    out.model.lambda = std::move(lam);
+    std::size_t off = 0;
+    for (const std::size_t d : dims) {
+        out.model.factors.emplace_back(
+            d, cfg.rank, std::vector<double>(fac.begin() + off, fac.begin() + off + d * cfg.rank));
+        off += d * cfg.rank;
+    }
+    return out;
+}
+
+}  // namespace detail
+
 inline SolveResult cp_als(const DenseTensor& x, const SolverConfig& cfg,
                           const std::optional<KruskalModel>& init = {}) {
     cfg.validate();
@@ -247,44 +294,8 @@ inline SolveResult cp_als(const DenseTensor& x, const SolverConfig& cfg,
     } guard{ctx};
     const std::vector<uint64_t> dims = abi::u64(x.shape().dims());
     abi::check(cpdb_tensor_set(ctx, x.data(), dims.data(), uint32_t(x.order())));
-    cpdb_config c{};
-    c.rank = cfg.rank;
-    c.max_iterations = cfg.max_iterations;
-    c.fitness_threshold = cfg.fitness_threshold;
-    c.alpha = cfg.alpha;
-    c.activation_gap = cfg.activation_gap;
-    c.seed = cfg.seed;
-    std::size_t nfac = 0;
-    for (const std::size_t d : x.shape().dims()) nfac += d * cfg.rank;
-    std::vector<cpdb_trace_row> rows(cfg.max_iterations);
-    std::vector<double> lam(cfg.rank), fac(nfac);
-    uint64_t n = 0;
-    abi::check(cpdb_als_solve(ctx, &c, init ? init_l.data() : nullptr,
-                              init ? init_f.data() : nullptr, rows.data(), &n, lam.data(),
-                              fac.data()));
-    SolveResult out;
-    for (uint64_t i = 0; i < n; ++i) {
-        const cpdb_trace_row& r = rows[i];
-        TraceRow t;
-        t.iteration = std::size_t(r.iteration);
-        t.update_order.assign(r.update_order, r.update_order + r.order);
-        t.fitness = r.fitness;
-        t.raw_radicand = r.raw_radicand;
-        t.wall_seconds = r.wall_seconds;
-        t.root_ttm_count = r.root_ttm_count;
-        t.flops = r.flops;
-        t.beta_used = r.beta_used;
-        t.regularized = r.regularized != 0;
-        out.trace.push_back(std::move(t));
-    }
-    out.model.lambda = std::move(lam);
-    std::size_t off = 0;
-    for (const std::size_t d : x.shape().dims()) {
-        out.model.factors.emplace_back(
-            d, cfg.rank, std::vector<double>(fac.begin() + off, fac.begin() + off + d * cfg.rank));
-        off += d * cfg.rank;
-    }
-    return out;
+    return detail::run_als_on_context(ctx, x.shape().dims(), cfg, init ? init_f.data() : nullptr,
+                                      init ? init_l.data() : nullptr);
 }
 
 inline SolveResult cp_als_qr(const DenseTensor& x, const SolverConfig& cfg,

@@ -69,7 +69,10 @@ def test_exit_codes(tmp_path, ref):
     bad.write_bytes(b"CPDT\x02\x01" + b"\x00" * 8)
     assert cli("decompose", "-i", bad, "--alg", "qr-bre", "--rank", 2).returncode == 3
     assert cli("info", "-i", bad).returncode == 3
-    assert cli("decompose", "-i", bad, "--alg", "als", "--rank", 2).returncode == 1
+    # --alg als runs CP-ALS on the device: a malformed file
+    # is a format error for it too, as in the reference
+    assert cli("decompose", "-i", bad, "--alg", "als", "--rank", 2).returncode == 3
+    assert cli("decompose", "-i", bad, "--alg", "bogus", "--rank", 2).returncode == 1
     assert cli("decompose", "-i", bad, "--alg", "qr", "--rank", 2, "--bogus", 1).returncode == 1
     assert cli("counts", "--order", 5, "--dims", "2,2,2,2,2", "--rank", 1).returncode == 1
     good = tmp_path / "g.cpdt"
@@ -124,3 +127,21 @@ def test_synth_baseline_device_generator(tmp_path):
     x = ctx.get_tensor([100, 100, 100])
     ctx.load_tensor(str(out))
     assert np.array_equal(ctx.get_tensor([100, 100, 100]), x)
+
+
+@pytest.mark.gpu
+def test_decompose_als_end_to_end(tmp_path, port, ref):
+    """cpd-b200 decompose --alg als (cli.hpp:86-88: cp_als) with X streamed to
+    HBM, trace and final fitness vs the reference's cp_als."""
+    x = ref.synth_baseline(0, (30, 28, 26), 4, 1e-2, 777)
+    xin = tmp_path / "x.cpdt"
+    ref.write_tensor_file(str(xin), x)
+    trace = tmp_path / "t.csv"
+    out = cli("decompose", "-i", xin, "--alg", "als", "--rank", 4, "--iters", 12, "--seed", 9,
+              "--trace", trace, check=0).stdout
+    o = ref.cp_als(x, 4, 12, seed=9)
+    rows = parse_trace(trace)
+    assert len(rows) == len(o.trace)
+    for r, w in zip(rows, o.trace):
+        assert abs(r["fitness"] - w["fitness"]) <= 1e-10 * abs(w["fitness"])
+    assert out.startswith("final_fitness ")

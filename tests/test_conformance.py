@@ -1,6 +1,6 @@
 """The reference's own hot-path unit tests (dim_tree_test, linalg_test,
-tensor_test, kruskal_test, solver_test, io_test, synth_test from
-/root/reference/proj/tests),
+tensor_test, kruskal_test, solver_test, io_test, synth_test, cli_test and the
+acceptance criteria C01-C12 of acceptance_test from /root/reference/proj/tests),
 compiled UNCHANGED against the drop-in `cpd::` headers (include/cpd) and
 libcpdb.so by oracle/conformance/Makefile, run on the B200.
 
@@ -19,7 +19,7 @@ from conftest import ROOT
 
 BIN = os.path.join(ROOT, "oracle", "_ref", "conformance")
 SUITES = ["dim_tree_test", "linalg_test", "tensor_test", "kruskal_test", "solver_test", "io_test",
-          "synth_test"]
+          "synth_test", "cli_test", "acceptance_test"]
 
 
 def run_suite(name):
@@ -39,3 +39,13 @@ def test_reference_suite_on_device(suite):
     passed, failed, p = run_suite(suite)
     assert passed > 0
     assert not failed, "\n".join(failed) + "\n" + p.stderr[-6000:]
+
+
+@pytest.mark.gpu
+def test_acceptance_criteria_all_pass():
+    """acceptance_test.cpp prints one line per criterion: C01-C12 all PASS on
+    the device path (C08 runs the CLI through cpd::run_command, cli.hpp)."""
+    passed, failed, p = run_suite("acceptance_test")
+    crit = re.findall(r"^\[criterion +(\d+)\] (.*): (PASS|FAIL)$", p.stdout, re.M)
+    assert len(crit) == 12, p.stdout[-3000:]
+    assert all(r == "PASS" for _, _, r in crit), crit
