@@ -196,8 +196,10 @@ __device__ __forceinline__ void vgemm_tile(const VgemmArgs& a, uint64_t i0, uint
     const double beta = extrap_beta(a);
 
     // two register sets: tiles t+1 and t+2 are in flight during tile t's MMAs
+    // (q0 and the history travel raw; the extrapolation is applied at the
+    // stash, so the loads stay in flight during the MMAs in between)
     struct Regs {
-        double y[YPT], p[PPT], f[DUAL ? PPT : 1];
+        double y[YPT], h[PPT], q[PPT];
     };
     auto fetch = [&](Regs& rg, uint32_t k0) {
 #pragma unroll
@@ -218,13 +220,13 @@ __device__ __forceinline__ void vgemm_tile(const VgemmArgs& a, uint64_t i0, uint
             const int e = threadIdx.x + u * kDThreads;
             const int kk = e / RM, r = e % RM;
             const uint32_t k = k0 + kk;
-            double q = 0.0, p = 0.0;
+            double q = 0.0, h = 0.0;
             if (e < kDK * RM && k < ke && r < R) {
                 q = a.q0[uint64_t(k) * R + r];
-                p = ex ? q + beta * (q - a.alpha * a.hist[uint64_t(k) * R + r]) : q;
+                if (ex) h = a.hist[uint64_t(k) * R + r];
             }
-            rg.p[u] = p;
-            if (DUAL) rg.f[u] = q;
+            rg.q[u] = q;
+            rg.h[u] = h;
         }
     };
     auto stash = [&](const Regs& rg) {
@@ -238,8 +240,9 @@ __device__ __forceinline__ void vgemm_tile(const VgemmArgs& a, uint64_t i0, uint
         for (int u = 0; u < PPT; ++u) {
             const int e = threadIdx.x + u * kDThreads;
             if (e < kDK * RM) {
-                ps[(e / RM) * PLD + e % RM] = rg.p[u];
-                if (DUAL) fs[(e / RM) * PLD + e % RM] = rg.f[u];
+                const double q = rg.q[u];
+                ps[(e / RM) * PLD + e % RM] = ex ? q + beta * (q - a.alpha * rg.h[u]) : q;
+                if (DUAL) fs[(e / RM) * PLD + e % RM] = q;
             }
         }
     };
@@ -377,6 +380,8 @@ __global__ void __launch_bounds__(kWT, 1) vgemm_wide_kernel(VgemmArgs a, uint64_
         }
     };
     constexpr int PPT = (kWK * 64 + kWT - 1) / kWT;  // 2 P elements per thread
+    // raw loads only: the extrapolation is applied when the values are
+    // stashed, a tile of MMAs later, so the loads' latency is hidden
     auto load_p = [&](int t, double (&pr)[PPT], double (&fr)[PPT]) {
         const uint64_t k0 = kb + uint64_t(t) * kWK;
 #pragma unroll
@@ -384,13 +389,13 @@ __global__ void __launch_bounds__(kWT, 1) vgemm_wide_kernel(VgemmArgs a, uint64_
             const int e = threadIdx.x + u * kWT;
             const int kk = e >> 6, c = e & 63;
             const uint64_t k = k0 + kk;
-            double q = 0.0, p = 0.0;
+            double q = 0.0, h = 0.0;
             if (k < ke && c < R) {
                 q = __ldg(a.q0 + k * R + c);
-                p = ex ? q + beta * (q - a.alpha * __ldg(a.hist + k * R + c)) : q;
+                if (ex) h = __ldg(a.hist + k * R + c);
             }
-            pr[u] = p;
             fr[u] = q;
+            pr[u] = h;
         }
     };
     auto stash_p = [&](int st, const double (&pr)[PPT], const double (&fr)[PPT]) {
@@ -398,8 +403,9 @@ __global__ void __launch_bounds__(kWT, 1) vgemm_wide_kernel(VgemmArgs a, uint64_
         for (int u = 0; u < PPT; ++u) {
             const int e = threadIdx.x + u * kWT;
             const int kk = e >> 6, c = e & 63;
-            ps[(st * kWK + kk) * kWLdP + c] = pr[u];
-            if (DUAL) fs[(st * kWK + kk) * kWLdP + c] = fr[u];
+            const double q = fr[u];
+            ps[(st * kWK + kk) * kWLdP + c] = ex ? q + beta * (q - a.alpha * pr[u]) : q;
+            if (DUAL) fs[(st * kWK + kk) * kWLdP + c] = q;
         }
     };
 

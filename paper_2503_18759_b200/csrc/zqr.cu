@@ -164,7 +164,7 @@ template <int RM>
 struct ZgSmem {
     static constexpr int LD = RM + 4;  // padded rows: conflict-free fragments
     static constexpr size_t doubles(int R) {
-        return size_t(RM) * LD + size_t(kGT) * LD + 2 * size_t(R) * R +
+        return size_t(RM) * LD + size_t(kGT) * LD + size_t(R) * LD + size_t(R) * R +
                size_t(kGT / R + 2) * R;
     }
 };
@@ -176,8 +176,8 @@ __global__ void __launch_bounds__(kNT) zqr_rows_gemm_kernel(ZqrArgs a) {
     const int R = a.R, nm = a.nm;
     double* w1 = sm;                // RM x LD
     double* zt = w1 + RM * LD;      // kGT x LD: Z tile, then Q1 tile
-    double* fast = zt + kGT * LD;   // R x R: the fastest digit's R_k
-    double* part = fast + R * R;    // R x R: this CTA's G2 partial
+    double* fast = zt + kGT * LD;   // R x LD: the fastest digit's R_k (padded rows)
+    double* part = fast + R * LD;   // R x R: this CTA's G2 partial
     double* slow = part + R * R;    // (kGT / R + 2) x R: products of the slower digits' rows
     const double* wsrc = a.work + 2 * R * R;
 #pragma unroll 1
@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(kNT) zqr_rows_gemm_kernel(ZqrArgs a) {
     }
 #pragma unroll 1
     for (int e = threadIdx.x; e < R * R; e += kNT) {
-        fast[e] = a.rmats[nm - 1][e];
+        fast[(e / R) * LD + e % R] = a.rmats[nm - 1][e];
         part[e] = 0.0;
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -217,29 +217,27 @@ __global__ void __launch_bounds__(kNT) zqr_rows_gemm_kernel(ZqrArgs a) {
             slow[e] = v;
         }
         __syncthreads();
-#pragma unroll 4
-        for (int e = threadIdx.x; e < kGT * RM; e += kNT) {
-            const int r = e / RM, c = e % RM;
-            double v = 0.0;
-            if (r < rows && c < R) {
-                const uint32_t t = uint32_t(row0) + uint32_t(r);
-                const uint32_t q = t / uint32_t(R);
-                v = fast[int(t - q * uint32_t(R)) * R + c] * slow[int(q - g0) * R + c];
-            }
-            zt[r * LD + c] = v;
-        }
-        __syncthreads();
+        // A fragments straight from the staged rows (no Z tile):
+        // Z[t][k] = R_fast[t % R][k] * P[t / R][k]
         double acc[NB][2];
 #pragma unroll
         for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
+        {
+            const int rr = warp * 8 + m;
+            const bool rowok = rr < rows;
+            const uint32_t t = uint32_t(row0) + uint32_t(rowok ? rr : 0);
+            const uint32_t q = t / uint32_t(R);
+            const double* fr = fast + int(t - q * uint32_t(R)) * LD;
+            const double* sr = slow + int(q - g0) * R;
 #pragma unroll
-        for (int k4 = 0; k4 < RM / 4; ++k4) {
-            const double av = zt[(warp * 8 + m) * LD + 4 * k4 + kq];
+            for (int k4 = 0; k4 < RM / 4; ++k4) {
+                const int k = 4 * k4 + kq;
+                const double av = (rowok && k < R) ? fr[k] * sr[k] : 0.0;
 #pragma unroll
-            for (int b = 0; b < NB; ++b)
-                dmma(acc[b][0], acc[b][1], av, w1[(4 * k4 + kq) * LD + b * 8 + m]);
+                for (int b = 0; b < NB; ++b)
+                    dmma(acc[b][0], acc[b][1], av, w1[(4 * k4 + kq) * LD + b * 8 + m]);
+            }
         }
-        __syncthreads();  // every warp done reading the Z tile
         {
             const int r = warp * 8 + m;
 #pragma unroll
