@@ -181,3 +181,36 @@ def test_sharded_resume_rebuilds_planned_layouts(ctx, port, policy, k):
             assert np.linalg.norm(fa - fb) <= 1e-10 * np.linalg.norm(fb)
     for c in group:
         c.close()
+
+
+@pytest.mark.parametrize("policy", ["eager", "scatter", "lazy", "auto"])
+@pytest.mark.parametrize("world", [2, 4])
+def test_sharded_c5_proxy_matches_unsharded(ctx, port, policy, world):
+    """Config 5's path sharded: fourth order, R = 64 (tall multi-kernel Z-QR
+    of Z = 262144 x 64, the wide V-GEMM, the 3-cycle branch reuse) at the
+    64^4 proxy, every reduction strategy, against the unsharded run."""
+    import paper_2503_18759_b200 as cpd
+    dims, rank = (64, 64, 64, 64), 64
+    x = port.synth_baseline(0, dims, rank, 1e-3, 20250005)
+    cfg = cpd.SolverConfig(rank=rank, max_iterations=5, seed=7)
+    ctx.set_tensor(x)
+    ref = ctx.solve(cfg, extrapolate=True)
+    rows = dims[0] // world
+    group = cpd.Context.local_group(0, world)
+    cost = {"bus_gbs": 0.05} if policy == "auto" else None
+
+    def rank_run(r, c):
+        c.set_shard_policy(policy, cost)
+        c.set_tensor(np.ascontiguousarray(x[r * rows:(r + 1) * rows]), dims)
+        return c.solve(cfg, extrapolate=True)
+
+    res = run_ranks(group, rank_run)
+    for g in res:
+        assert len(g.trace) == len(ref.trace)
+        for a, b in zip(g.trace, ref.trace):
+            assert a.update_order == b.update_order and a.flops == b.flops
+            assert abs(a.fitness - b.fitness) <= 1e-10 * b.fitness
+        for fa, fb in zip(g.model.factors, ref.model.factors):
+            assert np.linalg.norm(fa - fb) <= 1e-10 * np.linalg.norm(fb)
+    for c in group:
+        c.close()
