@@ -10,8 +10,9 @@
 // R-sized matrices, transpose, gram, dot, hadamard, kronecker, fold) are plain
 // host loops here as they are there; none of them is on the sweep's hot path.
 //
-// MTTKRP (tensor.hpp:415-518) belongs to the CP-ALS normal-equation solver,
-// which is outside this library's scope.
+// MTTKRP (tensor.hpp:415-518), the kernel of the CP-ALS normal-equation
+// solver, also runs on the device: mttkrp /
+// mttkrp_materialized below go through cpdb_mttkrp.
 #pragma once
 
 #include <cmath>

@@ -288,10 +288,17 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         const char* e = std::getenv("CPDB_ROOT_PREFETCH");
         // not for TTM-dominated runs (C5: the root is 95% of the sweep, so the
         // one-tile-per-CTA grid only costs)
-        prefetch_enabled = c->overlap && !sharded && !(e && e[0] == '0') &&
+        // Sharded runs keep the overlaps (CPDB_SHARD_OVERLAP=0: the simple
+        // stream-ordered form): every collective stays on the main stream,
+        // bracketed by events to the stream that produced / consumes its
+        // data (ttm_step, mode_update_back), so the NCCL operations of the
+        // communicator are issued and executed in one order on every rank.
+        const char* so = std::getenv("CPDB_SHARD_OVERLAP");
+        const bool shard_ok = !sharded || !(so && so[0] == '0');
+        prefetch_enabled = c->overlap && shard_ok && !(e && e[0] == '0') &&
                            numel(c->ldims) < (1ull << 32);
         const char* cs = std::getenv("CPDB_CHAIN_SIDE");
-        chain_side = c->overlap && !sharded && !(cs && cs[0] == '0');
+        chain_side = c->overlap && shard_ok && !(cs && cs[0] == '0');
         // An update that runs beside the prefetched root TTM is off the
         // critical path (the root is): its branch TTMs and V-GEMM take a few
         // SMs for longer instead of every SM briefly, so the root keeps more.
@@ -599,12 +606,14 @@ void Session::qr_factor(uint32_t k) {
 // Sharded runs contract a split mode m with this rank's rows of Q_m only;
 // they get their own packed copy (no row-alignment constraint), refreshed
 // after every update of m.
-void Session::pack_local(uint32_t m) {
+void Session::pack_local(uint32_t m, cudaStream_t st) {
     if (!sharded || !need_local[m]) return;
+    if (!st) st = s;
     const uint64_t rows = shard_rows_of(m);
     qp_local[m].ensure(uint64_t(ttm_kpad(rows)) * Rp);
-    CPDB_CK(pack_q(fb[m].q.p + uint64_t(c->rank) * rows * R, qp_local[m].p, uint32_t(rows), R,
-                   s));
+    const double* src = fb[m].q.p + uint64_t(c->rank) * rows * R;
+    CPDB_CK(pack_q(src, qp_local[m].p, uint32_t(rows), R, st));
+    acc(st, "pack_local", {rg(src, rows * R)}, {rg(qp_local[m].p, uint64_t(ttm_kpad(rows)) * Rp)});
     c->launches += 1;
 }
 
@@ -658,7 +667,7 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, const
     }
     // a reduce-scatter needs the whole partial first
     double* raw = dst;
-    if (sh && sh->red == kRedScatter) raw = rs_tmp.ensure(numel(sd) / sd[k] * R);
+    if (sh && sh->red == kRedScatter) raw = rs_tmp[st].ensure(numel(sd) / sd[k] * R);
     Timer t;
     if (c->timing) {
         t.a = events.get();
@@ -684,6 +693,12 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, const
         timers.push_back(t);
     }
     if (sh && sh->red != kRedNone) {
+        // the collective runs on the main stream, after this step's kernel
+        if (st != s) {
+            cudaEvent_t e0 = events.get();
+            CPDB_CK(cudaEventRecord(e0, st));
+            CPDB_CK(cudaStreamWaitEvent(s, e0, 0));
+        }
         Timer tc;
         if (c->timing) {
             tc.a = events.get();
@@ -707,6 +722,11 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, const
             CPDB_CK(cudaEventRecord(tc.b, s));
             timers.push_back(tc);
         }
+        if (st != s) {  // the producing stream goes on with the reduced data
+            cudaEvent_t e1 = events.get();
+            CPDB_CK(cudaEventRecord(e1, s));
+            CPDB_CK(cudaStreamWaitEvent(st, e1, 0));
+        }
     }
 }
 
@@ -728,6 +748,9 @@ void Session::prefetch_root(uint64_t sweep, uint32_t b, cudaStream_t after) {
         bool fresh = true;
         for (uint32_t bm = b + 1; bm < b2; ++bm) fresh = fresh && sw.updates[bm].mode != cm;
         if (!fresh) continue;
+        // sharded: a root whose partial sums are reduced stays in order (its
+        // collective on the main stream would wait for the whole prefetch)
+        if (sharded && splan.steps[sweep - 1][b2][0].red != kRedNone) continue;
         std::vector<uint64_t> od = c->ldims;
         od[cm] = R;
         pre.ensure(numel(od));
@@ -773,7 +796,10 @@ void Session::prefetch_root(uint64_t sweep, uint32_t b, cudaStream_t after) {
 void Session::launch_prefetch() {
     if (!pf.active || pf.launched) return;
     CPDB_CK(cudaStreamWaitEvent(c->lo, ev_fin, 0));
-    ttm_step(c->x, c->ldims, nullptr, pf.cm, pre.p, true, c->lo, true, true);
+    // (sharded: the planned step -- contracting the split mode takes this
+    // rank's rows of Q; prefetched roots are never reduced, prefetch_root)
+    ttm_step(c->x, c->ldims, sharded ? &splan.steps[pf.sweep - 1][pf.block][0] : nullptr, pf.cm,
+             pre.p, true, c->lo, true, true);
     CPDB_CK(cudaEventRecord(pf.ev, c->lo));
     pf.launched = true;
 }
@@ -1178,6 +1204,11 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
         tl_end(tla, bs, "reduce");
         c->launches += v.dual ? 2 : 1;
     }
+    if ((gather || vsum) && bs != s) {  // collectives on the main stream
+        cudaEvent_t e0 = events.get();
+        CPDB_CK(cudaEventRecord(e0, bs));
+        CPDB_CK(cudaStreamWaitEvent(s, e0, 0));
+    }
     if (gather) {
         allgather(c, vf.p, v.I * R);
         if (v.dual) allgather(c, vff.p, v.I * R);
@@ -1185,6 +1216,11 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     if (vsum) {
         allreduce_sum(c, vf.p, v.I * R);
         if (v.dual) allreduce_sum(c, vff.p, v.I * R);
+    }
+    if ((gather || vsum) && bs != s) {
+        cudaEvent_t e1 = events.get();
+        CPDB_CK(cudaEventRecord(e1, s));
+        CPDB_CK(cudaStreamWaitEvent(bs, e1, 0));
     }
     // 6-9. A_hat, lambda, factor QR, fitness (solvers.hpp:272-292)
     FinishArgs f{};
@@ -1245,7 +1281,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
             std::fprintf(stderr, " %d:%.2f", k, ts[k] ? (ts[k] - ts[0]) * 1e-3 : -1.0);
         std::fprintf(stderr, "\n");
     }
-    pack_local(n);
+    pack_local(n, bs);  // (on the finisher's stream: ev_fac[n] covers it)
     if (dep_events) {
         CPDB_CK(cudaEventRecord(ev_fac[n], bs));       // A_n, Q_n, R_n final
         CPDB_CK(cudaEventRecord(ev_zread[zpar], bs));  // Q0 / R0 / history consumed
@@ -1491,6 +1527,7 @@ void Session::undo_speculative_update() {
         std::swap(ev_hist[n], ev_zq_pending);
     }
     has_hist[n] = spec.had_hist;
+    pack_local(n);  // this rank's rows of the restored Q_n
     --versions[n];
     last_mode = spec.prev_last_mode;
     spec.issued = false;

@@ -53,7 +53,7 @@ struct Session {
     ShardPlan splan;
     std::vector<bool> need_local;
     std::vector<DevBuf> qp_local;
-    DevBuf rs_tmp;
+    std::map<cudaStream_t, DevBuf> rs_tmp;  // per producing stream
     DevBuf gate;  // {has_beta, beta, has_prev, prev_fitness} on the device (beta_gate)
     // the next sweep's first update issued before the host read this sweep's
     // fitness (Session::run); what undoing it needs
@@ -202,7 +202,7 @@ struct Session {
 private:
     std::vector<uint64_t> local_dims_of(uint32_t key) const;
     void qr_factor(uint32_t k);
-    void pack_local(uint32_t m);
+    void pack_local(uint32_t m, cudaStream_t st = nullptr);
     uint64_t shard_rows_of(uint32_t m) const;
     std::vector<uint64_t> dims_in(uint32_t key, const ShardLayout& L) const;
     void ttm_step(const double* src, const std::vector<uint64_t>& sd, const StepShard* sh,
