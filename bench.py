@@ -370,7 +370,9 @@ def main():
         ctx2.set_tensor(xh, dims)  # synchronous H2D from pinned memory
         t_h2d = time.perf_counter() - t0
         s2 = ctx2.session(cfg2, extrapolate=True)
+        t_begin = time.perf_counter()
         r2 = s2.run(K)
+        t_run = time.perf_counter()
         m2 = s2.end()
         t1 = time.perf_counter()
         s2.close()
@@ -380,6 +382,8 @@ def main():
         d2h = (sum(f.size for f in m2.factors) + m2.lam.size) * 8 + len(r2) * 128
         e2e = {"value": K / et, "unit": "sweeps/s", "h2d_bytes_per_step": h2d / K,
                "d2h_bytes_per_step": d2h / K, "h2d_ms": t_h2d * 1e3,
+               "begin_ms": (t_begin - t0 - t_h2d) * 1e3, "sweeps_ms": (t_run - t_begin) * 1e3,
+               "end_ms": (t1 - t_run) * 1e3,
                "h2d_gbs": h2d / t_h2d / 1e9,
                "rest_ms": (et - t_h2d) * 1e3,
                "note": "one job: H2D of X (pinned; h2d_ms of it) + setup + K sweeps + D2H of "
