@@ -311,3 +311,41 @@ def test_strategy_rules_and_costs_c5():
     r1 = cpd.shard_plan_ex(4, "branch-reuse", 6, dims, R, 1, "auto")
     assert all(s["reduction"] is None and s["out"][0] == "replicated" for s in r1["steps"])
     assert r1["est_comm_s"] == 0.0
+
+
+def test_plan_ex_rejects_bad_arguments():
+    with pytest.raises(ValueError):
+        cpd.shard_plan_ex(3, "branch-reuse", 4, (8, 6, 4), 3, 2, policy=7)
+    with pytest.raises(ValueError):
+        cpd.shard_plan_ex(3, "branch-reuse", 4, (8, 6, 4), 0, 2)
+    with pytest.raises(ValueError):
+        cpd.shard_plan_ex(3, "branch-reuse", 4, (8, 6, 4), 3, 0)
+
+
+@pytest.mark.parametrize("policy", POLICIES)
+def test_plan_ex_layout_invariants(policy):
+    """Every step's source layout is what the plan stored for that slot; a
+    split mode is always a free mode of the set; partial sums only come from
+    contracting the split mode or from a partial source; eager never leaves a
+    partial, lazy never reduces a step."""
+    for order, dims in ((3, (16, 12, 8)), (4, (16, 12, 8, 8))):
+        sched = cpd.build_schedule(order, "branch-reuse", 8)
+        plan = cpd.shard_plan_ex(order, "branch-reuse", 8, dims, 4, 4, policy,
+                                 cost={"bus_gbs": 0.05})
+        slots = {}
+        root = (1 << order) - 1
+        for (it, b, mode, src, c, prod), st in zip(sched.flat(), plan["steps"]):
+            want = ("sharded", 0) if src == root else slots[src]
+            assert st["src"] == want
+            kind, m = st["out"]
+            if kind == "sharded":
+                assert prod >> m & 1
+            raw_partial = (st["src"] == ("sharded", c)) or st["src"][0] == "partial"
+            if st["reduction"] is not None:
+                assert raw_partial
+            if policy == "eager":
+                assert kind != "partial"
+            if policy == "lazy":
+                assert st["reduction"] is None
+            if prod != (1 << mode):
+                slots[prod] = st["out"]
