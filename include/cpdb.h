@@ -137,6 +137,11 @@ int cpdb_create(int device, cpdb_ctx** out);
  * cpdb_nccl_unique_id on rank 0, broadcast by the caller. */
 int cpdb_create_sharded(int device, int rank, int world, const void* nccl_id, cpdb_ctx** out);
 int cpdb_nccl_unique_id(void* out128);
+/* The NCCL calls of the sharded path (all-reduce, all-gather, grouped
+ * per-slice reduce-scatter) on a one-rank communicator of `device`:
+ * *max_err = max |result - input| (0 when the transport works).  Checks the
+ * dlopen'ed NCCL on a single-GPU box, where no multi-rank run is possible. */
+int cpdb_nccl_selftest(int device, double* max_err);
 /* `world` ranks of a mode-1 sharded run inside ONE process on ONE device,
  * each to be driven by its own host thread; the collectives go through a
  * shared device buffer and host barriers instead of NCCL.  For exercising the

@@ -159,6 +159,14 @@ class Context:
         return out
 
     @staticmethod
+    def nccl_selftest(device: int = 0) -> float:
+        """The sharded path's NCCL calls on a one-rank communicator
+        (cpdb_nccl_selftest): returns the max error (0.0 when they work)."""
+        out = np.zeros(1)
+        _raise(_lib().cpdb_nccl_selftest(device, _p(out)))
+        return float(out[0])
+
+    @staticmethod
     def nccl_unique_id() -> bytes:
         buf = C.create_string_buffer(128)
         _raise(_lib().cpdb_nccl_unique_id(buf))

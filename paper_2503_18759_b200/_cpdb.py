@@ -110,6 +110,7 @@ SIGNATURES = {
     "cpdb_create": (C.c_int, [C.c_int, C.POINTER(CTX)]),
     "cpdb_create_sharded": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_void_p, C.POINTER(CTX)]),
     "cpdb_nccl_unique_id": (C.c_int, [C.c_void_p]),
+    "cpdb_nccl_selftest": (C.c_int, [C.c_int, P]),
     "cpdb_destroy": (None, [CTX]),
     "cpdb_shard_rows": (C.c_int, [C.c_uint64, C.c_int, C.c_int, U64P, U64P]),
     "cpdb_tensor_set": (C.c_int, [CTX, P, U64P, C.c_uint32]),

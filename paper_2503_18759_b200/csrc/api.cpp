@@ -227,6 +227,59 @@ int cpdb_create_sharded(int device, int rank, int world, const void* nccl_id, cp
     return CPDB_OK;
 }
 
+int cpdb_nccl_selftest(int device, double* max_err) {
+    return guarded([&] {
+        if (!max_err) fail(CPDB_INVALID_ARGUMENT, "nccl_selftest: null output");
+        const cpdb::Nccl& N = cpdb::nccl();
+        if (!N.ok) fail(CPDB_NCCL_ERROR, N.why);
+        CPDB_CK(cudaSetDevice(device));
+        ncclUniqueId id;
+        ncclResult_t r = N.GetUniqueId(&id);
+        if (r != ncclSuccess) fail(CPDB_NCCL_ERROR, N.GetErrorString(r));
+        ncclComm_t comm;
+        r = N.CommInitRank(&comm, 1, id, 0);
+        if (r != ncclSuccess) fail(CPDB_NCCL_ERROR, N.GetErrorString(r));
+        cudaStream_t st;
+        CPDB_CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+        // the three call patterns of runtime.cpp on a one-rank communicator:
+        // all-reduce in place, all-gather of this rank's chunk, and the
+        // grouped per-slice reduce-scatter (identities for one rank)
+        const size_t outer = 3, block = 40, n = outer * block;
+        std::vector<double> h(n), back(n);
+        for (size_t i = 0; i < n; ++i) h[i] = double(i) * 0.5 - 7.0;
+        double *a, *b;
+        CPDB_CK(cudaMalloc(&a, n * sizeof(double)));
+        CPDB_CK(cudaMalloc(&b, n * sizeof(double)));
+        CPDB_CK(cudaMemcpy(a, h.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+        double err = 0.0;
+        auto check = [&](const double* dev) {
+            CPDB_CK(cudaStreamSynchronize(st));
+            CPDB_CK(cudaMemcpy(back.data(), dev, n * sizeof(double), cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < n; ++i) err = std::max(err, std::fabs(back[i] - h[i]));
+        };
+        r = N.AllReduce(a, a, n, ncclDouble, ncclSum, comm, st);
+        if (r == ncclSuccess) check(a);
+        if (r == ncclSuccess) r = N.AllGather(a, b, n, ncclDouble, comm, st);
+        if (r == ncclSuccess) check(b);
+        if (r == ncclSuccess) {
+            CPDB_CK(cudaMemsetAsync(b, 0, n * sizeof(double), st));
+            r = N.GroupStart();
+            for (size_t o = 0; o < outer && r == ncclSuccess; ++o)
+                r = N.ReduceScatter(a + o * block, b + o * block, block, ncclDouble, ncclSum, comm,
+                                    st);
+            const ncclResult_t r2 = N.GroupEnd();
+            if (r == ncclSuccess) r = r2;
+            if (r == ncclSuccess) check(b);
+        }
+        cudaFree(a);
+        cudaFree(b);
+        cudaStreamDestroy(st);
+        N.CommDestroy(comm);
+        if (r != ncclSuccess) fail(CPDB_NCCL_ERROR, N.GetErrorString(r));
+        *max_err = err;
+    });
+}
+
 int cpdb_create_local_group(int device, int world, cpdb_ctx** out) {
     if (!out || world < 1) return CPDB_INVALID_ARGUMENT;
     for (int r = 0; r < world; ++r) out[r] = nullptr;

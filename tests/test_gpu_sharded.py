@@ -102,6 +102,15 @@ def test_sharded_synth_matches_unsharded(ctx):
         c.close()
 
 
+def test_nccl_calls_execute_on_one_rank():
+    """The NCCL operations the sharded session issues -- in-place all-reduce,
+    all-gather, and the grouped per-slice reduce-scatter -- run on a one-rank
+    communicator of this B200 and return their input (a multi-rank NCCL run
+    needs more than the one GPU this environment has)."""
+    import paper_2503_18759_b200 as cpd
+    assert cpd.Context.nccl_selftest(0) == 0.0
+
+
 def test_nccl_library_available():
     """The multi-GPU transport: libnccl.so.2 resolves (dlopen, comm.cpp) and
     hands out a unique id; one rank per GPU then calls cpdb_create_sharded."""
