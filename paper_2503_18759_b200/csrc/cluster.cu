@@ -35,6 +35,16 @@ namespace {
 constexpr int kCS = 8;    // cluster size (portable maximum)
 constexpr int kNT = 512;  // threads per CTA
 
+// Split cluster barrier: every CTA arrives once its remote reads of rank 0's
+// shared memory are done; only rank 0 waits, right before it exits (its
+// shared memory must outlive those reads), the others exit freely.
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // rank 0: G = sum_r P_r over the cluster, fixed rank order
 __device__ void cluster_reduce(cg::cluster_group& cl, const double* P, int n, double* G) {
 #pragma unroll 1
@@ -195,7 +205,9 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
         }
         if (threadIdx.x == 0) flag = cl.map_shared_rank(S.misc, 0)[2] != 0.0;
     }
-    cl.sync();  // rank 0 may reuse g / scratch only after every rank copied them
+    // (rank 0 next writes its g / scratch after barrier 3, which every rank
+    // reaches only after these copies: no cluster barrier needed here)
+    __syncthreads();
     CPDB_TS(7);
     if (flag) {
         if (rank == 0 && threadIdx.x == 0) *a.status = 2;
@@ -302,6 +314,7 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
         if (threadIdx.x == 0) flag = cl.map_shared_rank(S.misc, 0)[2] != 0.0;
     }
     __syncthreads();
+    cluster_arrive();  // this CTA's reads of rank 0's smem are done
     if (!flag) {
         // phase C: Q = A1 U2^-1 (+ packed copy [Kpad/4][Rp][4])
         const uint32_t Rp = ttm_rpad_dev(R);
@@ -325,7 +338,7 @@ __global__ void __launch_bounds__(kNT) finish_cluster_kernel(FinishArgs a) {
         *a.status = 2;
     }
     CPDB_TS(14);
-    cl.sync();  // rank 0's smem must outlive the other ranks' DSMEM reads
+    if (rank == 0) cluster_wait();  // rank 0's smem outlives the others' DSMEM reads
     CPDB_TS(15);
 }
 
@@ -456,6 +469,7 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
     CPDB_TS(7);
     stage_tri<RM>(cl.map_shared_rank(S.g, 0), R, R, S.u, S.dinv, kNT);
     __syncthreads();
+    cluster_arrive();  // this CTA's reads of rank 0's smem are done
     CPDB_TS(8);
     for (int li = grp; li < rows + (G - rows % G) % G; li += G) {
         const bool act = li < rows;
@@ -465,7 +479,7 @@ __global__ void __launch_bounds__(kNT) zqr_cluster_kernel(ZqrArgs a) {
         if (act) x.store(a.q0 + (r0 + li) * R, R, q);
     }
     CPDB_TS(9);
-    cl.sync();
+    if (rank == 0) cluster_wait();  // rank 0's smem outlives the others' reads
     CPDB_TS(10);
 }
 
