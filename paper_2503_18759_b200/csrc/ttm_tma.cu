@@ -399,6 +399,21 @@ bool tile_ok(const TtmArgs& a, int cb, int nc) {
 // 112-row tiles, 147 of them (99%).
 template <int RB, int CB0, int BK, int ST, int LAYOUT>
 cudaError_t launch_adaptive(const TtmArgs& a, cudaStream_t s, int sms) {
+    // Large (root-sized) TTMs: the widest tile with 16 consumer warps of half
+    // the column blocks each -- the same tile, four warps per SMSP instead of
+    // two, which hides the DMMA issue spacing (ncu's top stall, `wait`):
+    // C2 root 265.2 -> 260.6 us (87.3 -> 88.8% of peak), C5 16.52 -> 16.30 ms
+    // (89.6 -> 90.8%), C2 2501 -> 2545 sweeps/s.  CPDB_TTM_NC16=0: 8 warps;
+    // =2: also the (smaller) branch TTMs.
+    if constexpr (CB0 >= 2) {
+        static const int nc16 = [] {
+            const char* e = std::getenv("CPDB_TTM_NC16");
+            return e ? std::atoi(e) : 1;
+        }();
+        if (nc16 > 0 && (nc16 > 1 || tiles_with<LAYOUT>(a, CB0, 8) >= uint64_t(2 * sms)) &&
+            tile_ok<LAYOUT>(a, CB0 / 2, 16))
+            return launch_v2<RB, CB0 / 2, BK, ST, 16, LAYOUT>(a, s, sms);
+    }
     int best = CB0, best_nc = 8;
     double best_score = -1.0;
     // opt-in (CPDB_TTM_NC7=1): measured at C2, 147-CTA branch TTMs leave no
