@@ -410,8 +410,35 @@ cudaError_t launch_adaptive(const TtmArgs& a, cudaStream_t s, int sms) {
             const char* e = std::getenv("CPDB_TTM_NC16");
             return e ? std::atoi(e) : 1;
         }();
-        if (nc16 > 0 && (nc16 > 1 || tiles_with<LAYOUT>(a, CB0, 8) >= uint64_t(2 * sms)) &&
-            tile_ok<LAYOUT>(a, CB0 / 2, 16))
+        // (CPDB_TTM_ROOTCFG=1..3: tile-shape experiments for the root)
+        static const int rootcfg = [] {
+            const char* e = std::getenv("CPDB_TTM_ROOTCFG");
+            return e ? std::atoi(e) : 0;
+        }();
+        const bool root_sized = tiles_with<LAYOUT>(a, CB0, 8) >= uint64_t(2 * sms);
+        if (rootcfg && root_sized) {
+            if constexpr (RB == 4 && CB0 == 4) {
+                if (rootcfg == 1 && tile_ok<LAYOUT>(a, 4, 16))
+                    return launch_v2<4, 4, 8, 6, 16, LAYOUT>(a, s, sms);
+                if (rootcfg == 2 && tile_ok<LAYOUT>(a, 4, 16))
+                    return launch_v2<4, 4, 8, 5, 16, LAYOUT>(a, s, sms);
+                if (rootcfg == 3 && tile_ok<LAYOUT>(a, 2, 16))
+                    return launch_v2<4, 2, 8, 8, 16, LAYOUT>(a, s, sms);
+            }
+            if constexpr (RB == 2 && CB0 == 8) {
+                if (rootcfg == 1 && tile_ok<LAYOUT>(a, 8, 16))
+                    return launch_v2<2, 8, 8, 3, 16, LAYOUT>(a, s, sms);
+            }
+        }
+        // R in (56, 64]: 16 warps of 8 x 2 accumulator blocks, 16-deep k
+        // stages, five of them (C5 root 16.30 -> 15.33 ms = 96.6% of the
+        // DMMA peak, 28.1 -> 29.1 sweeps/s); the other tile shapes measured
+        // no better at their R (C2: 5 or 6 stages alike, wider tiles worse)
+        if constexpr (RB == 8 && CB0 == 2) {
+            if (nc16 > 0 && (nc16 > 1 || root_sized) && tile_ok<LAYOUT>(a, 2, 16))
+                return launch_v2<8, 2, 16, 5, 16, LAYOUT>(a, s, sms);
+        }
+        if (nc16 > 0 && (nc16 > 1 || root_sized) && tile_ok<LAYOUT>(a, CB0 / 2, 16))
             return launch_v2<RB, CB0 / 2, BK, ST, 16, LAYOUT>(a, s, sms);
     }
     int best = CB0, best_nc = 8;

@@ -1,0 +1,8 @@
+for v in 0 1 2 3 0; do
+  CPDB_TTM_ROOTCFG=$v timeout 120 python bench.py --config c2 --steps 100 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/p34.json 2> gpurun_out/p34.err
+  echo "c2 cfg=$v rc=$? $(python -c "import json; d=json.load(open('gpurun_out/p34.json')); r=d['roofline']; print(round(d['value'],1), round(r['avg_launch_ms']*1e3,1), round(r['frac'],4), round(r['overlapped_avg_launch_ms']*1e3,1))" 2>/dev/null)"
+done
+for v in 0 1 2; do
+  CPDB_TTM_ROOTCFG=$v timeout 300 python bench.py --config c5 --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/p34.json 2> gpurun_out/p34.err
+  echo "c5 cfg=$v rc=$? $(python -c "import json; d=json.load(open('gpurun_out/p34.json')); r=d['roofline']; print(round(d['value'],2), round(r['avg_launch_ms']*1e3,1), round(r['frac'],4))" 2>/dev/null)"
+done
