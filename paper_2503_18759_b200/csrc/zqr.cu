@@ -169,9 +169,21 @@ struct ZgSmem {
     }
 };
 
+// Warp tiling of a kGT x RM tile product over the 16 warps: WR x WC blocks
+// (16 x 32 at RM = 64: per 4-k step 2 A + 4 B fragment loads feed 8 DMMAs,
+// against 1 + 8 with one 8-row strip per warp)
+template <int RM>
+struct WarpTile {
+    static constexpr int WC = RM / 2 >= 8 ? RM / 2 : 8;  // columns per warp
+    static constexpr int CG = RM / WC;                   // column groups
+    static constexpr int RG = (kNT / 32) / CG;           // row groups
+    static constexpr int WR = kGT / RG;                  // rows per warp
+    static constexpr int RBW = WR / 8, CBW = WC / 8;
+};
+
 template <int RM>
 __global__ void __launch_bounds__(kNT) zqr_rows_gemm_kernel(ZqrArgs a) {
-    constexpr int LD = ZgSmem<RM>::LD, NB = RM / 8;
+    constexpr int LD = ZgSmem<RM>::LD;
     extern __shared__ double sm[];
     const int R = a.R, nm = a.nm;
     double* w1 = sm;                // RM x LD
@@ -219,36 +231,54 @@ __global__ void __launch_bounds__(kNT) zqr_rows_gemm_kernel(ZqrArgs a) {
         __syncthreads();
         // A fragments straight from the staged rows (no Z tile):
         // Z[t][k] = R_fast[t % R][k] * P[t / R][k]
-        double acc[NB][2];
+        using WT = WarpTile<RM>;
+        const int rw0 = (warp % WT::RG) * WT::WR, cw0 = (warp / WT::RG) * WT::WC;
+        double acc[WT::RBW][WT::CBW][2];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
+        for (int x = 0; x < WT::RBW; ++x)
+#pragma unroll
+            for (int y = 0; y < WT::CBW; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
         {
-            const int rr = warp * 8 + m;
-            const bool rowok = rr < rows;
-            const uint32_t t = uint32_t(row0) + uint32_t(rowok ? rr : 0);
-            const uint32_t q = t / uint32_t(R);
-            const double* fr = fast + int(t - q * uint32_t(R)) * LD;
-            const double* sr = slow + int(q - g0) * R;
+            const double* fr[WT::RBW];
+            const double* sr[WT::RBW];
+            bool rowok[WT::RBW];
+#pragma unroll
+            for (int x = 0; x < WT::RBW; ++x) {
+                const int rr = rw0 + x * 8 + m;
+                rowok[x] = rr < rows;
+                const uint32_t t = uint32_t(row0) + uint32_t(rowok[x] ? rr : 0);
+                const uint32_t q = t / uint32_t(R);
+                fr[x] = fast + int(t - q * uint32_t(R)) * LD;
+                sr[x] = slow + int(q - g0) * R;
+            }
 #pragma unroll
             for (int k4 = 0; k4 < RM / 4; ++k4) {
                 const int k = 4 * k4 + kq;
-                const double av = (rowok && k < R) ? fr[k] * sr[k] : 0.0;
+                double af[WT::RBW];
 #pragma unroll
-                for (int b = 0; b < NB; ++b)
-                    dmma(acc[b][0], acc[b][1], av, w1[(4 * k4 + kq) * LD + b * 8 + m]);
+                for (int x = 0; x < WT::RBW; ++x)
+                    af[x] = (rowok[x] && k < R) ? fr[x][k] * sr[x][k] : 0.0;
+#pragma unroll
+                for (int y = 0; y < WT::CBW; ++y) {
+                    const double bv = w1[(4 * k4 + kq) * LD + cw0 + y * 8 + m];
+#pragma unroll
+                    for (int x = 0; x < WT::RBW; ++x)
+                        dmma(acc[x][y][0], acc[x][y][1], af[x], bv);
+                }
             }
         }
-        {
-            const int r = warp * 8 + m;
 #pragma unroll
-            for (int b = 0; b < NB; ++b) {
-                const int c = b * 8 + 2 * kq;
-                zt[r * LD + c] = acc[b][0];
-                zt[r * LD + c + 1] = acc[b][1];
+        for (int x = 0; x < WT::RBW; ++x) {
+            const int r = rw0 + x * 8 + m;
+#pragma unroll
+            for (int y = 0; y < WT::CBW; ++y) {
+                const int c = cw0 + y * 8 + 2 * kq;
+                zt[r * LD + c] = acc[x][y][0];
+                zt[r * LD + c + 1] = acc[x][y][1];
                 if (r < rows) {
                     double* q = a.q1 + (row0 + r) * R;
-                    if (c < R) q[c] = acc[b][0];
-                    if (c + 1 < R) q[c + 1] = acc[b][1];
+                    if (c < R) q[c] = acc[x][y][0];
+                    if (c + 1 < R) q[c + 1] = acc[x][y][1];
                 }
             }
         }
@@ -264,7 +294,7 @@ __global__ void __launch_bounds__(kNT) zqr_rows_gemm_kernel(ZqrArgs a) {
 // Q0 = Q1 W2 (W2 = U2^-1, near the identity) on DMMA, kGT rows per tile.
 template <int RM>
 __global__ void __launch_bounds__(kNT, 2) zqr_apply_gemm_kernel(ZqrArgs a) {
-    constexpr int LD = ZgSmem<RM>::LD, NB = RM / 8;
+    constexpr int LD = ZgSmem<RM>::LD;
     extern __shared__ double sm[];
     const int R = a.R;
     double* w2 = sm;            // RM x LD
@@ -288,24 +318,35 @@ __global__ void __launch_bounds__(kNT, 2) zqr_apply_gemm_kernel(ZqrArgs a) {
             qt[r * LD + c] = (r < rows && c < R) ? __ldcs(a.q1 + (row0 + r) * R + c) : 0.0;
         }
         __syncthreads();
-        double acc[NB][2];
+        using WT = WarpTile<RM>;
+        const int rw0 = (warp % WT::RG) * WT::WR, cw0 = (warp / WT::RG) * WT::WC;
+        double acc[WT::RBW][WT::CBW][2];
 #pragma unroll
-        for (int b = 0; b < NB; ++b) acc[b][0] = acc[b][1] = 0.0;
+        for (int x = 0; x < WT::RBW; ++x)
+#pragma unroll
+            for (int y = 0; y < WT::CBW; ++y) acc[x][y][0] = acc[x][y][1] = 0.0;
 #pragma unroll
         for (int k4 = 0; k4 < RM / 4; ++k4) {
-            const double av = qt[(warp * 8 + m) * LD + 4 * k4 + kq];
+            double af[WT::RBW];
 #pragma unroll
-            for (int b = 0; b < NB; ++b)
-                dmma(acc[b][0], acc[b][1], av, w2[(4 * k4 + kq) * LD + b * 8 + m]);
+            for (int x = 0; x < WT::RBW; ++x) af[x] = qt[(rw0 + x * 8 + m) * LD + 4 * k4 + kq];
+#pragma unroll
+            for (int y = 0; y < WT::CBW; ++y) {
+                const double bv = w2[(4 * k4 + kq) * LD + cw0 + y * 8 + m];
+#pragma unroll
+                for (int x = 0; x < WT::RBW; ++x) dmma(acc[x][y][0], acc[x][y][1], af[x], bv);
+            }
         }
-        const int r = warp * 8 + m;
-        if (r < rows) {
+#pragma unroll
+        for (int x = 0; x < WT::RBW; ++x) {
+            const int r = rw0 + x * 8 + m;
+            if (r >= rows) continue;
             double* q = a.q0 + (row0 + r) * R;
 #pragma unroll
-            for (int b = 0; b < NB; ++b) {
-                const int c = b * 8 + 2 * kq;
-                if (c < R) q[c] = acc[b][0];
-                if (c + 1 < R) q[c + 1] = acc[b][1];
+            for (int y = 0; y < WT::CBW; ++y) {
+                const int c = cw0 + y * 8 + 2 * kq;
+                if (c < R) q[c] = acc[x][y][0];
+                if (c + 1 < R) q[c + 1] = acc[x][y][1];
             }
         }
     }
