@@ -204,6 +204,27 @@ __global__ void __launch_bounds__(kNT) zqr_rows_gemm_kernel(ZqrArgs a) {
     }
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = lane >> 2, kq = lane & 3;
+    // G2 partial in registers for the whole CTA: the (nt(nt+1)/2) upper 8x8
+    // blocks dealt round-robin to the warps (up to kGP each), every block one
+    // DMMA chain over the tile rows -- no shared-memory read-modify-write per
+    // tile, independent chains per warp
+    constexpr int NT8 = RM / 8, NPAIR = NT8 * (NT8 + 1) / 2;
+    constexpr int kGP = (NPAIR + kNT / 32 - 1) / (kNT / 32);
+    int gpa[kGP], gpb[kGP];
+    double gacc[kGP][2];
+#pragma unroll
+    for (int j = 0; j < kGP; ++j) {
+        const int pidx = warp + j * (kNT / 32);
+        int ti = 0, rem = pidx;
+        while (ti < NT8 && rem >= NT8 - ti) {
+            rem -= NT8 - ti;
+            ++ti;
+        }
+        const bool live = pidx < NPAIR;
+        gpa[j] = live ? ti : -1;
+        gpb[j] = live ? ti + rem : -1;
+        gacc[j][0] = gacc[j][1] = 0.0;
+    }
     const uint64_t ntiles = (a.zrows + kGT - 1) / kGT;
     for (uint64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
         const uint64_t row0 = t * kGT;
@@ -283,12 +304,36 @@ __global__ void __launch_bounds__(kNT) zqr_rows_gemm_kernel(ZqrArgs a) {
             }
         }
         __syncthreads();
-        gram_dmma<kNT>(zt, LD, rows, R, part, R, true);
+        // Gram of the Q1 tile (rows past `rows` are zero in zt)
+#pragma unroll 4
+        for (int k0 = 0; k0 < kGT; k0 += 4) {
+            const double* zr = zt + (k0 + kq) * LD;
+#pragma unroll
+            for (int j = 0; j < kGP; ++j) {
+                if (gpa[j] < 0) continue;
+                dmma(gacc[j][0], gacc[j][1], zr[gpa[j] * 8 + m], zr[gpb[j] * 8 + m]);
+            }
+        }
     }
-    __syncthreads();
+    // C[m][2kq + {0,1}] of each block; the mirrored copy of an off-diagonal
+    // block is written by the same lane (one writer per entry)
     double* out = a.work + kPartOff * R * R + size_t(blockIdx.x) * R * R;
-#pragma unroll 1
-    for (int e = threadIdx.x; e < R * R; e += kNT) out[e] = part[e];
+#pragma unroll
+    for (int j = 0; j < kGP; ++j) {
+        if (gpa[j] < 0) continue;
+        const int r = gpa[j] * 8 + m, cc = gpb[j] * 8 + 2 * kq;
+        if (r < R) {
+            if (cc < R) {
+                out[r * R + cc] = gacc[j][0];
+                if (gpa[j] != gpb[j]) out[cc * R + r] = gacc[j][0];
+            }
+            if (cc + 1 < R) {
+                out[r * R + cc + 1] = gacc[j][1];
+                if (gpa[j] != gpb[j]) out[(cc + 1) * R + r] = gacc[j][1];
+            }
+        }
+    }
+    (void)part;
 }
 
 // Q0 = Q1 W2 (W2 = U2^-1, near the identity) on DMMA, kGT rows per tile.
