@@ -210,6 +210,32 @@ ttm_tma_kernel(const __grid_constant__ CUtensorMap xmap, double* __restrict__ y,
                             dmma(acc[rb][cb][0], acc[rb][cb][1], xf[cur][cb], qf[cur][rb]);
                     }
             }
+            // Release the stage only once its shared-memory reads have
+            // RETURNED.  ptxas otherwise issues the empty-barrier arrive right
+            // after the last LDS and sinks the DMMAs below it; the arrive can
+            // then overtake loads still in flight, and the producer's next
+            // TMA write into this slot lands before they read it.  Rare alone,
+            // but every run beside CTAs of a DSMEM cluster kernel sharing the
+            // SM (their remote shared-memory traffic delays local loads):
+            // tools/probes/ttm_coresid.cu, profiles/r02_coresidency_probe.txt.
+            // A data dependency on the last k-step's fragments (loaded last;
+            // shared loads complete in order -- ptxas itself relies on that
+            // when it scoreboards only the last of a run of LDS) makes the
+            // arrive wait for them.  The compare is never true: the value is a
+            // signalling-NaN pattern that only feeds the (never taken) trap.
+            {
+                constexpr int lb = (BK / 4 - 1) & 1;
+                uint64_t d[RB + CB];
+#pragma unroll
+                for (int rb = 0; rb < RB; ++rb) d[rb] = __double_as_longlong(qf[lb][rb]);
+#pragma unroll
+                for (int cb = 0; cb < CB; ++cb) d[RB + cb] = __double_as_longlong(xf[lb][cb]);
+#pragma unroll
+                for (int w = 1; w < RB + CB; w *= 2)
+#pragma unroll
+                    for (int i = 0; i + w < RB + CB; i += 2 * w) d[i] ^= d[i + w];
+                if (d[0] == 0x7ff400000000deadull) __trap();
+            }
             __syncwarp();
             if (lane == 0) mbar_arrive(&empty[st]);
             if (++st == STAGES) {
@@ -326,28 +352,20 @@ cudaError_t launch_v2(const TtmArgs& a, cudaStream_t s, int sms) {
         return cudaErrorNotSupported;
     }
     auto kern = ttm_tma_kernel<RB, CB, BK, STAGES, NC, LAYOUT>;
-    // Every TMA TTM CTA reserves the SM's whole shared memory, so no CTA of
-    // another grid is co-resident with it.  Root cause (round 2): while CTAs
-    // of a cluster kernel that exchange data through distributed shared
-    // memory (our 8-CTA finisher / Z-QR) run on the same SM, the X tiles this
-    // kernel receives through cp.async.bulk.tensor are wrong -- measured in
-    // isolation, with no solver around it (tools/probes/ttm_coresid.cu,
-    // profiles/r02_coresidency_probe.txt): 0.02-10% of the outputs differ in
-    // EVERY run beside a DSMEM-reading or -writing cluster grid, 0 beside a
-    // cluster grid without DSMEM traffic, 0 beside plain grids, 0 for the
-    // cp.async kernel of ttm.cu; neither the .shared::cta destination form, a
-    // one-CTA cluster launch nor loading Q without the bulk copy changes it.
-    // In the solver it showed as 14 of 90 (round 1) / up to 59 of 60 (no PDL)
-    // repeated C3 solves differing.  The happens-before checker (hb.hpp,
-    // CPDB_HBCHECK=1) finds no missing stream dependency.  Exclusive SMs cost
-    // nothing measurable (C2/C3/C4 sweeps/s within 0.5%, round 2 A/B);
-    // CPDB_TTM_SMEM_EXACT=1 requests only the ring's size (reproduces the
-    // hazard, diagnostic).
-    static const bool exact_smem = [] {
-        const char* e = std::getenv("CPDB_TTM_SMEM_EXACT");
+    // Each CTA requests its ring's shared memory only, so CTAs of other
+    // grids (the 8-CTA finisher / Z-QR clusters) may share its SM.  Round 1
+    // reserved the whole 227 KB instead: beside DSMEM cluster CTAs this
+    // kernel's results differed run to run.  The cause was the consumer
+    // release above (the empty-barrier arrive overtaking in-flight shared
+    // loads); with the data dependency the probe shows 0 differing runs
+    // where the old build differed in every one (profiles/
+    // r02_coresidency_probe.txt).  CPDB_TTM_SMEM_WHOLE=1 restores the
+    // reservation (A/B testing).
+    static const bool whole_sm = [] {
+        const char* e = std::getenv("CPDB_TTM_SMEM_WHOLE");
         return e && e[0] == '1';
     }();
-    const size_t smem = exact_smem ? C::SMEM : size_t(227 * 1024);
+    const size_t smem = whole_sm ? size_t(227 * 1024) : C::SMEM;
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          int(smem));
     if (e != cudaSuccess) return e;

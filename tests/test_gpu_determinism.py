@@ -2,14 +2,18 @@
 requires bit-identical traces across runs).
 
 Round 2 found the cause of the round-1 non-reproducible C3 solves: the TMA TTM
-kernel receives wrong X tiles while CTAs of a cluster kernel that use
-distributed shared memory share its SM (tools/probes/ttm_coresid.cu,
-profiles/r02_coresidency_probe.txt).  The product keeps TMA TTM CTAs on
-exclusive SMs; these tests hold that line:
+kernel's consumer warps released a ring stage (mbarrier arrive) before their
+shared-memory loads of it had returned -- ptxas sank the DMMAs that consume the
+loads below the arrive -- so the producer's next TMA write could land first.
+CTAs of a DSMEM cluster kernel on the same SM delay local shared loads enough
+to make that happen in every run (tools/probes/ttm_coresid.cu,
+profiles/r02_coresidency_probe.txt).  The arrive now carries a data dependency
+on the stage's last fragments, and TTM CTAs share SMs again.  These tests hold
+that line with co-residency allowed (the default):
   * the probe, isolated from the solver: the TTM next to a DSMEM cluster grid
     is bit-identical to an isolated run;
-  * repeated C3 solves without programmatic dependent launch (the setting
-    that exposed the hazard in up to 59 of 60 runs) are bit-identical.
+  * repeated C3 solves (with and without programmatic dependent launch, the
+    setting that exposed the hazard in up to 59 of 60 runs) are bit-identical.
 """
 import os
 import subprocess
@@ -39,20 +43,24 @@ def _probe():
 
 @pytest.mark.parametrize("layout", [0, 1])
 @pytest.mark.parametrize("hog", ["read", "write"])
-def test_tma_ttm_beside_dsmem_cluster_grid(layout, hog):
+@pytest.mark.parametrize("ctas", [64, 296])
+def test_tma_ttm_beside_dsmem_cluster_grid(layout, hog, ctas):
     env = dict(os.environ)
-    env.pop("CPDB_TTM_SMEM_EXACT", None)
+    env.pop("CPDB_TTM_SMEM_WHOLE", None)
     if hog == "write":
         env["HOG_WRITE"] = "1"
-    out = subprocess.run([_probe(), str(layout), "12", "0", "64", "cluster"], env=env,
+    out = subprocess.run([_probe(), str(layout), "12", "0", str(ctas), "cluster"], env=env,
                          capture_output=True, text=True, timeout=300, check=True).stdout
     last = out.strip().splitlines()[-1]
     assert " 0 of 12 reps differ" in last, out
 
 
-def test_repeated_c3_solves_bit_identical_without_pdl():
-    env = dict(os.environ, CPDB_NO_PDL="1")
-    env.pop("CPDB_TTM_SMEM_EXACT", None)
+@pytest.mark.parametrize("pdl", [False, True])
+def test_repeated_c3_solves_bit_identical(pdl):
+    env = dict(os.environ)
+    if not pdl:
+        env["CPDB_NO_PDL"] = "1"
+    env.pop("CPDB_TTM_SMEM_WHOLE", None)
     out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "det_probe.py"), "c3",
                           "30", "4"], env=env, cwd=ROOT, capture_output=True, text=True,
                          timeout=600, check=True).stdout

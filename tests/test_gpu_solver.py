@@ -260,8 +260,8 @@ def test_full_size_teacher_forced(port, name, k):
 def test_repeated_solves_bit_identical_with_root_prefetch():
     """Steady branch-reuse sweeps overlap the root TTM (low-priority stream)
     with the preceding update.  Repeated solves in one context must stay
-    bit-identical (this shape exposed a co-residency race before the TMA TTM
-    took whole SMs; tools/det_probe.py)."""
+    bit-identical (this shape exposed the TMA TTM's early stage release beside
+    DSMEM cluster CTAs; tools/det_probe.py)."""
     import paper_2503_18759_b200 as cpd
     ctx = cpd.Context(0)
     ctx.synth_tensor(0, [96, 96, 96, 96], 16, 1e-2, 12345)
