@@ -190,6 +190,20 @@ cudaError_t sum_slots_scatter(const double* slots, uint64_t stride, uint32_t wor
 cudaError_t sum_slots(const double* slots, uint64_t stride, uint32_t world, uint64_t n,
                       double* out, cudaStream_t s);
 
+// ---------------------------------------------------------------- wide ranks
+// R > 64 (widerank.cu): the same launch interfaces served by rank-generic
+// kernels (Khatri-Rao + cooperative Householder QR, row solves, exact
+// normalisation) -- launch_zqr / launch_finish / launch_vgemm dispatch here.
+bool wide_rank(uint32_t R);
+size_t zqr_wide_work_doubles(uint32_t R);
+size_t finish_wide_scratch_doubles(uint64_t I, uint32_t R);
+cudaError_t launch_zqr_wide(const ZqrArgs& a, cudaStream_t s);
+cudaError_t launch_finish_wide(const FinishArgs& a, cudaStream_t s);
+// thin_qr (linalg.hpp:39-99) on the cooperative kernel; work = m*n +
+// zqr_wide_work_doubles(n)
+cudaError_t householder_qr_wide(const double* a, uint64_t m, uint32_t n, double* work, double* q,
+                                double* r, cudaStream_t s);
+
 // ---------------------------------------------------------------- misc
 // normalize_columns (linalg.hpp:225-242) with the reference's exact
 // operation order (sequential column sums, no FMA contraction).

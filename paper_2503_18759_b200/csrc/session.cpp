@@ -237,8 +237,8 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         if (cfg.rank > c->dims[k])
             fail(CPDB_INVALID_ARGUMENT,
                  "cp_als_qr: rank must not exceed any mode extent (compact QR)");
-    if (cfg.rank > 64)
-        fail(CPDB_INVALID_ARGUMENT, "cp_als_qr: ranks above 64 are not supported on the device");
+    if (cfg.rank > 1024)
+        fail(CPDB_INVALID_ARGUMENT, "cp_als_qr: ranks above 1024 are not supported on the device");
     R = static_cast<uint32_t>(cfg.rank);
     Rp = ttm_rpad(R);
     extrap = cfg.extrapolate != 0;
@@ -383,7 +383,9 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         CPDB_CK(cudaMemcpyAsync(lam.p, l.data(), R * sizeof(double), cudaMemcpyHostToDevice, s));
         CPDB_CK(cudaStreamSynchronize(s));
     }
-    for (DevBuf& b : fscratch) b.ensure(maxI * (R + 1));
+    // (wide ranks: A_hat, the Householder working copy and its partials)
+    for (DevBuf& b : fscratch)
+        b.ensure(wide_rank(R) ? finish_wide_scratch_doubles(maxI, R) : maxI * (R + 1));
     vout.ensure(maxI * R);
     fitbuf.ensure(8);
     for (ZBuf& z : zb) {
@@ -1302,6 +1304,11 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
                       cpdb_q0_observer observer, void* user) {
     uint64_t rows_out = 0;
     const uint64_t last_sweep = plan.sweeps.size();
+    if (ended) fail(CPDB_LOGIC_ERROR, "session: run() after end() took back speculative work");
+    // A resumable session keeps the device pipeline full across run() calls:
+    // the last sweep of this call still issues the next sweep's first update
+    // ahead of its host sync (the next call consumes it; end() undoes it).
+    const bool across = observer == nullptr && fps == nullptr && lps == nullptr;
     while (rows_out < nsweeps && !converged && done < last_sweep) {
         const uint64_t sweep = done + 1;
         const Sweep& sw = plan.sweeps[sweep - 1];
@@ -1315,7 +1322,7 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         const bool tail_low = low_tail && long_root && order == 3 && dep_events && speculate &&
                               !sharded &&
                               observer == nullptr && fps == nullptr && lps == nullptr &&
-                              (!extrap || has_beta) && rows_out + 1 < nsweeps &&
+                              (!extrap || has_beta) && (rows_out + 1 < nsweeps || across) &&
                               done + 1 < last_sweep;
         for (uint32_t b = 0; b < order; ++b) {
             const bool low = tail_low && b == order - 1;
@@ -1359,7 +1366,7 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         // Hide the host round trip: the next sweep's first Z-QR + TTM chain do
         // not depend on the beta gate, so they go on the stream before the
         // host waits for this sweep's fitness (wasted only if it converges).
-        const bool more = rows_out + 1 < nsweeps && done + 1 < last_sweep;
+        const bool more = (rows_out + 1 < nsweeps || across) && done + 1 < last_sweep;
         if (more && observer == nullptr && fps == nullptr) {
             mode_update_front(sweep + 1, 0, nullptr, nullptr);
             front_issued = true;
@@ -1407,7 +1414,15 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
                         front1_issued = true;
                     }
                 } else {
+                    // beta still open: the update takes the gate's decision on
+                    // the device, behind this sweep's finisher on the main
+                    // stream; its successor's front (root prefetch included)
+                    // follows it without waiting for the host either
                     mode_update_back(sweep + 1, 0, unused);
+                    if (order > 2 && dep_events) {
+                        mode_update_front(sweep + 1, 1, nullptr, nullptr);
+                        front1_issued = true;
+                    }
                 }
                 spec.issued = true;
                 spec.beta_used = 0.0;
@@ -1538,6 +1553,13 @@ void Session::undo_speculative_update() {
 
 // ---------------------------------------------------------------- results
 void Session::end(cpdb_state* state, double* out_lambda, double* out_factors) {
+    // work issued ahead for a sweep the caller never ran: take it back so the
+    // exported state is the one after `done` sweeps (the reference's)
+    if (spec.issued) undo_speculative_update();
+    if (front_issued || front1_issued) {
+        CPDB_CK(cudaDeviceSynchronize());
+        ended = true;
+    }
     auto get_factors = [&](double* dst) {
         uint64_t off = 0;
         for (uint32_t k = 0; k < order; ++k) {

@@ -153,6 +153,7 @@ struct Session {
         cudaEvent_t ev = nullptr;
     } pf;
     void launch_prefetch();
+    bool ended = false;          // end() took back work issued ahead: no further run()
     bool front1_issued = false;  // next sweep's second front issued ahead (Session::run)
     DevBuf pre;
     cudaEvent_t ev_fin = nullptr;

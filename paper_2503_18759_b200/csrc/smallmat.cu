@@ -77,6 +77,7 @@ vgemm_kernel(VgemmArgs a, uint64_t kchunk) {
     __shared__ double pt[kVBK][RM];
     __shared__ double ft[DUAL ? kVBK : 1][RM];
     const int R = a.R;
+    const int rbase = int(blockIdx.z) * RM;  // column block (ranks wider than RM)
     const uint64_t I = a.I, J = a.J, K = a.O * a.J;
     const uint64_t i0 = uint64_t(blockIdx.x) * kVBI;
     const uint64_t kb = uint64_t(blockIdx.y) * kchunk;
@@ -113,7 +114,7 @@ vgemm_kernel(VgemmArgs a, uint64_t kchunk) {
             yt[r_][c_] = v;
         }
         for (int e = threadIdx.x; e < kVBK * RM; e += kVThreads) {
-            const int kk = e / RM, r = e % RM;
+            const int kk = e / RM, r = rbase + e % RM;
             const uint64_t k = k0 + kk;
             double q = 0.0, p = 0.0;
             if (k < ke && r < R) {
@@ -121,8 +122,8 @@ vgemm_kernel(VgemmArgs a, uint64_t kchunk) {
                 p = q;
                 if (ex) p = q + beta * (q - a.alpha * a.hist[k * R + r]);
             }
-            pt[kk][r] = p;
-            if (DUAL) ft[kk][r] = q;
+            pt[kk][r - rbase] = p;
+            if (DUAL) ft[kk][r - rbase] = q;
         }
         __syncthreads();
 #pragma unroll 4
@@ -142,7 +143,7 @@ vgemm_kernel(VgemmArgs a, uint64_t kchunk) {
         double* fp = DUAL ? a.vfitpart + (uint64_t(blockIdx.y) * I + i) * R : nullptr;
 #pragma unroll
         for (int u = 0; u < RPT; ++u) {
-            const int r = rg + 4 * u;
+            const int r = rbase + rg + 4 * u;
             if (r < R) {
                 vp[r] = acc[u];
                 if (DUAL) fp[r] = accf[u];
@@ -701,12 +702,13 @@ template <int RM, bool DUAL>
 cudaError_t vgemm_run(VgemmArgs& a, cudaStream_t s, int sms) {
     const uint64_t K = a.O * a.J;
     a.reduced = 0;
+    const bool wide = a.R > uint32_t(RM);  // column blocks of the plain kernel
     // short K: one cluster per 64-row block, chunks summed on chip
     static const bool cluster_ok = [] {
         const char* e = std::getenv("CPDB_VGEMM_CLUSTER");
         return !(e && e[0] == '0');
     }();
-    if (RM >= 8 && cluster_ok && a.v_out && (!DUAL || a.vfit_out) &&
+    if (RM >= 8 && !wide && cluster_ok && a.v_out && (!DUAL || a.vfit_out) &&
         (K + kDK - 1) / kDK <= uint64_t(kVCluster) * kVClusterTiles) {
         const uint64_t iblocks = (a.I + kDM - 1) / kDM;
         const uint64_t ktiles = (K + kDK - 1) / kDK;
@@ -737,7 +739,7 @@ cudaError_t vgemm_run(VgemmArgs& a, cudaStream_t s, int sms) {
         const char* e = std::getenv("CPDB_VGEMM_WIDE");
         return !(e && e[0] == '0');
     }();
-    if (RM == 64 && a.R > 32 && wide_ok && (a.J % kWK == 0 || a.J == 1) && K >= (1ull << 16) &&
+    if (RM == 64 && !wide && a.R > 32 && wide_ok && (a.J % kWK == 0 || a.J == 1) && K >= (1ull << 16) &&
         (a.I % 2 == 0)) {
         const uint64_t iblocks = (a.I + WideCfg<DUAL>::WI - 1) / WideCfg<DUAL>::WI;
         const uint64_t ktiles = (K + kWK - 1) / kWK;
@@ -755,7 +757,7 @@ cudaError_t vgemm_run(VgemmArgs& a, cudaStream_t s, int sms) {
         vgemm_wide_kernel<DUAL><<<grid, kWT, smem, s>>>(a, kchunk);
         return cudaGetLastError();
     }
-    if (RM >= 8 && K < (1ull << 32)) {  // DMMA path
+    if (RM >= 8 && !wide && K < (1ull << 32)) {  // DMMA path
         const uint64_t iblocks = (a.I + kDM - 1) / kDM;
         const uint64_t ktiles = (K + kDK - 1) / kDK;
         uint64_t nsplit = std::max<uint64_t>(1, (2 * uint64_t(sms)) / iblocks);
@@ -780,7 +782,7 @@ cudaError_t vgemm_run(VgemmArgs& a, cudaStream_t s, int sms) {
     const uint64_t kchunk = ((ktiles + nsplit - 1) / nsplit) * kVBK;
     nsplit = (K + kchunk - 1) / kchunk;
     a.nsplit = uint32_t(nsplit);
-    const dim3 grid{unsigned(iblocks), unsigned(nsplit), 1u};
+    const dim3 grid{unsigned(iblocks), unsigned(nsplit), unsigned((a.R + RM - 1) / RM)};
     // plain launch: V waits on the Z-QR's event (side stream), which
     // programmatic serialisation must not relax
     vgemm_kernel<RM, DUAL><<<grid, kVThreads, 0, s>>>(a, kchunk);
@@ -876,8 +878,8 @@ cudaError_t launch_vgemm(VgemmArgs& a, cudaStream_t s, int sms) {
     if (a.R <= 8) return d ? vgemm_run<8, true>(a, s, sms) : vgemm_run<8, false>(a, s, sms);
     if (a.R <= 16) return d ? vgemm_run<16, true>(a, s, sms) : vgemm_run<16, false>(a, s, sms);
     if (a.R <= 32) return d ? vgemm_run<32, true>(a, s, sms) : vgemm_run<32, false>(a, s, sms);
-    if (a.R <= 64) return d ? vgemm_run<64, true>(a, s, sms) : vgemm_run<64, false>(a, s, sms);
-    return cudaErrorInvalidValue;
+    // (wider ranks: 64-column blocks of the plain kernel, widerank.cu)
+    return d ? vgemm_run<64, true>(a, s, sms) : vgemm_run<64, false>(a, s, sms);
 }
 
 cudaError_t reduce_splits(const double* part, uint32_t nsplit, uint64_t n, double* out,

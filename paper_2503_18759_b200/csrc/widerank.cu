@@ -1,0 +1,355 @@
+// Wide ranks (R > 64): the mode-update tail in rank-generic kernels.
+//
+// The tuned kernels (zqr.cu, cluster.cu, smallmat.cu, finish.cu) keep a whole
+// R x R triangle and R-wide rows in shared memory / registers and are
+// instantiated for R <= 64 -- the BASELINE configs.  The reference accepts any
+// rank up to the smallest extent (solvers.hpp:221-224), so beyond 64 the same
+// launch interfaces (ZqrArgs / FinishArgs, kernels.hpp) are served by the
+// kernels below, which follow the reference's own algorithm step by step:
+//   Z = KhatriRao(R_k, k != n)                        tensor.hpp:343-368
+//   Q0, R0 = thin_qr(Z)        Householder            linalg.hpp:39-99
+//   A_hat  = V R0^-T           row-wise back substitution   linalg.hpp:192-216
+//   lambda, A_n = normalize_columns(A_hat)            linalg.hpp:225-242
+//   Q_n, R_n = thin_qr(A_n)                           factor_state.hpp:42-47
+//   fitness_fast_qr                                   kruskal.hpp:109-128
+// The Householder QR is a cooperative multi-CTA kernel: rows are split across
+// the grid, each reflector costs two grid barriers (column norm, then the
+// dot products with the trailing columns), every sum runs in a fixed order
+// (deterministic), and the conventions are the reference's (alpha = -sign
+// ||x||, zero columns skipped, nonnegative diag(R) by a final sign flip).
+#include <cooperative_groups.h>
+
+#include <algorithm>
+
+#include "device.cuh"
+#include "kernels.hpp"
+#include "prims.hpp"
+
+namespace cg = cooperative_groups;
+
+namespace cpdb {
+namespace {
+
+constexpr int kHT = 256;        // threads per CTA
+constexpr int kHW = kHT / 32;   // warps = row groups
+constexpr int kMaxWide = 1024;  // widest supported matrix (columns)
+
+// Z rows in the natural order of the final Y: digits over the other modes in
+// ascending mode order, the last fastest (ZqrArgs, kernels.hpp).
+__global__ void kr_natural_kernel(ZqrArgs a, double* z) {
+    const uint32_t R = a.R;
+    const uint64_t n = a.zrows * R;
+    for (uint64_t e = blockIdx.x * uint64_t(blockDim.x) + threadIdx.x; e < n;
+         e += uint64_t(gridDim.x) * blockDim.x) {
+        uint64_t rem = e / R;
+        const uint32_t j = uint32_t(e % R);
+        double p = 1.0;
+        for (int k = int(a.nm) - 1; k >= 0; --k) {
+            const uint64_t d = rem % R;
+            rem /= R;
+            p = __dmul_rn(p, a.rmats[k][d * R + j]);
+        }
+        z[e] = p;
+    }
+}
+
+struct HhArgs {
+    double* w;        // m x n, row-major; in: A, out: reflectors below the diagonal
+    double* q;        // m x n out
+    double* r;        // n x n out
+    double* scratch;  // hh_scratch_doubles(n, grid)
+    uint64_t m;
+    uint32_t n;
+};
+
+__host__ __device__ inline size_t hh_scratch_doubles(uint32_t n, int grid) {
+    return size_t(2) * grid * 2 + size_t(2) * grid * n;
+}
+
+// sum of x over the CTA in a fixed order (warp tree, then warps in order)
+__device__ double cta_sum(double x, double* red) {
+    x = warp_sum(x);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = x;
+    __syncthreads();
+    double t = 0.0;
+    for (int w = 0; w < kHW; ++w) t += red[w];
+    return t;
+}
+
+// d[j] = sum over this CTA's rows i in [lo, hi) of vcoef(i) * mat[i][j], for
+// j in [j0, n): warp g takes rows lo+g, lo+g+8, ... and lanes take 32
+// consecutive columns; the warps' partials are added in warp order.
+template <class V>
+__device__ void cta_col_dots(const double* mat, uint32_t n, uint64_t lo, uint64_t hi, uint32_t j0,
+                             V vcoef, double* part /*[kHW][n]*/, double* out /*[n]*/) {
+    const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint32_t jb = (j0 / 32) * 32; jb < n; jb += 32) {
+        const uint32_t j = jb + lane;
+        double d = 0.0;
+        if (j < n)
+            for (uint64_t i = lo + g; i < hi; i += kHW) d = fma(vcoef(i), mat[i * n + j], d);
+        if (j < n) part[g * n + j] = d;
+    }
+    __syncthreads();
+    for (uint32_t j = j0 + threadIdx.x; j < n; j += kHT) {
+        double t = 0.0;
+        for (int w = 0; w < kHW; ++w) t += part[w * n + j];
+        out[j] = t;
+    }
+}
+
+__global__ void __launch_bounds__(kHT) hh_coop_kernel(HhArgs a) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ double sm[];
+    __shared__ double red[kHW];
+    const uint32_t n = a.n;
+    const uint64_t m = a.m;
+    double* betas = sm;           // n
+    double* vdiag = betas + n;    // n: v_k[0] = w_kk - alpha
+    double* sgn = vdiag + n;      // n: -1 where R(k,k) < 0
+    double* dsh = sgn + n;        // n
+    double* part = dsh + n;       // kHW x n
+    const int G = int(gridDim.x), c = int(blockIdx.x);
+    const uint64_t chunk = (m + G - 1) / G;
+    const uint64_t row0 = uint64_t(c) * chunk < m ? uint64_t(c) * chunk : m;
+    const uint64_t row1 = row0 + chunk < m ? row0 + chunk : m;
+    double* pn = a.scratch;                       // [2][G][2]: (w_kk^2 owner term, tail sum)
+    double* pd = a.scratch + size_t(2) * G * 2;   // [2][G][n]
+    double* w = a.w;
+
+    // ---- factorisation: reflector k from column k, applied to columns > k
+    for (uint32_t k = 0; k < n; ++k) {
+        // (a) tail = sum_{i > k} w_ik^2 over the whole column (fixed order)
+        double t = 0.0;
+        for (uint64_t i = (row0 > k ? row0 : uint64_t(k) + 1) + threadIdx.x; i < row1; i += kHT)
+            t = fma(w[i * n + k], w[i * n + k], t);
+        t = cta_sum(t, red);
+        double* pnk = pn + size_t(k & 1) * G * 2;
+        if (threadIdx.x == 0) pnk[c * 2] = t;
+        grid.sync();
+        double tail = 0.0;
+        for (int b = 0; b < G; ++b) tail += pnk[b * 2];
+        const double wkk = w[uint64_t(k) * n + k];
+        const double norm = sqrt(fma(wkk, wkk, tail));
+        if (norm == 0.0) {  // zero column: R(k,k) stays 0 (uniform over the grid)
+            if (threadIdx.x == 0) {
+                betas[k] = 0.0;
+                vdiag[k] = 0.0;
+                sgn[k] = 1.0;
+            }
+            __syncthreads();
+            continue;
+        }
+        const double alpha = wkk >= 0.0 ? -norm : norm;
+        const double v0 = wkk - alpha;
+        const double beta = 2.0 / fma(v0, v0, tail);
+        if (threadIdx.x == 0) {
+            betas[k] = beta;
+            vdiag[k] = v0;
+            sgn[k] = alpha < 0.0 ? -1.0 : 1.0;
+        }
+        // (b) d_j = sum_{i >= k} v_i w_ij, j > k
+        const uint64_t lo = row0 > k ? row0 : uint64_t(k);
+        auto vco = [&](uint64_t i) { return i == k ? v0 : w[i * n + k]; };
+        double* pdk = pd + size_t(k & 1) * G * n;
+        cta_col_dots(w, n, lo, row1, k + 1, vco, part, pdk + size_t(c) * n);
+        grid.sync();
+        for (uint32_t j = k + 1 + threadIdx.x; j < n; j += kHT) {
+            double s = 0.0;
+            for (int b = 0; b < G; ++b) s += pdk[size_t(b) * n + j];
+            dsh[j] = s * beta;
+        }
+        __syncthreads();
+        // (c) w_ij -= (beta d_j) v_i on this CTA's rows; column k keeps v below
+        // the diagonal and alpha on it
+        {
+            const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+            for (uint64_t i = lo + g; i < row1; i += kHW) {
+                const double vi = vco(i);
+                for (uint32_t j = ((k + 1) / 32) * 32 + lane; j < n; j += 32)
+                    if (j > k) w[i * n + j] = fma(-dsh[j], vi, w[i * n + j]);
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0 && k >= row0 && k < row1) w[uint64_t(k) * n + k] = alpha;
+        __syncthreads();
+    }
+    grid.sync();
+    // ---- R (upper triangle, rows flipped to a nonnegative diagonal)
+    for (uint64_t e = uint64_t(c) * kHT + threadIdx.x; e < uint64_t(n) * n; e += uint64_t(G) * kHT) {
+        const uint32_t i = uint32_t(e / n), j = uint32_t(e % n);
+        a.r[e] = j >= i ? w[e] * sgn[i] : 0.0;
+    }
+    // ---- Q = H_0 ... H_{n-1} [I; 0], reflectors applied in descending order
+    double* q = a.q;
+    for (uint64_t e = row0 * n + threadIdx.x; e < row1 * n; e += kHT)
+        q[e] = (e / n == e % n) ? 1.0 : 0.0;
+    __syncthreads();
+    uint32_t it = 0;  // applied reflectors: parity of the partials buffer
+    for (int k = int(n) - 1; k >= 0; --k) {
+        const double beta = betas[k];
+        if (beta == 0.0) continue;
+        const double v0 = vdiag[k];
+        const uint64_t lo = row0 > uint64_t(k) ? row0 : uint64_t(k);
+        auto vco = [&](uint64_t i) { return i == uint64_t(k) ? v0 : w[i * n + k]; };
+        double* pdk = pd + size_t(it++ & 1) * G * n;
+        // (columns j < k of rows >= k are still zero)
+        cta_col_dots(q, n, lo, row1, uint32_t(k), vco, part, pdk + size_t(c) * n);
+        grid.sync();
+        for (uint32_t j = uint32_t(k) + threadIdx.x; j < n; j += kHT) {
+            double s = 0.0;
+            for (int b = 0; b < G; ++b) s += pdk[size_t(b) * n + j];
+            dsh[j] = s * beta;
+        }
+        __syncthreads();
+        const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        for (uint64_t i = lo + g; i < row1; i += kHW) {
+            const double vi = vco(i);
+            for (uint32_t j = (uint32_t(k) / 32) * 32 + lane; j < n; j += 32)
+                if (j >= uint32_t(k)) q[i * n + j] = fma(-dsh[j], vi, q[i * n + j]);
+        }
+        __syncthreads();
+    }
+    for (uint64_t e = row0 * n + threadIdx.x; e < row1 * n; e += kHT)
+        if (sgn[e % n] < 0.0) q[e] = -q[e];
+}
+
+int wide_sms() {
+    static const int n = [] {
+        int dev = 0, v = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+        return v > 0 ? v : 1;
+    }();
+    return n;
+}
+
+// one CTA per SM at most (cooperative launch: all CTAs co-resident)
+cudaError_t hh_launch(const HhArgs& a, cudaStream_t s) {
+    const int sms = wide_sms();
+    if (a.n > uint32_t(kMaxWide)) return cudaErrorInvalidValue;
+    const size_t smem = (size_t(4) + kHW) * a.n * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(hh_coop_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    int grid = int(std::min<uint64_t>(uint64_t(sms), (a.m + 63) / 64));
+    grid = std::max(grid, 1);
+    HhArgs args = a;
+    void* params[] = {&args};
+    return cudaLaunchCooperativeKernel(reinterpret_cast<void*>(hh_coop_kernel), dim3(grid),
+                                       dim3(kHT), params, smem, s);
+}
+
+// A_hat = V R0^-T (x R0^T = v per row): warp per row, the row in shared
+// memory, back substitution with lane-split dot products.  status gets
+// 1 | col << 8 for a ~0 diagonal entry (same test as the reference).
+__global__ void __launch_bounds__(kHT)
+solve_rows_wide_kernel(const double* v, const double* r0, uint32_t n, uint64_t rows, double* x,
+                       int* status) {
+    extern __shared__ double sm[];
+    __shared__ int bad;
+    if (threadIdx.x == 0) {
+        double mx = 0.0;
+        for (uint32_t i = 0; i < n; ++i) mx = fmax(mx, fabs(r0[size_t(i) * n + i]));
+        bad = -1;
+        for (uint32_t i = 0; i < n; ++i)
+            if (fabs(r0[size_t(i) * n + i]) <= 1e-14 * mx) {
+                bad = int(i);
+                break;
+            }
+        if (bad >= 0 && blockIdx.x == 0) atomicOr(status, 1 | (bad << 8));
+    }
+    __syncthreads();
+    if (bad >= 0) return;
+    const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* xr = sm + size_t(g) * n;
+    for (uint64_t row = uint64_t(blockIdx.x) * kHW + g; row < rows; row += uint64_t(gridDim.x) * kHW) {
+        for (uint32_t j = lane; j < n; j += 32) xr[j] = v[row * n + j];
+        __syncwarp();
+        for (int c = int(n) - 1; c >= 0; --c) {
+            double s = 0.0;
+            for (uint32_t j = uint32_t(c) + 1 + lane; j < n; j += 32)
+                s = fma(xr[j], r0[size_t(c) * n + j], s);
+            s = warp_sum(s);
+            if (lane == 0) xr[c] = (xr[c] - s) / r0[size_t(c) * n + c];
+            __syncwarp();
+        }
+        for (uint32_t j = lane; j < n; j += 32) x[row * n + j] = xr[j];
+        __syncwarp();
+    }
+}
+
+__global__ void fit_copy_kernel(const double* out4, double* fit_out) {
+    fit_out[0] = out4[2];
+    fit_out[1] = out4[3];
+}
+
+}  // namespace
+
+bool wide_rank(uint32_t R) { return R > 64; }
+
+size_t zqr_wide_work_doubles(uint32_t R) { return hh_scratch_doubles(R, wide_sms()) + 8; }
+
+size_t finish_wide_scratch_doubles(uint64_t I, uint32_t R) {
+    return 2 * I * R + hh_scratch_doubles(R, wide_sms()) + 16;
+}
+
+// Z into q1 (the kernel's working copy), Householder in place, Q0 / R0 out.
+cudaError_t launch_zqr_wide(const ZqrArgs& a, cudaStream_t s) {
+    const uint64_t n = a.zrows * a.R;
+    const unsigned grid = unsigned(std::min<uint64_t>((n + 255) / 256, 8192));
+    kr_natural_kernel<<<grid, 256, 0, s>>>(a, a.q1);
+    HhArgs h{a.q1, a.q0, a.r0, a.work, a.zrows, a.R};
+    return hh_launch(h, s);
+}
+
+cudaError_t launch_finish_wide(const FinishArgs& a, cudaStream_t s) {
+    const int sms = wide_sms();
+    if (a.scratch == nullptr) return cudaErrorInvalidValue;
+    const uint64_t I = a.I;
+    const uint32_t R = a.R;
+    double* ahat = a.scratch;           // I x R
+    double* w = ahat + I * R;           // I x R: Householder working copy of A_n
+    double* hs = w + I * R;             // hh scratch
+    double* out4 = hs + hh_scratch_doubles(R, sms);
+    if (!a.init) {
+        if (a.nsplit != 1) return cudaErrorInvalidValue;
+        const unsigned grid = unsigned(std::min<uint64_t>((I + kHW - 1) / kHW, 1024));
+        const size_t smem = size_t(kHW) * R * sizeof(double);
+        cudaError_t e = cudaFuncSetAttribute(solve_rows_wide_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             int(smem));
+        if (e != cudaSuccess) return e;
+        solve_rows_wide_kernel<<<grid, kHT, smem, s>>>(a.vpart, a.r0, R, I, ahat, a.status);
+        e = cudaMemcpyAsync(a.a_out, ahat, I * R * sizeof(double), cudaMemcpyDeviceToDevice, s);
+        if (e != cudaSuccess) return e;
+        e = normalize_exact(a.a_out, I, R, a.lambda, s);
+        if (e != cudaSuccess) return e;
+    }
+    cudaError_t e = cudaMemcpyAsync(w, a.a_out, I * R * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return e;
+    HhArgs h{w, a.q_out, a.r_out, hs, I, R};
+    e = hh_launch(h, s);
+    if (e != cudaSuccess) return e;
+    e = pack_q(a.q_out, a.qp_out, uint32_t(I), R, s);
+    if (e != cudaSuccess) return e;
+    if (a.fitness && !a.init) {
+        const double* vfit = a.dual ? a.vfitpart : a.vpart;
+        e = fitness_dev(a.norm_x_sq, vfit, ahat, I, a.r0, a.r_out, a.lambda, R, out4, s);
+        if (e != cudaSuccess) return e;
+        fit_copy_kernel<<<1, 1, 0, s>>>(out4, a.fit_out);
+    }
+    return cudaGetLastError();
+}
+
+// thin_qr primitive on the cooperative kernel (a is copied into work first)
+cudaError_t householder_qr_wide(const double* a, uint64_t m, uint32_t n, double* work, double* q,
+                                double* r, cudaStream_t s) {
+    cudaError_t e = cudaMemcpyAsync(work, a, m * n * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return e;
+    HhArgs h{work, q, r, work + m * n, m, n};
+    return hh_launch(h, s);
+}
+
+}  // namespace cpdb

@@ -467,3 +467,67 @@ def test_ill_conditioned_factors_do_not_break_down(ctx, port, delta):
     assert err <= max(1e-9, 100 * floor), (err, floor)
     for t, b in zip(g.trace, o.trace):
         assert t.flops == b["flops"] and t.update_order == b["update_order"]
+
+
+@pytest.mark.parametrize("dims,rank", [((40, 36, 32), 8), ((20, 18, 16, 14), 6),
+                                       ((512, 512, 512), 32), ((128, 128, 128, 128), 16)])
+def test_split_runs_keep_the_pipeline_and_the_results(dims, rank):
+    """A resumable session issues the next sweep's first update ahead of the
+    host sync even on the last sweep of a run() call.  run(a) + run(b) must be
+    bit-identical to run(a + b); end() after run(a) takes the work issued
+    ahead back and returns the state after a sweeps (a fresh a-sweep run's,
+    bit for bit), after which the session accepts no further run()."""
+    import paper_2503_18759_b200 as cpd
+    ctx = cpd.Context(0)
+    ctx.synth_tensor(0, list(dims), rank, 1e-3, 4711)  # (beta gate opens mid-run)
+
+    def go(parts, iters):
+        s = ctx.session(cfg_of(rank, iters, seed=11), extrapolate=True)
+        rows = []
+        for n in parts:
+            rows += s.run(n)
+        m = s.end()
+        return s, [(r.iteration, r.fitness, r.raw_radicand, r.flops, r.beta_used) for r in rows], m
+
+    s0, whole, m_whole = go([12], 12)
+    s0.close()
+    s1, split, m_split = go([1, 4, 2, 5], 12)
+    s1.close()
+    assert split == whole
+    assert np.array_equal(m_split.lam, m_whole.lam)
+    for a, b in zip(m_split.factors, m_whole.factors):
+        assert np.array_equal(a, b)
+    # end() in the middle of a longer session == a run that stops there
+    s2, part, m_part = go([7], 12)
+    s3, short, m_short = go([7], 7)
+    s3.close()
+    assert part == short == whole[:7]
+    assert np.array_equal(m_part.lam, m_short.lam)
+    for a, b in zip(m_part.factors, m_short.factors):
+        assert np.array_equal(a, b)
+    with pytest.raises(cpd.CpdLogicError):
+        s2.run(1)
+    s2.close()
+
+
+@pytest.mark.parametrize("dims,rank,variant,sweeps", [
+    ((70, 68, 66), 65, "bre", 8),
+    ((100, 96, 98), 96, "bre", 6),
+    ((140, 132, 136), 130, "dim-tree", 3),
+    ((132, 131, 130), 130, "naive", 2),
+    ((66, 65, 67, 65), 65, "bre", 3),
+])
+def test_wide_ranks_vs_oracle(ctx, port, dims, rank, variant, sweeps):
+    """Ranks above 64 (the reference accepts any rank up to the smallest
+    extent, solvers.hpp:221-224): the rank-generic tail (widerank.cu --
+    Khatri-Rao + cooperative Householder QR, row solves, exact normalisation)
+    behind the same session, against the oracle at the north-star bar."""
+    import paper_2503_18759_b200 as cpd
+    x = port.rng_normals(900 + rank, int(np.prod(dims))).reshape(dims)
+    if variant == "bre":
+        g = cpd.als_qr_bre(x, cfg_of(rank, sweeps, seed=5), ctx=ctx)
+        o = port.solve(x, rank, sweeps, extrapolate=True, seed=5)
+    else:
+        g = cpd.cp_als_qr(x, cfg_of(rank, sweeps, seed=5, strategy=variant), ctx=ctx)
+        o = port.solve(x, rank, sweeps, extrapolate=False, strategy=variant, seed=5)
+    compare(g, o)
