@@ -121,6 +121,8 @@ typedef struct {
     uint64_t kernel_launches; /* device kernels launched by the solve              */
     uint64_t qr_shifted;      /* sweeps in which a CholeskyQR first pass needed the
                                  shifted retry (kappa beyond ~1e8)                 */
+    uint64_t qr_householder;  /* solves restarted on the Householder kernels after
+                                 a CholeskyQR breakdown the retry could not cure   */
 } cpdb_profile;
 
 /* ---- version / device ----------------------------------------------------- */

@@ -81,6 +81,7 @@ class Profile(C.Structure):
         ("comm_ms", C.c_double),
         ("kernel_launches", C.c_uint64),
         ("qr_shifted", C.c_uint64),
+        ("qr_householder", C.c_uint64),
     ]
 
 

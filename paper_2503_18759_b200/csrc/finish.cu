@@ -194,7 +194,7 @@ bool finish_sums_splits(uint64_t I, uint32_t R) {
 }
 
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s) {
-    if (wide_rank(a.R)) return launch_finish_wide(a, s);
+    if (wide_rank(a.R) || a.householder) return launch_finish_wide(a, s);
     // the 8-CTA cluster kernel (cluster.cu) whenever its smem plan fits
     if (finish_cluster_smem(a.I, a.R) <= 220 * 1024) return launch_finish_cluster(a, s);
     return launch_finish_single(a, s);

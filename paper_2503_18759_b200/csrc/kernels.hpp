@@ -51,6 +51,7 @@ struct ZqrArgs {
     int* status;             // device flag: non-zero = Cholesky breakdown
     unsigned long long* ts;  // optional phase timestamps (profiling)
     int pdl;                 // launch programmatically after the previous kernel
+    int householder;         // rank-generic Householder kernels (widerank.cu) at any R
 };
 size_t zqr_work_doubles(uint32_t R);
 cudaError_t launch_zqr(const ZqrArgs& a, cudaStream_t s, int sms);
@@ -165,6 +166,7 @@ struct FinishArgs {
     double* fit_out;       // [fitness, raw]
     int* status;           // 1 singular R0 (+col<<8), 2 Cholesky breakdown
     unsigned long long* ts;  // optional phase timestamps (profiling)
+    int householder;         // rank-generic Householder kernels (widerank.cu) at any R
 };
 cudaError_t launch_finish(const FinishArgs& a, cudaStream_t s);
 // true when launch_finish(I, R) sums FinishArgs::nsplit V partials itself

@@ -51,6 +51,9 @@
 #include "session.hpp"
 
 namespace cpdb {
+
+static const char* const kBreakdownMessage =
+    "Cholesky QR breakdown: rank-deficient Khatri-Rao or factor matrix";
 namespace {
 
 // Stream/event calls of the session go through these so the happens-before
@@ -241,6 +244,10 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         fail(CPDB_INVALID_ARGUMENT, "cp_als_qr: ranks above 1024 are not supported on the device");
     R = static_cast<uint32_t>(cfg.rank);
     Rp = ttm_rpad(R);
+    {
+        const char* hh = std::getenv("CPDB_HOUSEHOLDER");
+        if (hh && hh[0] == '1') robust = true;
+    }
     extrap = cfg.extrapolate != 0;
     const Strategy strategy =
         extrap ? Strategy::branch_reuse : static_cast<Strategy>(cfg.strategy);
@@ -277,7 +284,11 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         maxI = std::max(maxI, d);
         nfac += d * R;
     }
-    c->prof = cpdb_profile{};
+    {
+        const uint64_t restarts = c->prof.qr_householder;
+        c->prof = cpdb_profile{};
+        if (robust) c->prof.qr_householder = restarts;  // (solve()'s second attempt)
+    }
     launches0 = c->launches;
     CPDB_CK(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
     CPDB_CK(cudaEventCreateWithFlags(&ev_zqr, cudaEventDisableTiming));
@@ -385,7 +396,7 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     }
     // (wide ranks: A_hat, the Householder working copy and its partials)
     for (DevBuf& b : fscratch)
-        b.ensure(wide_rank(R) ? finish_wide_scratch_doubles(maxI, R) : maxI * (R + 1));
+        b.ensure(wide_rank(R) || robust ? finish_wide_scratch_doubles(maxI, R) : maxI * (R + 1));
     vout.ensure(maxI * R);
     fitbuf.ensure(8);
     for (ZBuf& z : zb) {
@@ -406,6 +417,10 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     {
         const char* fe = std::getenv("CPDB_FAULT_SWEEP");
         fault_sweep = fe ? std::strtoull(fe, nullptr, 10) : 0;
+        // (CPDB_FAULT_ONCE=1: only on the CholeskyQR kernels, so the
+        // Householder restart of solve() goes through)
+        const char* fo = std::getenv("CPDB_FAULT_ONCE");
+        if (fo && fo[0] == '1' && robust) fault_sweep = 0;
     }
     for (uint32_t k = 0; k < order; ++k) qr_factor(k);
     for (uint32_t k = 0; k < order; ++k) pack_local(k);
@@ -596,6 +611,7 @@ void Session::qr_factor(uint32_t k) {
     f.r_out = fb[k].r.p;
     f.lambda = lam.p;
     f.scratch = fscratch[0].p;
+    f.householder = robust ? 1 : 0;
     f.status = status_word(done + 1);  // reported with the first sweep
     f.v_out = vout.p;
     CPDB_CK(launch_finish(f, s));
@@ -895,6 +911,7 @@ void Session::mode_update_front(uint64_t sweep, uint32_t b, cpdb_q0_observer obs
     z.r0 = zcur.r0.p;
     z.work = zcur.work.p;
     z.status = status_word(sweep);
+    z.householder = robust ? 1 : 0;
     // Z-QR depends only on R_k (k != n), final since the previous update's
     // finisher, and overlaps the TTM chain on a second stream.  Unsharded, the
     // Z-QR follows the finisher on the main stream (programmatic launch: its
@@ -1170,7 +1187,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
         const char* e = std::getenv("CPDB_VSPLIT_MAX");
         return e ? uint32_t(std::atoi(e)) : 16u;
     }();
-    v.max_split = (vsplit_max > 0 && !gather && !vsum && finish_sums_splits(v.I, R)) ? vsplit_max
+    v.max_split = (vsplit_max > 0 && !gather && !vsum && !robust && finish_sums_splits(v.I, R)) ? vsplit_max
                                                                                         : 0;
     const int vsms = bs == c->tailq && tail_sms > 0 ? tail_sms : budget(sweep, b);
     fp(bs, "vgemm", "in_before",
@@ -1193,7 +1210,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     // the cluster finisher sums the split-K partials itself (no reduction
     // launch on the chain); gathered (sharded mode-0) V needs them reduced
     const bool fused = vsplit_max > 0 && !v.reduced && !gather && !vsum && v.nsplit <= 64 &&
-                       finish_sums_splits(v.I, R);
+                       !robust && finish_sums_splits(v.I, R);
     if (!v.reduced && !fused) {
         tla = tl_begin(bs);
         CPDB_CK(reduce_splits(v.vpart, v.nsplit, v.I * R, vf.p + off, bs));
@@ -1241,6 +1258,7 @@ void Session::mode_update_back(uint64_t sweep, uint32_t b, double& beta_used, cu
     f.r_out = fb_alt[n].r.p;
     f.lambda = lam_alt.p;
     f.scratch = fscratch[zpar].p;
+    f.householder = robust ? 1 : 0;
     f.fitness = last ? 1 : 0;
     f.norm_x_sq = nx2;
     f.fit_out = fitbuf.p;
@@ -1445,8 +1463,7 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
                 fail(CPDB_SINGULAR_TRIANGULAR,
                      "triangular solve: diagonal entry of column " + std::to_string(status >> 8) +
                          " is ~0 (rank-deficient Khatri-Rao factor)");
-            fail(CPDB_SINGULAR_TRIANGULAR,
-                 "Cholesky QR breakdown: rank-deficient Khatri-Rao or factor matrix");
+            fail(CPDB_SINGULAR_TRIANGULAR, kBreakdownMessage);
         }
         static const bool dbg_guard = std::getenv("CPDB_GUARD") != nullptr;
         if (dbg_guard) dev_guard_check(("sweep " + std::to_string(sweep)).c_str());
@@ -1599,11 +1616,27 @@ void Session::end(cpdb_state* state, double* out_lambda, double* out_factors) {
 void solve(cpdb_ctx* c, const cpdb_config& cfg, cpdb_state* state, cpdb_trace_row* trace,
            uint64_t* trace_len, double* out_lambda, double* out_factors, double* fps,
            double* lps, cpdb_q0_observer observer, void* user) {
-    Session ss;
-    ss.begin(c, cfg, state);
-    const uint64_t n = ss.run(cfg.max_iterations, trace, fps, lps, observer, user);
-    if (trace_len) *trace_len = n;
-    ss.end(state, out_lambda, out_factors);
+    // CholeskyQR2 (with its shifted retry) breaks down beyond kappa ~1e15,
+    // where the reference's Householder QR carries on (linalg.hpp:39-99): such
+    // a run is started again on the Householder kernels (widerank.cu), which
+    // follow the reference's algorithm at any rank.  (Q0 observers have seen
+    // the first attempt's sweeps by then, so observed runs are not restarted.)
+    for (int attempt = 0;; ++attempt) {
+        Session ss;
+        ss.robust = attempt > 0;
+        try {
+            ss.begin(c, cfg, state);
+            const uint64_t n = ss.run(cfg.max_iterations, trace, fps, lps, observer, user);
+            if (trace_len) *trace_len = n;
+            ss.end(state, out_lambda, out_factors);
+            return;
+        } catch (const Fail& e) {
+            if (attempt > 0 || ss.robust || observer != nullptr ||
+                e.code != CPDB_SINGULAR_TRIANGULAR || e.what != kBreakdownMessage)
+                throw;
+            c->prof.qr_householder += 1;
+        }
+    }
 }
 
 }  // namespace cpdb

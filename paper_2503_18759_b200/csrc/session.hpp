@@ -153,6 +153,9 @@ struct Session {
         cudaEvent_t ev = nullptr;
     } pf;
     void launch_prefetch();
+    // CholeskyQR kernels replaced by the Householder ones (widerank.cu) at any
+    // rank: set by solve() when a run broke down, or CPDB_HOUSEHOLDER=1
+    bool robust = false;
     bool ended = false;          // end() took back work issued ahead: no further run()
     bool front1_issued = false;  // next sweep's second front issued ahead (Session::run)
     DevBuf pre;

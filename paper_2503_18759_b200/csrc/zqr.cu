@@ -526,12 +526,12 @@ cudaError_t run_multi(const ZqrArgs& a, cudaStream_t s, int sms) {
 }  // namespace
 
 size_t zqr_work_doubles(uint32_t R) {
-    if (wide_rank(R)) return zqr_wide_work_doubles(R);
-    return size_t(kPartOff + kMaxParts) * R * R;
+    return std::max(zqr_wide_work_doubles(R), wide_rank(R) ? size_t(0)
+                                                           : size_t(kPartOff + kMaxParts) * R * R);
 }
 
 cudaError_t launch_zqr(const ZqrArgs& a, cudaStream_t s, int sms) {
-    if (wide_rank(a.R)) return launch_zqr_wide(a, s);
+    if (wide_rank(a.R) || a.householder) return launch_zqr_wide(a, s);
     if (zqr_cluster_fits(a.zrows, a.R, a.nm)) return launch_zqr_cluster(a, s);
     return launch_zqr_multi(a, s, sms);
 }

@@ -531,3 +531,38 @@ def test_wide_ranks_vs_oracle(ctx, port, dims, rank, variant, sweeps):
         g = cpd.cp_als_qr(x, cfg_of(rank, sweeps, seed=5, strategy=variant), ctx=ctx)
         o = port.solve(x, rank, sweeps, extrapolate=False, strategy=variant, seed=5)
     compare(g, o)
+
+
+@pytest.mark.parametrize("dims,rank,variant", [((9, 8, 7), 3, "bre"), ((16, 24, 20), 5, "dim-tree"),
+                                               ((12, 10, 8, 16), 4, "bre"), ((40, 38, 36), 33, "bre"),
+                                               ((70, 66, 65), 64, "naive")])
+def test_householder_kernels_at_small_ranks(ctx, port, monkeypatch, dims, rank, variant):
+    """CPDB_HOUSEHOLDER=1 swaps the CholeskyQR kernels for the rank-generic
+    Householder ones (widerank.cu) at any rank: same trajectories."""
+    import paper_2503_18759_b200 as cpd
+    monkeypatch.setenv("CPDB_HOUSEHOLDER", "1")
+    x = port.rng_normals(61, int(np.prod(dims))).reshape(dims)
+    if variant == "bre":
+        g = cpd.als_qr_bre(x, cfg_of(rank, 10, seed=3), ctx=ctx)
+        o = port.solve(x, rank, 10, extrapolate=True, seed=3)
+    else:
+        g = cpd.cp_als_qr(x, cfg_of(rank, 10, seed=3, strategy=variant), ctx=ctx)
+        o = port.solve(x, rank, 10, extrapolate=False, strategy=variant, seed=3)
+    compare(g, o)
+
+
+def test_breakdown_restarts_on_householder(ctx, port, monkeypatch):
+    """A CholeskyQR breakdown that the shifted retry cannot cure does not end
+    the solve where the reference's Householder QR carries on
+    (linalg.hpp:39-99): cpdb_solve starts the run again on the Householder
+    kernels.  The test hook injects the breakdown into the CholeskyQR attempt
+    only; the restarted run matches the oracle."""
+    import paper_2503_18759_b200 as cpd
+    dims, rank = (40, 36, 32), 6
+    x = port.synth_baseline(0, dims, rank, 1e-2, 20250017)
+    o = port.solve(x, rank, 12, extrapolate=True, seed=5)
+    monkeypatch.setenv("CPDB_FAULT_SWEEP", "4")
+    monkeypatch.setenv("CPDB_FAULT_ONCE", "1")
+    g = cpd.als_qr_bre(x, cfg_of(rank, 12, seed=5), ctx=ctx)
+    assert ctx.profile()["qr_householder"] == 1
+    compare(g, o)
