@@ -63,6 +63,7 @@ struct Session {
         bool had_hist = false;  // has_hist[mode] before it (extrapolation possible)
         int prev_last_mode = -1;
         double beta_used = 0.0;  // its trace contribution, once the host knows the gate
+        bool reused = false;     // it took the previous update's Y_(n) / Q0 (no history swap)
     } spec;
     bool speculate = false;  // CPDB_SPECULATE=0 turns it off
     bool self_hist = true;   // CPDB_SELF_HIST=0: always wait for the history's own Z-QR
@@ -89,7 +90,22 @@ struct Session {
         // it reads changed since that update's Z-QR, so its Q0 -- this
         // mode's extrapolation history -- equals this Z-QR's Q0 bit for bit
         bool hist_is_self = false;
+        // this update takes the previous update's Y_(n), Q0 and R0 (the
+        // other parity's buffers): the sweep boundary repeats the mode with
+        // unchanged inputs, see mode_update_front
+        bool reuse = false;
     } zb[2];
+    // What the last front computed, to recognise a repetition: mode, the
+    // single chain step that produced Y_(n) straight from a cached source
+    // (key, contracted mode, the source's buffer and stamps) and the factor
+    // versions its Z-QR and chain read
+    struct LastFront {
+        bool valid = false;
+        uint32_t mode = 0, source = 0, contract = 0;
+        const double* src_buf = nullptr;
+        std::vector<uint64_t> src_stamps, versions;
+    } prev_front;
+    bool reuse_ok = true;  // CPDB_REUSE_BOUNDARY=0: recompute (A/B testing)
     int zpar = 0;  // parity of the update in flight (set by the front, used by the back)
     // Dependency events of the event-driven schedule (dep_events): the
     // finisher that last updated each mode, the V-GEMM that last read ybuf[n],
@@ -97,6 +113,9 @@ struct Session {
     bool dep_events = false;
     // ev_v[2n + parity]: the V-GEMM that last read ybuf[2n + parity]
     cudaEvent_t ev_fac[CPDB_MAX_ORDER] = {}, ev_v[2 * CPDB_MAX_ORDER] = {}, ev_zread[2] = {};
+    // second readers of the same buffers: an update that repeats the previous
+    // one reads its Y_(n) / Q0 / R0 from another stream (zb[].reuse)
+    cudaEvent_t ev_v_b[2 * CPDB_MAX_ORDER] = {}, ev_zread_b[2] = {};
     std::map<uint32_t, cudaEvent_t> slot_ready;  // cache slot -> its producer done
     // ev_hist[n]: the Z-QR that produced hist[n] (the Q0 history of mode n);
     // ev_zq_pending: this update's Z-QR, swapped into ev_hist[n] by its back

@@ -566,3 +566,42 @@ def test_breakdown_restarts_on_householder(ctx, port, monkeypatch):
     g = cpd.als_qr_bre(x, cfg_of(rank, 12, seed=5), ctx=ctx)
     assert ctx.profile()["qr_householder"] == 1
     compare(g, o)
+
+
+@pytest.mark.parametrize("dims,rank,extrap", [((40, 36, 32), 8, True), ((40, 36, 32), 8, False),
+                                              ((20, 18, 16, 14), 6, True),
+                                              ((256, 256, 256), 20, True),
+                                              ((64, 64, 64, 64), 16, True)])
+def test_boundary_repetition_elided_bit_identical(monkeypatch, dims, rank, extrap):
+    """The permuted update orders end one sweep and begin the next with the
+    same mode, whose Z-QR and TTM chain inputs have not changed in between:
+    the session takes the previous update's Y_(n) / Q0 / R0 instead of
+    launching the kernels again (mode_update_front).  Same bits as
+    recomputing (CPDB_REUSE_BOUNDARY=0), same integer cost report, also when
+    the stop test undoes a speculative update that reused."""
+    import paper_2503_18759_b200 as cpd
+    ctx = cpd.Context(0)
+    ctx.synth_tensor(0, list(dims), rank, 1e-2, 99)
+
+    def go(reuse, iters, thr=1.0):
+        monkeypatch.setenv("CPDB_REUSE_BOUNDARY", reuse)
+        cfg = cfg_of(rank, iters, seed=3, fitness_threshold=thr)
+        ctx.profile()
+        r = ctx.solve(cfg, extrapolate=extrap)
+        return r, ctx.profile()["kernel_launches"]
+
+    (a, la), (b, lb) = go("1", 14), go("0", 14)
+    assert la < lb  # launches were elided
+    assert [(t.fitness, t.raw_radicand, t.flops, t.root_ttm_count, t.beta_used) for t in a.trace] == \
+           [(t.fitness, t.raw_radicand, t.flops, t.root_ttm_count, t.beta_used) for t in b.trace]
+    for fa, fb in zip(a.model.factors, b.model.factors):
+        assert np.array_equal(fa, fb)
+    assert np.array_equal(a.model.lam, b.model.lam)
+    # early stop in the middle: the undone speculative update had reused
+    f = [t.fitness for t in a.trace]
+    k = max(i for i in range(3, 12) if f[i] > f[i - 1])
+    thr = 0.5 * (f[k - 1] + f[k])
+    (c, _), (d, _) = go("1", 14, thr), go("0", 14, thr)
+    assert len(c.trace) == len(d.trace) == k + 1
+    for fa, fb in zip(c.model.factors, d.model.factors):
+        assert np.array_equal(fa, fb)
