@@ -53,7 +53,8 @@ __global__ void __launch_bounds__(kKT) krc_rfast_kernel(KrcArgs a, const double*
                                                         double* __restrict__ out) {
     constexpr int G = kKT / RP;
     __shared__ double red[G][kTN][RP];
-    const int r = threadIdx.x % RP, g = threadIdx.x / RP;
+    const int rl = threadIdx.x % RP, g = threadIdx.x / RP;
+    const int r = int(blockIdx.z) * RP + rl;  // column block (ranks wider than RP)
     const uint32_t R = a.R;
     const uint64_t In = a.In, Q = a.Q, PQ = a.P * a.Q;
     const uint64_t i0 = uint64_t(blockIdx.x) * kTN;
@@ -81,13 +82,13 @@ __global__ void __launch_bounds__(kKT) krc_rfast_kernel(KrcArgs a, const double*
         }
     }
 #pragma unroll
-    for (int t = 0; t < kTN; ++t) red[g][t][r] = acc[t];
+    for (int t = 0; t < kTN; ++t) red[g][t][rl] = acc[t];
     __syncthreads();
     for (int e = threadIdx.x; e < kTN * RP; e += kKT) {
-        const int t = e / RP, rr = e % RP;
+        const int t = e / RP, rr = e % RP, rc = int(blockIdx.z) * RP + rr;
         double s = 0.0;
         for (int gg = 0; gg < G; ++gg) s += red[gg][t][rr];
-        if (rr < int(R) && i0 + t < In) out[(uint64_t(blockIdx.y) * In + i0 + t) * R + rr] = s;
+        if (rc < int(R) && i0 + t < In) out[(uint64_t(blockIdx.y) * In + i0 + t) * R + rc] = s;
     }
 }
 
@@ -283,7 +284,6 @@ cudaError_t launch_kr_table(const KrcArgs& a, double* w, cudaStream_t s) {
 
 cudaError_t launch_krc(const KrcArgs& a, const double* w, double* out, uint64_t split,
                        cudaStream_t s) {
-    if (a.R > 64) return cudaErrorInvalidValue;
     if (a.router) {
         const int ti = pow2_at_least(a.In, 32, 256);
         const dim3 grid(unsigned(uint64_t(a.R) * ((a.In + ti - 1) / ti)), unsigned(split));
@@ -296,7 +296,7 @@ cudaError_t launch_krc(const KrcArgs& a, const double* w, double* out, uint64_t 
         return cudaGetLastError();
     }
     const int rp = pow2_at_least(a.R, 8, 64);
-    const dim3 grid(unsigned((a.In + kTN - 1) / kTN), unsigned(split));
+    const dim3 grid(unsigned((a.In + kTN - 1) / kTN), unsigned(split), unsigned((a.R + rp - 1) / rp));
     switch (rp) {
         case 8: krc_rfast_kernel<8><<<grid, kKT, 0, s>>>(a, w, out); break;
         case 16: krc_rfast_kernel<16><<<grid, kKT, 0, s>>>(a, w, out); break;
@@ -306,10 +306,12 @@ cudaError_t launch_krc(const KrcArgs& a, const double* w, double* out, uint64_t 
     return cudaGetLastError();
 }
 
+size_t spd_work_doubles(uint32_t n) { return (n > 64 ? 2 : 1) * size_t(n) * n; }
+
 cudaError_t launch_spd_solve(const double* g, uint32_t n, double* u_work, double* x, uint64_t rows,
                              int* status, int* reg, cudaStream_t s, int sms) {
     const uint32_t rm = n <= 8 ? 8 : n <= 16 ? 16 : n <= 32 ? 32 : 64;
-    if (n > 64) return cudaErrorInvalidValue;
+    if (n > 64) return launch_spd_solve_wide(g, n, u_work, x, rows, status, reg, s);
     const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>(rows / 16 + 1,
                                                                             uint64_t(2 * sms))));
 #define CPDB_SPD(RM_)                                                                    \

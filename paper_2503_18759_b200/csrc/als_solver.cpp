@@ -102,8 +102,8 @@ void als_solve(cpdb_ctx* c, const cpdb_config& cfg, const double* init_lambda,
     if (N < 2) fail(CPDB_INVALID_ARGUMENT, "cp_als: tensor order must be >= 2");
     const double nx2 = ctx_norm_sq(c);
     if (nx2 == 0.0) fail(CPDB_INVALID_ARGUMENT, "cp_als: zero-norm tensor");
-    if (cfg.rank > 64)
-        fail(CPDB_INVALID_ARGUMENT, "cp_als: ranks above 64 are not supported on the device");
+    if (cfg.rank > 1024)
+        fail(CPDB_INVALID_ARGUMENT, "cp_als: ranks above 1024 are not supported on the device");
     const uint32_t R = uint32_t(cfg.rank);
     cudaStream_t s = c->stream;
     const bool sharded = c->world > 1;
@@ -209,8 +209,8 @@ void als_solve(cpdb_ctx* c, const cpdb_config& cfg, const double* init_lambda,
                 CPDB_CK(hadamard_dev(gl, R, gp, s));
                 CPDB_CK(cudaMemcpyAsync(ah, M.p, I * R * sizeof(double), cudaMemcpyDeviceToDevice,
                                         s));
-                int* dreg_n = reinterpret_cast<int*>(uwork.ensure(uint64_t(R) * R + 2)) +
-                              2 * uint64_t(R) * R;
+                const size_t uw = spd_work_doubles(R);
+                int* dreg_n = reinterpret_cast<int*>(uwork.ensure(uw + 2)) + 2 * uw;
                 CPDB_CK(launch_spd_solve(gp, R, uwork.p, ah, I, c->dstatus, dreg_n, s, c->sms));
                 CPDB_CK(cudaMemcpyAsync(A[n].p, ah, I * R * sizeof(double),
                                         cudaMemcpyDeviceToDevice, s));

@@ -745,7 +745,7 @@ int cpdb_mttkrp(cpdb_ctx* c, const double* t, const uint64_t* dims, uint32_t ord
                 fail(CPDB_INVALID_ARGUMENT, "mttkrp: factor rows do not match mode extent");
         }
         if (rank == 0) fail(CPDB_INVALID_ARGUMENT, "mttkrp: order must be >= 2");
-        if (rank > 64) fail(CPDB_INVALID_ARGUMENT, "mttkrp: ranks above 64 are not supported");
+        if (rank > 1024) fail(CPDB_INVALID_ARGUMENT, "mttkrp: ranks above 1024 are not supported");
         const uint32_t R = uint32_t(rank);
         const uint64_t nx = cpdb::numel(d);
         uint64_t nf = 0;
@@ -777,13 +777,15 @@ int cpdb_solve_spd(cpdb_ctx* c, const double* g, uint64_t g_rows, uint64_t g_col
         if (g_cols != g_rows) fail(CPDB_INVALID_ARGUMENT, "solve_spd: G must be square");
         if (cols != g_rows) fail(CPDB_INVALID_ARGUMENT, "solve_spd: RHS columns must match G");
         if (g_rows == 0) fail(CPDB_INVALID_ARGUMENT, "Matrix: zero dimension");
-        if (g_rows > 64) fail(CPDB_INVALID_ARGUMENT, "solve_spd: n above 64 is not supported");
+        if (g_rows > 1024)
+            fail(CPDB_INVALID_ARGUMENT, "solve_spd: n above 1024 is not supported");
         const uint32_t n = uint32_t(g_rows);
-        double* dg = c->scratch_a.ensure(2 * uint64_t(n) * n + 8);
+        const uint64_t uw = cpdb::spd_work_doubles(n);
+        double* dg = c->scratch_a.ensure(uint64_t(n) * n + uw + 8);
         double* dx = c->scratch_b.ensure(std::max<uint64_t>(rows * n, 1));
         upload(c, dg, g, uint64_t(n) * n);
         if (rows) upload(c, dx, rhs, rows * n);
-        int* flags = reinterpret_cast<int*>(dg + 2 * uint64_t(n) * n);
+        int* flags = reinterpret_cast<int*>(dg + uint64_t(n) * n + uw);
         CPDB_CK(cudaMemsetAsync(flags, 0, 2 * sizeof(int), c->stream));
         CPDB_CK(cpdb::launch_spd_solve(dg, n, dg + uint64_t(n) * n, dx, rows, flags, flags + 1,
                                        c->stream, c->sms));

@@ -106,8 +106,10 @@ uint64_t krc_split(const KrcArgs& a, int sms);
 // out: split x In x R partials (split == 1: M itself)
 cudaError_t launch_krc(const KrcArgs& a, const double* w, double* out, uint64_t split,
                        cudaStream_t s);
+// u_work: spd_work_doubles(n) doubles (n^2 up to n = 64, 2 n^2 beyond)
 cudaError_t launch_spd_solve(const double* g, uint32_t n, double* u_work, double* x, uint64_t rows,
                              int* status, int* reg, cudaStream_t s, int sms);
+size_t spd_work_doubles(uint32_t n);
 struct GramList {
     const double* g[8];
     uint32_t n;
@@ -201,6 +203,9 @@ size_t zqr_wide_work_doubles(uint32_t R);
 size_t finish_wide_scratch_doubles(uint64_t I, uint32_t R);
 cudaError_t launch_zqr_wide(const ZqrArgs& a, cudaStream_t s);
 cudaError_t launch_finish_wide(const FinishArgs& a, cudaStream_t s);
+// solve_spd for n > 64 (launch_spd_solve dispatches here); u_work: 2 n^2 doubles
+cudaError_t launch_spd_solve_wide(const double* g, uint32_t n, double* u_work, double* x,
+                                  uint64_t rows, int* status, int* reg, cudaStream_t s);
 // thin_qr (linalg.hpp:39-99) on the cooperative kernel; work = m*n +
 // zqr_wide_work_doubles(n)
 cudaError_t householder_qr_wide(const double* a, uint64_t m, uint32_t n, double* work, double* q,

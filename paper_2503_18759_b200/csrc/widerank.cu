@@ -24,6 +24,7 @@
 #include "device.cuh"
 #include "kernels.hpp"
 #include "prims.hpp"
+#include "rowalg.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -285,6 +286,109 @@ __global__ void fit_copy_kernel(const double* out4, double* fit_out) {
     fit_out[1] = out4[3];
 }
 
+
+// ---------------------------------------------------------------- solve_spd, n > 64
+// linalg.hpp:132-185 with the factor in global memory: symmetry check,
+// Cholesky G = U^T U (right-looking, one CTA), one ridge retry with delta =
+// 1e-12 trace / n, then X = RHS U^-1 U^-T row by row.  u: n x n (U), ut: n x n
+// (U^T, so both substitutions read contiguous rows).
+__global__ void __launch_bounds__(512)
+spd_factor_wide_kernel(const double* g, uint32_t n, double* u, double* ut, int* status, int* reg) {
+    __shared__ double red[32];
+    __shared__ int fail;
+    double mabs = 0.0, masym = 0.0;
+    for (uint32_t e = threadIdx.x; e < n * n; e += 512) {
+        const uint32_t i = e / n, j = e % n;
+        mabs = fmax(mabs, fabs(g[e]));
+        masym = fmax(masym, fabs(g[e] - g[j * n + i]));
+    }
+    mabs = block_max<512>(mabs, red);
+    masym = block_max<512>(masym, red);
+    if (masym > 1e-10 * mabs) {
+        if (threadIdx.x == 0) *status = 5;
+        return;
+    }
+    int used = 0;
+    bool ok = false;
+    for (int attempt = 0; attempt < 2 && !ok; ++attempt) {
+        double delta = 0.0;
+        if (attempt == 1) {
+            double tr = 0.0;
+            for (uint32_t i = 0; i < n; ++i) tr += g[i * n + i];
+            delta = 1e-12 * tr / double(n);
+            used = 1;
+        }
+        for (uint32_t e = threadIdx.x; e < n * n; e += 512)
+            u[e] = g[e] + ((e / n == e % n) ? delta : 0.0);
+        if (threadIdx.x == 0) fail = 0;
+        __syncthreads();
+        ok = true;
+        for (uint32_t j = 0; j < n; ++j) {
+            const double d = u[j * n + j];
+            if (!(d > 0.0)) {  // uniform: every thread read the same d
+                ok = false;
+                break;
+            }
+            const double root = sqrt(d);
+            __syncthreads();
+            for (uint32_t b = j + threadIdx.x; b < n; b += 512)
+                u[j * n + b] = b == j ? root : u[j * n + b] / root;
+            __syncthreads();
+            const uint32_t t = n - j - 1;  // trailing block (a, b > j, a <= b)
+            for (uint32_t e = threadIdx.x; e < t * t; e += 512) {
+                const uint32_t a = j + 1 + e / t, b = j + 1 + e % t;
+                if (a <= b) u[a * n + b] = fma(-u[j * n + a], u[j * n + b], u[a * n + b]);
+            }
+            __syncthreads();
+        }
+        __syncthreads();
+    }
+    for (uint32_t e = threadIdx.x; e < n * n; e += 512) {
+        const uint32_t i = e / n, j = e % n;
+        const double v = j >= i ? u[e] : 0.0;
+        ut[j * n + i] = v;
+    }
+    __syncthreads();
+    for (uint32_t e = threadIdx.x; e < n * n; e += 512)
+        if (e % n < e / n) u[e] = 0.0;
+    if (threadIdx.x == 0) {
+        *status = ok ? 0 : 4;
+        *reg = used;
+    }
+}
+
+__global__ void __launch_bounds__(kHT)
+spd_rows_wide_kernel(const double* u, const double* ut, uint32_t n, double* x, uint64_t rows,
+                     const int* status) {
+    extern __shared__ double sm[];
+    if (*status) return;
+    const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double* xr = sm + size_t(g) * n;
+    for (uint64_t row = uint64_t(blockIdx.x) * kHW + g; row < rows; row += uint64_t(gridDim.x) * kHW) {
+        for (uint32_t j = lane; j < n; j += 32) xr[j] = x[row * n + j];
+        __syncwarp();
+        // w U = rhs  (w L^T = rhs, L = U^T): forward, column c of U = row c of U^T
+        for (uint32_t c = 0; c < n; ++c) {
+            double s = 0.0;
+            for (uint32_t j = lane; j < c; j += 32) s = fma(xr[j], ut[size_t(c) * n + j], s);
+            s = warp_sum(s);
+            if (lane == 0) xr[c] = (xr[c] - s) / ut[size_t(c) * n + c];
+            __syncwarp();
+        }
+        // x U^T = w  (x L = w): backward, L[j][c] = U[c][j]
+        for (int c = int(n) - 1; c >= 0; --c) {
+            double s = 0.0;
+            for (uint32_t j = uint32_t(c) + 1 + lane; j < n; j += 32)
+                s = fma(xr[j], u[size_t(c) * n + j], s);
+            s = warp_sum(s);
+            if (lane == 0) xr[c] = (xr[c] - s) / u[size_t(c) * n + c];
+            __syncwarp();
+        }
+        for (uint32_t j = lane; j < n; j += 32) x[row * n + j] = xr[j];
+        __syncwarp();
+    }
+}
+
 }  // namespace
 
 bool wide_rank(uint32_t R) { return R > 64; }
@@ -350,6 +454,23 @@ cudaError_t householder_qr_wide(const double* a, uint64_t m, uint32_t n, double*
     if (e != cudaSuccess) return e;
     HhArgs h{work, q, r, work + m * n, m, n};
     return hh_launch(h, s);
+}
+
+
+// u_work: 2 n^2 doubles (U and U^T)
+cudaError_t launch_spd_solve_wide(const double* g, uint32_t n, double* u_work, double* x,
+                                  uint64_t rows, int* status, int* reg, cudaStream_t s) {
+    if (n > uint32_t(kMaxWide)) return cudaErrorInvalidValue;
+    double* u = u_work;
+    double* ut = u_work + size_t(n) * n;
+    spd_factor_wide_kernel<<<1, 512, 0, s>>>(g, n, u, ut, status, reg);
+    const size_t smem = size_t(kHW) * n * sizeof(double);
+    cudaError_t e = cudaFuncSetAttribute(spd_rows_wide_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+    if (e != cudaSuccess) return e;
+    const unsigned grid = unsigned(std::max<uint64_t>(1, std::min<uint64_t>((rows + kHW - 1) / kHW, 1024)));
+    spd_rows_wide_kernel<<<grid, kHT, smem, s>>>(u, ut, n, x, rows, status);
+    return cudaGetLastError();
 }
 
 }  // namespace cpdb

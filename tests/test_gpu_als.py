@@ -35,7 +35,7 @@ def compare(g, o, fit_tol=FIT_TOL, factor_tol=1e-10):
 
 # ---------------------------------------------------------------- MTTKRP
 @pytest.mark.parametrize("dims", [(9, 8, 7), (7, 6, 5, 4), (5, 11), (3, 4, 2, 3, 2), (100, 30, 64)])
-@pytest.mark.parametrize("rank", [1, 3, 10, 32, 64])
+@pytest.mark.parametrize("rank", [1, 3, 10, 32, 64, 65, 130])
 def test_mttkrp_every_mode(ctx, ref, dims, rank):
     import paper_2503_18759_b200 as cpd
     rng = np.random.default_rng(sum(dims) * 7 + rank)
@@ -84,7 +84,8 @@ def test_solve_spd_reference_cases(ctx):
         cpd.solve_spd(np.ones((2, 3)), np.zeros((1, 3)), ctx=ctx)
 
 
-@pytest.mark.parametrize("n,rows", [(1, 5), (5, 7), (16, 300), (20, 33), (32, 1000), (64, 129)])
+@pytest.mark.parametrize("n,rows", [(1, 5), (5, 7), (16, 300), (20, 33), (32, 1000), (64, 129),
+                                    (65, 40), (100, 333), (200, 77)])
 def test_solve_spd_vs_oracle(ctx, ref, n, rows):
     import paper_2503_18759_b200 as cpd
     rng = np.random.default_rng(n * 131 + rows)
@@ -191,8 +192,22 @@ def test_cp_als_rejections(ctx):
         cpd.cp_als(np.zeros((3, 3)), als_cfg(2, 5), ctx=ctx)
     with pytest.raises(cpd.CpdInvalidArgument, match="algorithm must be als"):
         cpd.cp_als(np.ones((3, 3)), cpd.SolverConfig(rank=2, max_iterations=5), ctx=ctx)
-    with pytest.raises(cpd.CpdInvalidArgument, match="ranks above 64"):
-        cpd.cp_als(np.ones((70, 70)), als_cfg(65, 1), ctx=ctx)
+    with pytest.raises(cpd.CpdInvalidArgument, match="ranks above 1024"):
+        cpd.cp_als(np.ones((70, 70)), als_cfg(1025, 1), ctx=ctx)
+
+
+@pytest.mark.parametrize("dims,rank", [((70, 72, 68), 65), ((40, 30, 20), 80), ((30, 20, 16, 12), 70),
+                                       ((150, 140), 130)])
+def test_cp_als_wide_ranks(ctx, ref, dims, rank):
+    """Ranks above 64 (cp_als has no rank <= extent requirement,
+    solvers.hpp:149-156): column blocks of the Khatri-Rao contraction and the
+    global-memory solve_spd (widerank.cu)."""
+    import paper_2503_18759_b200 as cpd
+    x = np.random.default_rng(rank).standard_normal(dims)
+    g = cpd.cp_als(x, als_cfg(rank, 6, seed=4), ctx=ctx)
+    o = ref.cp_als(x, rank, 6, seed=4)
+    assert [t.regularized for t in g.trace] == [t["regularized"] for t in o.trace]
+    compare(g, o)
 
 
 def test_cp_als_deterministic(ctx, ref):
