@@ -812,11 +812,12 @@ void Session::prefetch_root(uint64_t sweep, uint32_t b, cudaStream_t after) {
             for (uint32_t bm = b + 1; bm < b2; ++bm)
                 for (const Step& st : sw.updates[bm].steps) upd += step_flops(st);
             const double per_sm = 0.15e12;  // FP64 FLOP/s per SM on a small grid
-            // finish in ~0.38 of the root's time (measured: 0.5 C2 2235
-            // sweeps/s, 0.38 2264, 0.3 2192; C3 flat)
+            // finish in ~0.5 of the root's time (measured on the final
+            // schedule, C2: 0.3 2474, 0.38 2482, 0.5 2507, 0.75 2507, 1.0 2514
+            // sweeps/s; C3 flat)
             static const double frac = [] {
                 const char* e = std::getenv("CPDB_OVERLAP_FRAC");
-                return e ? std::atof(e) : 0.38;
+                return e ? std::atof(e) : 0.5;
             }();
             const int need = int(std::ceil(upd / (frac * root_s * per_sm)));
             if (root_s >= 150e-6 && need < c->sms / 2) pf.sms = std::max(need, 16);
@@ -1527,7 +1528,11 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
                         // (fourth order) -2%, so third order only;
                         // CPDB_ZQR_AUX=0/1 overrides)
                         static const char* zae = std::getenv("CPDB_ZQR_AUX");
-                        const bool zaux = zae ? zae[0] == '1' : order == 3;
+                        // (long roots, C2: with the boundary repetition elided
+                        // the main stream is free at this point and the Z-QR is
+                        // better off there -- 2507 -> 2523 sweeps/s; C4 loses 2%
+                        // without it)
+                        const bool zaux = zae ? zae[0] == '1' : order == 3 && !long_root;
                         if (zaux) zqr_stream_override = ss;
                         mode_update_front(sweep + 1, 1, nullptr, nullptr);
                         zqr_stream_override = nullptr;
