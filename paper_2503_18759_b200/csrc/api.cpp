@@ -554,10 +554,8 @@ int cpdb_ttm(cpdb_ctx* c, const double* t, const uint64_t* dims, uint32_t order,
         CPDB_CK(cpdb::transpose_dev(db, b_rows, K, dq, c->stream));
         double* qp = nullptr;
         cpdb::DevBuf packed;
-        if (b_rows <= 64) {
-            qp = packed.ensure(uint64_t(cpdb::ttm_kpad(K)) * cpdb::ttm_rpad(uint32_t(b_rows)));
-            CPDB_CK(cpdb::pack_q(dq, qp, uint32_t(K), uint32_t(b_rows), c->stream));
-        }
+        qp = packed.ensure(uint64_t(cpdb::ttm_kpad(K)) * cpdb::ttm_rpad(uint32_t(b_rows)));
+        CPDB_CK(cpdb::pack_q(dq, qp, uint32_t(K), uint32_t(b_rows), c->stream));
         cpdb::run_ttm(c, dx, d, mode, dq, qp, uint32_t(b_rows), dy);
         download(c, out, dy, nout);
     });
@@ -1054,10 +1052,8 @@ int cpdb_exec_step(cpdb_ctx* c, uint32_t source, uint32_t contract, uint32_t pro
         upload(c, dq, q, K * rank);
         cpdb::DevBuf packed;
         double* qp = nullptr;
-        if (rank <= 64) {
-            qp = packed.ensure(uint64_t(cpdb::ttm_kpad(K)) * cpdb::ttm_rpad(uint32_t(rank)));
-            CPDB_CK(cpdb::pack_q(dq, qp, uint32_t(K), uint32_t(rank), c->stream));
-        }
+        qp = packed.ensure(uint64_t(cpdb::ttm_kpad(K)) * cpdb::ttm_rpad(uint32_t(rank)));
+        CPDB_CK(cpdb::pack_q(dq, qp, uint32_t(K), uint32_t(rank), c->stream));
         cpdb::Slot& sl = c->slots[produces];
         double* dst = sl.buf.ensure(cpdb::numel(od));
         cpdb::run_ttm(c, src, sd, contract, dq, qp, uint32_t(rank), dst);

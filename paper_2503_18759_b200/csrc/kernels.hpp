@@ -14,6 +14,7 @@ struct TtmArgs {
     const double* qp;  // Q packed by pack_q -- tensor-core paths
     uint64_t outer, K, inner;
     uint32_t R, Rp;
+    uint32_t Rtot;     // 0, or Y's extent when this launch writes a column block of it
     uint32_t tiles_per_cta;  // non-persistent form: tiles per CTA (0: CPDB_PREFETCH_TPC or 2)
     int one_tile_per_cta;  // non-persistent grid (a low-priority launch that
                            // yields SMs to concurrent work as its CTAs retire)
@@ -29,6 +30,9 @@ cudaError_t launch_ttm_tma(const TtmArgs& a, cudaStream_t s, int sms);
 uint32_t ttm_kpad(uint64_t K);
 uint32_t ttm_rpad(uint32_t R);
 cudaError_t pack_q(const double* q, double* qp, uint32_t K, uint32_t R, cudaStream_t s);
+// columns [c0, c0 + Rc) (Rc <= 64) of a K x ld row-major matrix, packed as a K x Rc Q
+cudaError_t pack_q_cols(const double* q, uint32_t ld, uint32_t c0, uint32_t Rc, double* qp,
+                        uint32_t K, cudaStream_t s);
 
 // ---------------------------------------------------------------- K6 norms
 constexpr int kNormBlocks = 1184;  // fixed (8 x 148): deterministic partition

@@ -350,6 +350,12 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         // sweep); C3 -2% (fourth order, small Z: the repeated chain ran early
         // beside the previous update for free), so fourth order only with a
         // tall Z.  CPDB_REUSE_BOUNDARY=0/1 overrides.
+        // slabs of a reduced TTM step whose collectives overlap the next
+        // slab's kernel (ttm_step); steps below ~0.2 GFLOP are launch-bound
+        const char* rc = std::getenv("CPDB_RS_CHUNKS");
+        rs_chunks = rc ? uint32_t(std::max(1, std::atoi(rc))) : 4u;
+        const char* rf = std::getenv("CPDB_RS_MIN_FLOPS");
+        rs_min_flops = rf ? std::atof(rf) : 2e8;
         const char* rb = std::getenv("CPDB_REUSE_BOUNDARY");
         reuse_ok = rb ? rb[0] != '0' : (order == 3 || !zqr_cluster_fits(zrows, R, order - 1));
         const char* sp = std::getenv("CPDB_SPECULATE");
@@ -706,57 +712,109 @@ void Session::ttm_step(const double* src, const std::vector<uint64_t>& sd, const
     // a reduce-scatter needs the whole partial first
     double* raw = dst;
     if (sh && sh->red == kRedScatter) raw = rs_tmp[st].ensure(numel(sd) / sd[k] * R);
-    Timer t;
-    if (c->timing) {
-        t.a = events.get();
-        t.b = events.get();
-        t.kind = is_root ? 0 : 1;
-        CPDB_CK(cudaEventRecord(t.a, st));
+    std::vector<uint64_t> od = sd;
+    od[k] = R;
+    // Reduced steps run in slabs of the outermost mode: the collective of slab
+    // p (main stream) overlaps the TTM of slab p + 1 (producing stream), so
+    // only the last slab's reduction is exposed.  Slabs are whole outer
+    // slices of both the source and the result (k != 0), and for a
+    // reduce-scatter the scattered mode lies inside them (scatter != 0), so
+    // each slab's collective is the same call on a sub-range.  Every output
+    // element is accumulated in the same order as in one launch.
+    // CPDB_RS_CHUNKS=<n> (default 4; 1: one launch, one collective).
+    const uint32_t want_chunks = rs_chunks;
+    const double min_flops = rs_min_flops;
+    uint32_t chunks = 1;
+    // contracting the leading mode (the split one): the result is [R][rest],
+    // so the slabs are column halves of Q (rows of the result) -- two 32-column
+    // TTMs stay tensor-bound (C2's root shape), narrower ones would not
+    const bool by_cols = k == 0;
+    const bool big = sh && sh->red != kRedNone &&
+                     2.0 * double(numel(od)) * double(sd[k]) >= min_flops;
+    // (tensor-core TTM layouts only: the plain kernel reads the unpacked Q)
+    if (big && by_cols && want_chunks > 1 && R % 2 == 0 && R / 2 >= 32 && R <= 64 &&
+        (numel(sd) / sd[0]) % 8 == 0) {
+        chunks = 2;
+    } else if (big && !by_cols && !(sh->red == kRedScatter && sh->scatter == 0)) {
+        for (uint32_t cnum = want_chunks; cnum > 1; --cnum)
+            if (sd[0] % cnum == 0) {
+                chunks = cnum;
+                break;
+            }
     }
-    cudaEvent_t tla = tl_begin(st);
-    fp(st, prefetch ? "root_prefetch" : is_root ? "root_ttm" : "branch_ttm", "in_before",
-       {rg(src, numel(sd)), rg(qp, uint64_t(ttm_kpad(sd[k])) * Rp)});
-    run_ttm(c, src, sd, k, q, qp, R, raw, st, prefetch || yield_now, no_pdl, sms,
-            prefetch ? pf.tpc : 0);
-    acc(st, prefetch ? "root_prefetch" : is_root ? "root_ttm" : "branch_ttm",
-          {rg(src, numel(sd)), rg(qp, uint64_t(ttm_kpad(sd[k])) * Rp)},
-          {rg(raw, numel(sd) / sd[k] * R)});
-    tl_end(tla, st, prefetch ? "root_prefetch" : is_root ? "root" : "branch");
-    if (c->timing) {
-        CPDB_CK(cudaEventRecord(t.b, st));
-        const uint64_t nin = numel(sd);
-        const uint64_t nout = nin / sd[k] * R;
-        t.flops = 2.0 * double(nout) * double(sd[k]);
-        t.bytes = 8.0 * (double(nin) + double(nout) + double(sd[k]) * R);
-        timers.push_back(t);
-    }
-    if (sh && sh->red != kRedNone) {
-        // the collective runs on the main stream, after this step's kernel
+    const bool cols = by_cols && chunks > 1;
+    const uint32_t Rc = cols ? R / chunks : R;
+    const uint64_t in_slab = cols ? numel(sd) : numel(sd) / chunks;
+    const uint64_t out_slab = numel(od) / chunks;
+    std::vector<uint64_t> sdp = sd, odp = od;
+    if (!cols) sdp[0] /= chunks;
+    odp[0] /= chunks;
+    double* qcols = cols ? qcol_tmp[st].ensure(uint64_t(chunks) * ttm_kpad(sd[k]) * ttm_rpad(Rc))
+                         : nullptr;
+    Timer tc;
+    bool comm_timed = false;
+    for (uint32_t p = 0; p < chunks; ++p) {
+        const double* srcp = cols ? src : src + uint64_t(p) * in_slab;
+        double* rawp = raw + uint64_t(p) * out_slab;
+        const double* qpp = qp;
+        if (cols) {  // this half's columns of (this rank's rows of) Q_k, packed
+            double* dstq = qcols + uint64_t(p) * ttm_kpad(sd[k]) * ttm_rpad(Rc);
+            CPDB_CK(pack_q_cols(q, R, p * Rc, Rc, dstq, uint32_t(sd[k]), st));
+            acc(st, "pack_cols", {rg(q, sd[k] * R)},
+                {rg(dstq, uint64_t(ttm_kpad(sd[k])) * ttm_rpad(Rc))});
+            c->launches += 1;
+            qpp = dstq;
+        }
+        Timer t;
+        if (c->timing) {
+            t.a = events.get();
+            t.b = events.get();
+            t.kind = is_root ? 0 : 1;
+            CPDB_CK(cudaEventRecord(t.a, st));
+        }
+        cudaEvent_t tla = tl_begin(st);
+        fp(st, prefetch ? "root_prefetch" : is_root ? "root_ttm" : "branch_ttm", "in_before",
+           {rg(srcp, in_slab), rg(qp, uint64_t(ttm_kpad(sd[k])) * Rp)});
+        run_ttm(c, srcp, sdp, k, q, qpp, Rc, rawp, st, prefetch || yield_now, no_pdl || p > 0, sms,
+                prefetch ? pf.tpc : 0);
+        acc(st, prefetch ? "root_prefetch" : is_root ? "root_ttm" : "branch_ttm",
+              {rg(srcp, in_slab), rg(qp, uint64_t(ttm_kpad(sd[k])) * Rp)}, {rg(rawp, out_slab)});
+        tl_end(tla, st, prefetch ? "root_prefetch" : is_root ? "root" : "branch");
+        if (c->timing) {
+            CPDB_CK(cudaEventRecord(t.b, st));
+            t.flops = 2.0 * double(out_slab) * double(sd[k]);
+            t.bytes = 8.0 * (double(in_slab) + double(out_slab) + double(sd[k]) * R);
+            timers.push_back(t);
+        }
+        if (!sh || sh->red == kRedNone) continue;
+        // the collective runs on the main stream, after this slab's kernel
         if (st != s) {
             cudaEvent_t e0 = events.get();
             CPDB_CK(cudaEventRecord(e0, st));
             CPDB_CK(cudaStreamWaitEvent(s, e0, 0));
         }
-        Timer tc;
-        if (c->timing) {
+        if (c->timing && !comm_timed) {
             tc.a = events.get();
             tc.b = events.get();
             tc.kind = 2;
             CPDB_CK(cudaEventRecord(tc.a, s));
+            comm_timed = true;
         }
-        std::vector<uint64_t> od = sd;
-        od[k] = R;
         if (sh->red == kRedAllReduce) {
-            allreduce_sum(c, dst, numel(od));
+            allreduce_sum(c, dst + uint64_t(p) * out_slab, out_slab);
         } else {
             // blocks: everything from the scattered mode inward (contiguous,
             // that mode outermost), one per index of the modes before it
             const uint32_t m = uint32_t(sh->scatter);
             uint64_t outer = 1;
-            for (uint32_t j = 0; j < m; ++j) outer *= od[j];
-            reduce_scatter(c, raw, outer, numel(od) / outer, dst);
+            for (uint32_t j = 0; j < m; ++j) outer *= odp[j];
+            const uint64_t block = out_slab / outer;
+            reduce_scatter(c, rawp, outer, block,
+                           dst + uint64_t(p) * outer * (block / uint64_t(c->world)));
         }
-        if (c->timing) {
+    }
+    if (sh && sh->red != kRedNone) {
+        if (comm_timed) {
             CPDB_CK(cudaEventRecord(tc.b, s));
             timers.push_back(tc);
         }

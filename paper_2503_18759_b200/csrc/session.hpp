@@ -54,6 +54,9 @@ struct Session {
     std::vector<bool> need_local;
     std::vector<DevBuf> qp_local;
     std::map<cudaStream_t, DevBuf> rs_tmp;  // per producing stream
+    uint32_t rs_chunks = 4;      // CPDB_RS_CHUNKS
+    double rs_min_flops = 2e8;   // CPDB_RS_MIN_FLOPS
+    std::map<cudaStream_t, DevBuf> qcol_tmp;  // packed column halves of Q (ttm_step)
     DevBuf gate;  // {has_beta, beta, has_prev, prev_fitness} on the device (beta_gate)
     // the next sweep's first update issued before the host read this sweep's
     // fitness (Session::run); what undoing it needs

@@ -50,7 +50,10 @@ template <int RB, int CB, int BK, int STAGES, int LAYOUT>
 __global__ void __launch_bounds__(kThreads)
 ttm_dmma_kernel(const double* __restrict__ x, double* __restrict__ y, const double* __restrict__ qp,
                 uint64_t outer, uint64_t K, uint64_t inner, uint32_t R, uint64_t ntiles,
-                uint32_t nk) {
+                uint32_t nk, uint32_t Rtot) {
+    // (R: columns of this launch; Rtot: Y's extent in the contracted position
+    // -- larger than R when a wide rank is computed in 64-column blocks, y
+    // then points at the block's first column)
     pdl_entry();
     using C = TtmCfg<RB, CB, BK, STAGES, LAYOUT>;
     extern __shared__ __align__(128) double smem[];
@@ -167,7 +170,7 @@ ttm_dmma_kernel(const double* __restrict__ x, double* __restrict__ y, const doub
                         for (int rb = 0; rb < RB; ++rb) {
                             const uint32_t r = rb * 8 + (lane >> 2);
                             if (r < R)
-                                *reinterpret_cast<double2*>(y + (o * R + r) * inner + j) =
+                                *reinterpret_cast<double2*>(y + (o * Rtot + r) * inner + j) =
                                     make_double2(acc[rb][cb][0], acc[rb][cb][1]);
                         }
                     }
@@ -177,8 +180,8 @@ ttm_dmma_kernel(const double* __restrict__ x, double* __restrict__ y, const doub
 #pragma unroll
                         for (int rb = 0; rb < RB; ++rb) {
                             const uint32_t r = rb * 8 + 2 * (lane & 3);
-                            double* dst = y + m * R + r;
-                            if (r + 1 < R && (R % 2 == 0)) {
+                            double* dst = y + m * Rtot + r;
+                            if (r + 1 < R && (Rtot % 2 == 0)) {
                                 *reinterpret_cast<double2*>(dst) =
                                     make_double2(acc[rb][cb][0], acc[rb][cb][1]);
                             } else {
@@ -226,6 +229,33 @@ __global__ void pack_q_kernel(const double* __restrict__ q, double* __restrict__
     }
 }
 
+// columns [c0, c0 + Rc) of a K x ld matrix, packed like a K x Rc Q of their own
+__global__ void pack_q_cols_kernel(const double* __restrict__ q, double* __restrict__ qp,
+                                   uint32_t K, uint32_t ld, uint32_t c0, uint32_t Rc,
+                                   uint32_t Kpad, uint32_t Rp) {
+    pdl_entry();
+    const uint32_t n = Kpad * Rp;
+    for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+         idx += gridDim.x * blockDim.x) {
+        const uint32_t kq = idx % 4, r = (idx / 4) % Rp, kg = idx / (4 * Rp);
+        const uint32_t k = kg * 4 + kq;
+        qp[idx] = (k < K && r < Rc) ? q[size_t(k) * ld + c0 + r] : 0.0;
+    }
+}
+
+// R > 64: block b (columns 64b .. 64b+63) packed like a 64-column Q of its
+// own, [Kpad/4][64][4], the blocks one after the other
+__global__ void pack_q_blocks_kernel(const double* __restrict__ q, double* __restrict__ qp,
+                                     uint32_t K, uint32_t R, uint32_t Kpad) {
+    const uint32_t per = Kpad * 64, n = per * ((R + 63) / 64);
+    for (uint32_t idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n;
+         idx += gridDim.x * blockDim.x) {
+        const uint32_t b = idx / per, e = idx % per;
+        const uint32_t kq = e % 4, r = b * 64 + (e / 4) % 64, k = (e / 256) * 4 + kq;
+        qp[idx] = (k < K && r < R) ? q[size_t(k) * R + r] : 0.0;
+    }
+}
+
 template <int RB, int CB, int BK, int STAGES, int LAYOUT>
 cudaError_t launch_cfg(const TtmArgs& a, cudaStream_t s, int sms) {
     using C = TtmCfg<RB, CB, BK, STAGES, LAYOUT>;
@@ -246,7 +276,7 @@ cudaError_t launch_cfg(const TtmArgs& a, cudaStream_t s, int sms) {
     const uint64_t grid = std::min<uint64_t>(ntiles, uint64_t(sms) * per_sm);
     if (grid == 0) return cudaSuccess;
     return launch_pdl(kern, dim3(static_cast<unsigned>(grid)), dim3(kThreads), C::SMEM, s, a.x,
-                      a.y, a.qp, a.outer, a.K, a.inner, a.R, ntiles, nk);
+                      a.y, a.qp, a.outer, a.K, a.inner, a.R, ntiles, nk, a.Rtot ? a.Rtot : a.R);
 }
 
 // Tile shapes per padded rank: RB*CB accumulator tiles per warp <= 16, and an
@@ -269,17 +299,32 @@ cudaError_t dispatch(const TtmArgs& a, cudaStream_t s, int sms) {
 }  // namespace
 
 uint32_t ttm_kpad(uint64_t K) { return static_cast<uint32_t>(((K + 31) / 32) * 32); }
-uint32_t ttm_rpad(uint32_t R) { return ((R + 7) / 8) * 8; }
+// (wide ranks: whole 64-column blocks, each packed on its own)
+uint32_t ttm_rpad(uint32_t R) { return R <= 64 ? ((R + 7) / 8) * 8 : ((R + 63) / 64) * 64; }
 
 cudaError_t pack_q(const double* q, double* qp, uint32_t K, uint32_t R, cudaStream_t s) {
     const uint32_t Kpad = ttm_kpad(K), Rp = ttm_rpad(R);
+    if (R > 64) {
+        const uint32_t n = Kpad * Rp;
+        pack_q_blocks_kernel<<<(n + 255) / 256, 256, 0, s>>>(q, qp, K, R, Kpad);
+        return cudaGetLastError();
+    }
     const uint32_t n = Kpad * Rp;
     return launch_pdl(pack_q_kernel, dim3((n + 255) / 256), dim3(256), 0, s, q, qp, K, R, Kpad,
                       Rp);
 }
 
+cudaError_t pack_q_cols(const double* q, uint32_t ld, uint32_t c0, uint32_t Rc, double* qp,
+                        uint32_t K, cudaStream_t s) {
+    if (Rc > 64) return cudaErrorInvalidValue;
+    const uint32_t Kpad = ttm_kpad(K), Rp = ttm_rpad(Rc);
+    const uint32_t n = Kpad * Rp;
+    return launch_pdl(pack_q_cols_kernel, dim3((n + 255) / 256), dim3(256), 0, s, q, qp, K, ld, c0,
+                      Rc, Kpad, Rp);
+}
+
 TtmPath ttm_path(const TtmArgs& a) {
-    if (a.Rp > 64 || a.R == 0) return TtmPath::simple;
+    if (a.R == 0) return TtmPath::simple;
     if (a.inner % 8 == 0) return TtmPath::groups;
     if (a.inner == 1 && a.K % 2 == 0) return TtmPath::rows;
     return TtmPath::simple;
@@ -293,6 +338,23 @@ cudaError_t launch_ttm(const TtmArgs& a, cudaStream_t s, int sms) {
     if (version >= 2 && a.qp != nullptr && !a.no_tma) {
         const cudaError_t e = launch_ttm_tma(a, s, sms);  // warp-specialised TMA path
         if (e != cudaErrorNotSupported) return e;
+    }
+    if (a.R > 64 && a.qp != nullptr && ttm_path(a) != TtmPath::simple) {
+        // wide rank: one pass over X per 64-column block of Q (pack_q's
+        // blocked layout), each writing its columns of Y
+        const bool groups = ttm_path(a) == TtmPath::groups;
+        const uint32_t kpad = ttm_kpad(a.K);
+        for (uint32_t b = 0; b * 64 < a.R; ++b) {
+            TtmArgs ab = a;
+            ab.R = std::min<uint32_t>(64, a.R - b * 64);
+            ab.Rp = 64;
+            ab.Rtot = a.R;
+            ab.qp = a.qp + size_t(b) * kpad * 64;
+            ab.y = a.y + (groups ? uint64_t(b) * 64 * a.inner : uint64_t(b) * 64);
+            const cudaError_t e = groups ? dispatch<kGroups>(ab, s, sms) : dispatch<kRows>(ab, s, sms);
+            if (e != cudaSuccess) return e;
+        }
+        return cudaSuccess;
     }
     switch (ttm_path(a)) {
         case TtmPath::groups: return dispatch<kGroups>(a, s, sms);

@@ -13,8 +13,8 @@
 //   Q_n, R_n = thin_qr(A_n)                           factor_state.hpp:42-47
 //   fitness_fast_qr                                   kruskal.hpp:109-128
 // The Householder QR is a cooperative multi-CTA kernel: rows are split across
-// the grid, each reflector costs two grid barriers (column norm, then the
-// dot products with the trailing columns), every sum runs in a fixed order
+// the grid, each reflector costs one grid barrier in the factorisation and one
+// in the accumulation of Q, every sum runs in a fixed order
 // (deterministic), and the conventions are the reference's (alpha = -sign
 // ||x||, zero columns skipped, nonnegative diag(R) by a final sign flip).
 #include <cooperative_groups.h>
@@ -64,7 +64,7 @@ struct HhArgs {
 };
 
 __host__ __device__ inline size_t hh_scratch_doubles(uint32_t n, int grid) {
-    return size_t(2) * grid * 2 + size_t(2) * grid * n;
+    return size_t(2) * grid * n + size_t(2) * n;
 }
 
 // sum of x over the CTA in a fixed order (warp tree, then warps in order)
@@ -115,23 +115,35 @@ __global__ void __launch_bounds__(kHT) hh_coop_kernel(HhArgs a) {
     const uint64_t chunk = (m + G - 1) / G;
     const uint64_t row0 = uint64_t(c) * chunk < m ? uint64_t(c) * chunk : m;
     const uint64_t row1 = row0 + chunk < m ? row0 + chunk : m;
-    double* pn = a.scratch;                       // [2][G][2]: (w_kk^2 owner term, tail sum)
-    double* pd = a.scratch + size_t(2) * G * 2;   // [2][G][n]
+    double* pd = a.scratch;  // [2][G][n]: per-CTA partial products, double-buffered
+    double* prow = a.scratch + size_t(2) * G * n;  // [2][n]: row k as it was before its update
     double* w = a.w;
 
-    // ---- factorisation: reflector k from column k, applied to columns > k
+    // ---- factorisation: reflector k from column k, applied to columns > k.
+    // One grid barrier per reflector: the products s_j = sum_{i > k} w_ik w_ij
+    // (j >= k; s_k is the column's tail norm) need nothing from the
+    // reflector's head, so each CTA publishes them for its rows first; after
+    // the barrier every CTA knows ||x||, alpha, v_0 = w_kk - alpha, beta and
+    // d_j = v_0 w_kj + s_j, and updates its own rows.
     for (uint32_t k = 0; k < n; ++k) {
-        // (a) tail = sum_{i > k} w_ik^2 over the whole column (fixed order)
-        double t = 0.0;
-        for (uint64_t i = (row0 > k ? row0 : uint64_t(k) + 1) + threadIdx.x; i < row1; i += kHT)
-            t = fma(w[i * n + k], w[i * n + k], t);
-        t = cta_sum(t, red);
-        double* pnk = pn + size_t(k & 1) * G * 2;
-        if (threadIdx.x == 0) pnk[c * 2] = t;
+        const uint64_t lo1 = row0 > k ? row0 : uint64_t(k) + 1;  // rows below the diagonal
+        auto wk = [&](uint64_t i) { return w[i * n + k]; };
+        double* pdk = pd + size_t(k & 1) * G * n;
+        cta_col_dots(w, n, lo1, row1, k, wk, part, pdk + size_t(c) * n);
+        // (its owner updates row k right after the barrier: the others read
+        // this copy)
+        double* prk = prow + size_t(k & 1) * n;
+        if (k >= row0 && k < row1)
+            for (uint32_t j = k + threadIdx.x; j < n; j += kHT) prk[j] = w[uint64_t(k) * n + j];
         grid.sync();
-        double tail = 0.0;
-        for (int b = 0; b < G; ++b) tail += pnk[b * 2];
-        const double wkk = w[uint64_t(k) * n + k];
+        for (uint32_t j = k + threadIdx.x; j < n; j += kHT) {
+            double s = 0.0;
+            for (int b = 0; b < G; ++b) s += pdk[size_t(b) * n + j];
+            dsh[j] = s;
+        }
+        __syncthreads();
+        const double tail = dsh[k];
+        const double wkk = prk[k];
         const double norm = sqrt(fma(wkk, wkk, tail));
         if (norm == 0.0) {  // zero column: R(k,k) stays 0 (uniform over the grid)
             if (threadIdx.x == 0) {
@@ -150,24 +162,19 @@ __global__ void __launch_bounds__(kHT) hh_coop_kernel(HhArgs a) {
             vdiag[k] = v0;
             sgn[k] = alpha < 0.0 ? -1.0 : 1.0;
         }
-        // (b) d_j = sum_{i >= k} v_i w_ij, j > k
-        const uint64_t lo = row0 > k ? row0 : uint64_t(k);
-        auto vco = [&](uint64_t i) { return i == k ? v0 : w[i * n + k]; };
-        double* pdk = pd + size_t(k & 1) * G * n;
-        cta_col_dots(w, n, lo, row1, k + 1, vco, part, pdk + size_t(c) * n);
-        grid.sync();
-        for (uint32_t j = k + 1 + threadIdx.x; j < n; j += kHT) {
-            double s = 0.0;
-            for (int b = 0; b < G; ++b) s += pdk[size_t(b) * n + j];
-            dsh[j] = s * beta;
-        }
+        // d_j = v_0 w_kj + s_j, scaled by beta (row k is final since the
+        // previous reflector's update, before this barrier)
         __syncthreads();
-        // (c) w_ij -= (beta d_j) v_i on this CTA's rows; column k keeps v below
+        for (uint32_t j = k + 1 + threadIdx.x; j < n; j += kHT)
+            dsh[j] = fma(v0, prk[j], dsh[j]) * beta;
+        __syncthreads();
+        // w_ij -= (beta d_j) v_i on this CTA's rows; column k keeps v below
         // the diagonal and alpha on it
         {
+            const uint64_t lo = row0 > k ? row0 : uint64_t(k);
             const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
             for (uint64_t i = lo + g; i < row1; i += kHW) {
-                const double vi = vco(i);
+                const double vi = i == k ? v0 : w[i * n + k];
                 for (uint32_t j = ((k + 1) / 32) * 32 + lane; j < n; j += 32)
                     if (j > k) w[i * n + j] = fma(-dsh[j], vi, w[i * n + j]);
             }
@@ -234,7 +241,8 @@ cudaError_t hh_launch(const HhArgs& a, cudaStream_t s) {
     cudaError_t e = cudaFuncSetAttribute(hh_coop_kernel,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
     if (e != cudaSuccess) return e;
-    int grid = int(std::min<uint64_t>(uint64_t(sms), (a.m + 63) / 64));
+    // (at least 128 rows per CTA: a barrier costs more than a few rows)
+    int grid = int(std::min<uint64_t>(uint64_t(sms), (a.m + 127) / 128));
     grid = std::max(grid, 1);
     HhArgs args = a;
     void* params[] = {&args};

@@ -21,6 +21,10 @@ TTM_SHAPES = [
     ((33, 40, 48), 32),
     ((24, 32, 40), 64),
     ((100, 100, 100), 10),   # C1 shape
+    ((24, 32, 40), 65),      # wide ranks: 64-column blocks (one column in the second)
+    ((40, 48, 32, 16), 130),
+    ((18, 20, 22), 96),      # a contracted extent that is not a multiple of 4
+    ((9, 8, 7), 70),         # generic path at a wide rank
 ]
 
 

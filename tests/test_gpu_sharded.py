@@ -223,3 +223,43 @@ def test_sharded_c5_proxy_matches_unsharded(ctx, port, policy, world):
             assert np.linalg.norm(fa - fb) <= 1e-10 * np.linalg.norm(fb)
     for c in group:
         c.close()
+
+
+@pytest.mark.parametrize("policy", ["eager", "scatter", "auto"])
+@pytest.mark.parametrize("dims,rank,world", [((64, 64, 64, 64), 64, 2), ((128, 72, 64), 64, 4),
+                                             ((32, 24, 24, 20), 8, 2)])
+def test_reduced_steps_in_slabs_bit_identical(monkeypatch, policy, dims, rank, world):
+    """A reduced TTM step runs in slabs whose collectives overlap the next
+    slab's kernel (Session::ttm_step): column halves of Q when it contracts
+    the leading (split) mode at R = 64, outer slices otherwise.  Every output
+    element is accumulated and reduced in the same order as in one launch and
+    one collective: bit-identical runs."""
+    import paper_2503_18759_b200 as cpd
+    rows = dims[0] // world
+    cfg = cpd.SolverConfig(rank=rank, max_iterations=5, seed=7)
+    monkeypatch.setenv("CPDB_RS_MIN_FLOPS", "0")
+    outs = []
+    for chunks in ("1", "4"):
+        monkeypatch.setenv("CPDB_RS_CHUNKS", chunks)
+        group = cpd.Context.local_group(0, world)
+        cost = {"bus_gbs": 0.05} if policy == "auto" else None
+
+        def rank_run(r, c):
+            c.set_shard_policy(policy, cost)
+            c.synth_tensor(0, list(dims), rank, 1e-3, 31337)
+            res = c.solve(cfg, extrapolate=True)
+            return res, c.profile()["kernel_launches"]
+
+        outs.append(run_ranks(group, rank_run))
+        for c in group:
+            c.close()
+    one, four = outs
+    # (auto may pick lazy everywhere, and eager at R < 64 only reduces
+    # leading-mode contractions, which stay whole: no slabs there)
+    if policy == "scatter" or (policy == "eager" and rank == 64):
+        assert four[0][1] > one[0][1]  # the slabs did launch
+    for (a, _), (b, _) in zip(one, four):
+        assert [(t.fitness, t.raw_radicand) for t in a.trace] == \
+               [(t.fitness, t.raw_radicand) for t in b.trace]
+        for fa, fb in zip(a.model.factors, b.model.factors):
+            assert np.array_equal(fa, fb)
