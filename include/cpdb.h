@@ -193,7 +193,11 @@ int cpdb_tensor_norm_sq(cpdb_ctx* ctx, double* out);
 /* Runs cp_als_qr / als_qr_bre on the context's X entirely in HBM.  state may
  * be NULL (fresh run).  trace holds max_iterations rows.  factors_per_sweep
  * (max_iterations x sum I_k R) and lambda_per_sweep (max_iterations x R) are
- * optional per-sweep dumps for parity checks. */
+ * optional per-sweep dumps for parity checks.  Ranks up to 1024 (the tuned
+ * kernels up to 64, rank-generic ones beyond).  A CholeskyQR breakdown that the
+ * shifted retry cannot cure restarts the run on the Householder kernels, as
+ * the reference's thin_qr (linalg.hpp:39-99) never breaks down
+ * (cpdb_profile.qr_householder counts the restarts). */
 int cpdb_solve(cpdb_ctx* ctx, const cpdb_config* cfg, cpdb_state* state, cpdb_trace_row* trace,
                uint64_t* trace_len, double* out_lambda, double* out_factors,
                double* factors_per_sweep, double* lambda_per_sweep, cpdb_q0_observer observer,
@@ -201,7 +205,12 @@ int cpdb_solve(cpdb_ctx* ctx, const cpdb_config* cfg, cpdb_state* state, cpdb_tr
 /* The same run as a resumable session: begin = run_qr setup
  * (solvers.hpp:217-241), run = n more sweeps of the loop (:243-302), end =
  * model + sweep-boundary state (:304-308).  cfg->max_iterations bounds the
- * plan; *finished is set once it is exhausted or the fitness threshold hit. */
+ * plan; *finished is set once it is exhausted or the fitness threshold hit.
+ * While sweeps remain, run() leaves the next sweep's first update in flight
+ * on the device (the following run() consumes it); end() takes it back, so
+ * the exported state is the one after the sweeps that were run, and a
+ * session that was ended in the middle accepts no further run()
+ * (CPDB_LOGIC_ERROR): begin a new one from the exported state. */
 typedef struct cpdb_session cpdb_session;
 int cpdb_session_begin(cpdb_ctx* ctx, const cpdb_config* cfg, const cpdb_state* state,
                        cpdb_session** out);

@@ -289,9 +289,50 @@ solve_rows_wide_kernel(const double* v, const double* r0, uint32_t n, uint64_t r
     }
 }
 
-__global__ void fit_copy_kernel(const double* out4, double* fit_out) {
-    fit_out[0] = out4[2];
-    fit_out[1] = out4[3];
+// fitness_fast_qr (kruskal.hpp:109-128) across the grid: block b sums
+// <V_fit, A_hat R0^T> over its rows (warp per row, lanes over the columns);
+// the last kernel adds the blocks in order and forms ||K||^2 and the fitness.
+constexpr int kFitBlocks = 148;
+
+__global__ void __launch_bounds__(kHT)
+fit_xk_kernel(const double* v, const double* ah, const double* r0, uint64_t rows, uint32_t r,
+              double* partial) {
+    __shared__ double red[kHW];
+    const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double s = 0.0;
+    for (uint64_t i = uint64_t(blockIdx.x) * kHW + g; i < rows; i += uint64_t(gridDim.x) * kHW)
+        for (uint32_t j = lane; j < r; j += 32) {
+            double m = 0.0;
+            for (uint32_t p = j; p < r; ++p) m = fma(ah[i * r + p], r0[size_t(j) * r + p], m);
+            s = fma(v[i * r + j], m, s);
+        }
+    s = cta_sum(s, red);
+    if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+__global__ void __launch_bounds__(kHT)
+fit_final_kernel(double nx2, const double* partial, int nb, const double* r0, const double* rn,
+                 const double* lam, uint32_t r, double* fit_out) {
+    __shared__ double red[kHW];
+    double k = 0.0;
+    for (uint32_t e = threadIdx.x; e < r * r; e += kHT) {
+        const uint32_t i = e / r, j = e % r, top = i < j ? i : j;
+        double g0 = 0.0, gn = 0.0;
+        for (uint32_t p = 0; p <= top; ++p) {
+            g0 = fma(r0[size_t(p) * r + i], r0[size_t(p) * r + j], g0);
+            gn = fma(rn[size_t(p) * r + i], rn[size_t(p) * r + j], gn);
+        }
+        k += g0 * lam[i] * gn * lam[j];
+    }
+    k = cta_sum(k, red);
+    if (threadIdx.x == 0) {
+        double xk = 0.0;
+        for (int b = 0; b < nb; ++b) xk += partial[b];
+        const double raw = nx2 - 2.0 * xk + k;
+        const double rad = raw < 0.0 ? 0.0 : raw;
+        fit_out[0] = 1.0 - sqrt(rad) / sqrt(nx2);
+        fit_out[1] = raw;
+    }
 }
 
 
@@ -404,7 +445,7 @@ bool wide_rank(uint32_t R) { return R > 64; }
 size_t zqr_wide_work_doubles(uint32_t R) { return hh_scratch_doubles(R, wide_sms()) + 8; }
 
 size_t finish_wide_scratch_doubles(uint64_t I, uint32_t R) {
-    return 2 * I * R + hh_scratch_doubles(R, wide_sms()) + 16;
+    return 2 * I * R + hh_scratch_doubles(R, wide_sms()) + kFitBlocks + 16;
 }
 
 // Z into q1 (the kernel's working copy), Householder in place, Q0 / R0 out.
@@ -448,9 +489,10 @@ cudaError_t launch_finish_wide(const FinishArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     if (a.fitness && !a.init) {
         const double* vfit = a.dual ? a.vfitpart : a.vpart;
-        e = fitness_dev(a.norm_x_sq, vfit, ahat, I, a.r0, a.r_out, a.lambda, R, out4, s);
-        if (e != cudaSuccess) return e;
-        fit_copy_kernel<<<1, 1, 0, s>>>(out4, a.fit_out);
+        const int nb = int(std::min<uint64_t>(kFitBlocks, (I + kHW - 1) / kHW));
+        fit_xk_kernel<<<nb, kHT, 0, s>>>(vfit, ahat, a.r0, I, R, out4);
+        fit_final_kernel<<<1, kHT, 0, s>>>(a.norm_x_sq, out4, nb, a.r0, a.r_out, a.lambda, R,
+                                           a.fit_out);
     }
     return cudaGetLastError();
 }
