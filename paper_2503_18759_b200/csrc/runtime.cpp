@@ -137,6 +137,15 @@ void dev_trim(int device) {
     if (cur != device) cudaSetDevice(device);
     for (void* p : drop) cudaFree(p);
     if (cur != device) cudaSetDevice(cur);
+    if (!drop.empty()) {  // (CPDB_GUARD: freed blocks leave the registry)
+        std::lock_guard<std::mutex> lk(g_pool_mu);
+        for (size_t i = 0; i < g_guarded.size();) {
+            if (std::find(drop.begin(), drop.end(), g_guarded[i].p) != drop.end())
+                g_guarded.erase(g_guarded.begin() + long(i));
+            else
+                ++i;
+        }
+    }
 }
 
 DevBuf::~DevBuf() { dev_release(p, n * sizeof(double), dev); }

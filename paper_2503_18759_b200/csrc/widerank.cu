@@ -100,6 +100,39 @@ __device__ void cta_col_dots(const double* mat, uint32_t n, uint64_t lo, uint64_
     }
 }
 
+// out[j] = sum over the grid's CTAs b of pd[b][j], j in [j0, n), in a fixed
+// order: up to 8 threads per column take interleaved b with four loads in
+// flight each (the partials come from L2), then the column's threads are
+// added in order.  part: kHW x n shared scratch.
+__device__ void grid_partials_sum(const double* pd, int G, uint32_t n, uint32_t j0, double* part,
+                                  double* out) {
+    const uint32_t nc = n - j0;
+    uint32_t parts = kHT / nc;
+    parts = parts < 1 ? 1 : parts > uint32_t(kHW) ? uint32_t(kHW) : parts;
+    if (parts > uint32_t(G)) parts = uint32_t(G);
+    for (uint32_t e = threadIdx.x; e < nc * parts; e += kHT) {
+        const uint32_t j = j0 + e % nc, sub = e / nc;
+        double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+        int b = int(sub);
+        const int st = int(parts);
+        for (; b + 3 * st < G; b += 4 * st) {
+            s0 += pd[size_t(b) * n + j];
+            s1 += pd[size_t(b + st) * n + j];
+            s2 += pd[size_t(b + 2 * st) * n + j];
+            s3 += pd[size_t(b + 3 * st) * n + j];
+        }
+        for (; b < G; b += st) s0 += pd[size_t(b) * n + j];
+        part[sub * n + j] = (s0 + s1) + (s2 + s3);
+    }
+    __syncthreads();
+    for (uint32_t j = j0 + threadIdx.x; j < n; j += kHT) {
+        double t = 0.0;
+        for (uint32_t sub = 0; sub < parts; ++sub) t += part[sub * n + j];
+        out[j] = t;
+    }
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(kHT) hh_coop_kernel(HhArgs a) {
     cg::grid_group grid = cg::this_grid();
     extern __shared__ double sm[];
@@ -136,12 +169,7 @@ __global__ void __launch_bounds__(kHT) hh_coop_kernel(HhArgs a) {
         if (k >= row0 && k < row1)
             for (uint32_t j = k + threadIdx.x; j < n; j += kHT) prk[j] = w[uint64_t(k) * n + j];
         grid.sync();
-        for (uint32_t j = k + threadIdx.x; j < n; j += kHT) {
-            double s = 0.0;
-            for (int b = 0; b < G; ++b) s += pdk[size_t(b) * n + j];
-            dsh[j] = s;
-        }
-        __syncthreads();
+        grid_partials_sum(pdk, G, n, k, part, dsh);
         const double tail = dsh[k];
         const double wkk = prk[k];
         const double norm = sqrt(fma(wkk, wkk, tail));
@@ -205,11 +233,8 @@ __global__ void __launch_bounds__(kHT) hh_coop_kernel(HhArgs a) {
         // (columns j < k of rows >= k are still zero)
         cta_col_dots(q, n, lo, row1, uint32_t(k), vco, part, pdk + size_t(c) * n);
         grid.sync();
-        for (uint32_t j = uint32_t(k) + threadIdx.x; j < n; j += kHT) {
-            double s = 0.0;
-            for (int b = 0; b < G; ++b) s += pdk[size_t(b) * n + j];
-            dsh[j] = s * beta;
-        }
+        grid_partials_sum(pdk, G, n, uint32_t(k), part, dsh);
+        for (uint32_t j = uint32_t(k) + threadIdx.x; j < n; j += kHT) dsh[j] *= beta;
         __syncthreads();
         const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
         for (uint64_t i = lo + g; i < row1; i += kHW) {
