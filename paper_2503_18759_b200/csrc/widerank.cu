@@ -31,7 +31,7 @@ namespace cg = cooperative_groups;
 namespace cpdb {
 namespace {
 
-constexpr int kHT = 256;        // threads per CTA
+constexpr int kHT = 512;        // threads per CTA
 constexpr int kHW = kHT / 32;   // warps = row groups
 constexpr int kMaxWide = 1024;  // widest supported matrix (columns)
 
@@ -81,22 +81,67 @@ __device__ double cta_sum(double x, double* red) {
 // d[j] = sum over this CTA's rows i in [lo, hi) of vcoef(i) * mat[i][j], for
 // j in [j0, n): warp g takes rows lo+g, lo+g+8, ... and lanes take 32
 // consecutive columns; the warps' partials are added in warp order.
+constexpr int kHU = 8;  // rows in flight per lane (the loads are L2 hits: latency-bound)
+
 template <class V>
 __device__ void cta_col_dots(const double* mat, uint32_t n, uint64_t lo, uint64_t hi, uint32_t j0,
                              V vcoef, double* part /*[kHW][n]*/, double* out /*[n]*/) {
     const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (uint32_t jb = (j0 / 32) * 32; jb < n; jb += 32) {
         const uint32_t j = jb + lane;
-        double d = 0.0;
-        if (j < n)
-            for (uint64_t i = lo + g; i < hi; i += kHW) d = fma(vcoef(i), mat[i * n + j], d);
-        if (j < n) part[g * n + j] = d;
+        if (j >= n) continue;
+        double d[kHU];
+#pragma unroll
+        for (int u = 0; u < kHU; ++u) d[u] = 0.0;
+        for (uint64_t i = lo + g; i < hi; i += uint64_t(kHU) * kHW) {
+            double v[kHU], x[kHU];
+#pragma unroll
+            for (int u = 0; u < kHU; ++u) {
+                const uint64_t r = i + uint64_t(u) * kHW;
+                v[u] = r < hi ? vcoef(r) : 0.0;
+                x[u] = r < hi ? mat[r * n + j] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kHU; ++u) d[u] = fma(v[u], x[u], d[u]);
+        }
+        part[g * n + j] = ((d[0] + d[1]) + (d[2] + d[3])) + ((d[4] + d[5]) + (d[6] + d[7]));
     }
     __syncthreads();
     for (uint32_t j = j0 + threadIdx.x; j < n; j += kHT) {
         double t = 0.0;
         for (int w = 0; w < kHW; ++w) t += part[w * n + j];
         out[j] = t;
+    }
+}
+
+// mat[i][j] -= dsh[j] * vcoef(i) for this CTA's rows i in [lo, hi) and the
+// columns j >= j0: kHU rows per lane in flight.
+template <class V>
+__device__ void cta_rank1_update(double* mat, uint32_t n, uint64_t lo, uint64_t hi, uint32_t j0,
+                                 V vcoef, const double* dsh) {
+    const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint64_t i = lo + g; i < hi; i += uint64_t(kHU) * kHW) {
+        double v[kHU];
+#pragma unroll
+        for (int u = 0; u < kHU; ++u) {
+            const uint64_t r = i + uint64_t(u) * kHW;
+            v[u] = r < hi ? vcoef(r) : 0.0;
+        }
+        for (uint32_t j = (j0 / 32) * 32 + lane; j < n; j += 32) {
+            if (j < j0) continue;
+            double x[kHU];
+#pragma unroll
+            for (int u = 0; u < kHU; ++u) {
+                const uint64_t r = i + uint64_t(u) * kHW;
+                x[u] = r < hi ? mat[r * n + j] : 0.0;
+            }
+            const double dj = dsh[j];
+#pragma unroll
+            for (int u = 0; u < kHU; ++u) {
+                const uint64_t r = i + uint64_t(u) * kHW;
+                if (r < hi) mat[r * n + j] = fma(-dj, v[u], x[u]);
+            }
+        }
     }
 }
 
@@ -200,12 +245,8 @@ __global__ void __launch_bounds__(kHT) hh_coop_kernel(HhArgs a) {
         // the diagonal and alpha on it
         {
             const uint64_t lo = row0 > k ? row0 : uint64_t(k);
-            const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
-            for (uint64_t i = lo + g; i < row1; i += kHW) {
-                const double vi = i == k ? v0 : w[i * n + k];
-                for (uint32_t j = ((k + 1) / 32) * 32 + lane; j < n; j += 32)
-                    if (j > k) w[i * n + j] = fma(-dsh[j], vi, w[i * n + j]);
-            }
+            auto vco = [&](uint64_t i) { return i == k ? v0 : w[i * n + k]; };
+            cta_rank1_update(w, n, lo, row1, k + 1, vco, dsh);
         }
         __syncthreads();
         if (threadIdx.x == 0 && k >= row0 && k < row1) w[uint64_t(k) * n + k] = alpha;
@@ -236,12 +277,7 @@ __global__ void __launch_bounds__(kHT) hh_coop_kernel(HhArgs a) {
         grid_partials_sum(pdk, G, n, uint32_t(k), part, dsh);
         for (uint32_t j = uint32_t(k) + threadIdx.x; j < n; j += kHT) dsh[j] *= beta;
         __syncthreads();
-        const int g = threadIdx.x >> 5, lane = threadIdx.x & 31;
-        for (uint64_t i = lo + g; i < row1; i += kHW) {
-            const double vi = vco(i);
-            for (uint32_t j = (uint32_t(k) / 32) * 32 + lane; j < n; j += 32)
-                if (j >= uint32_t(k)) q[i * n + j] = fma(-dsh[j], vi, q[i * n + j]);
-        }
+        cta_rank1_update(q, n, lo, row1, uint32_t(k), vco, dsh);
         __syncthreads();
     }
     for (uint64_t e = row0 * n + threadIdx.x; e < row1 * n; e += kHT)
