@@ -43,6 +43,7 @@ def run_ranks(ctxs, fn):
     ((128, 96, 64), 16, 4, "bre"),
     ((32, 24, 24, 20), 8, 8, "bre"),
     ((16, 16, 16, 16), 64 // 4, 4, "bre"),
+    ((132, 70, 68), 66, 2, "bre"),  # a rank above 64: the rank-generic tail, blocked Q packing
 ])
 def test_sharded_matches_unsharded(ctx, port, dims, rank, world, variant, policy):
     """Every reduction strategy of the sharded session (csrc/shard.cpp: eager
