@@ -123,6 +123,9 @@ typedef struct {
                                  shifted retry (kappa beyond ~1e8)                 */
     uint64_t qr_householder;  /* solves restarted on the Householder kernels after
                                  a CholeskyQR breakdown the retry could not cure   */
+    uint64_t gate_mispredictions; /* updates issued ahead on "the beta gate stays
+                                 closed" and issued again when it opened (once
+                                 per run at most)                                  */
 } cpdb_profile;
 
 /* ---- version / device ----------------------------------------------------- */

@@ -82,6 +82,7 @@ class Profile(C.Structure):
         ("kernel_launches", C.c_uint64),
         ("qr_shifted", C.c_uint64),
         ("qr_householder", C.c_uint64),
+        ("gate_mispredictions", C.c_uint64),
     ]
 
 

@@ -352,6 +352,12 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
         // tall Z.  CPDB_REUSE_BOUNDARY=0/1 overrides.
         // slabs of a reduced TTM step whose collectives overlap the next
         // slab's kernel (ttm_step); steps below ~0.2 GFLOP are launch-bound
+        // (measured: the 6-7 pre-activation sweeps at C2 run 0.48 -> 0.45 ms,
+        // but the steady state that follows the one misprediction settles
+        // 1% (C2) to 3% (C1) slower -- the streams' phase alignment differs
+        // -- so it is off unless CPDB_PREDICT_GATE=1)
+        const char* pg = std::getenv("CPDB_PREDICT_GATE");
+        predict_gate = pg && pg[0] == '1';
         const char* rc = std::getenv("CPDB_RS_CHUNKS");
         rs_chunks = rc ? uint32_t(std::max(1, std::atoi(rc))) : 4u;
         const char* rf = std::getenv("CPDB_RS_MIN_FLOPS");
@@ -1559,7 +1565,20 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
                 spec.had_hist = has_hist[n1];
                 spec.prev_last_mode = last_mode;
                 double unused = 0.0;
-                if (dep_events && (!extrap || has_beta)) {
+                // Until the beta gate opens no update extrapolates, and it
+                // opens once per run: the update is issued on the prediction
+                // that this sweep's fitness leaves it closed (plain V, the
+                // host's decision -- nothing read from this sweep's finisher),
+                // beside the last update like a frozen-beta one.  If the gate
+                // does open on this sweep, the update is undone and issued
+                // again with beta (below); its successor's front waits for
+                // the host in the predicted case, so nothing else is redone.
+                // CPDB_PREDICT_GATE=1 enables it (off by default, see begin()).
+                const bool frozen = !extrap || has_beta;
+                const bool predicted = !frozen && predict_gate;
+                spec.predicted = false;
+                if (dep_events && (frozen || predicted)) {
+                    spec.predicted = predicted;
                     // beta frozen (or no extrapolation): the update needs
                     // nothing from this sweep's last V-GEMM / finisher, so
                     // it runs beside them on its own stream (its front waited
@@ -1580,7 +1599,7 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
                     // and the second update's front (Z-QR + chain: no beta,
                     // no returned state -- nothing to undo), which also
                     // launches the root prefetch planned by the first
-                    if (order > 2) {
+                    if (order > 2 && frozen) {
                         // (its Z-QR right behind the speculative finisher on
                         // aux: measured C4 6270 -> 6440 sweeps/s, C1 +1%; C3
                         // (fourth order) -2%, so third order only;
@@ -1696,6 +1715,12 @@ uint64_t Session::run(uint64_t nsweeps, cpdb_trace_row* trace, double* fps, doub
         if (spec.issued) {
             if (converged) {
                 undo_speculative_update();
+            } else if (spec.predicted && spec.had_hist && has_beta && beta != 0.0) {
+                // the gate opened on this sweep: the update issued ahead
+                // assumed it closed.  Taken back; the next iteration issues
+                // it again, extrapolated (its front's results stand).
+                undo_speculative_update();
+                c->prof.gate_mispredictions += 1;
             } else if (extrap && spec.had_hist && has_beta && beta != 0.0) {
                 spec.beta_used = beta;  // what the device gate decided for it
             }
@@ -1719,6 +1744,11 @@ void Session::undo_speculative_update() {
     fb[n].swap(fb_alt[n]);
     lam.swap(lam_alt);
     zpar ^= 1;
+    zb[zpar].reuse = spec.reused;  // (an update issued again reads the same buffers)
+    // the root prefetch its back planned (not launched yet: that happens in
+    // the next front) is planned again by the update issued in its place --
+    // and must not budget that update's own kernels meanwhile
+    if (pf.active && !pf.launched) pf.active = false;
     if (extrap && !spec.reused) {
         hist[n].swap(zb[zpar].q0);
         std::swap(ev_hist[n], ev_zq_pending);

@@ -67,6 +67,7 @@ struct Session {
         int prev_last_mode = -1;
         double beta_used = 0.0;  // its trace contribution, once the host knows the gate
         bool reused = false;     // it took the previous update's Y_(n) / Q0 (no history swap)
+        bool predicted = false;  // issued on the prediction that the beta gate stays closed
     } spec;
     bool speculate = false;  // CPDB_SPECULATE=0 turns it off
     bool self_hist = true;   // CPDB_SELF_HIST=0: always wait for the history's own Z-QR
@@ -109,6 +110,7 @@ struct Session {
         std::vector<uint64_t> src_stamps, versions;
     } prev_front;
     bool reuse_ok = true;  // CPDB_REUSE_BOUNDARY=0: recompute (A/B testing)
+    bool predict_gate = false;  // CPDB_PREDICT_GATE=1: pre-activation updates issued on "the gate stays closed"
     int zpar = 0;  // parity of the update in flight (set by the front, used by the back)
     // Dependency events of the event-driven schedule (dep_events): the
     // finisher that last updated each mode, the V-GEMM that last read ybuf[n],

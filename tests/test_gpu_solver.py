@@ -605,3 +605,46 @@ def test_boundary_repetition_elided_bit_identical(monkeypatch, dims, rank, extra
     assert len(c.trace) == len(d.trace) == k + 1
     for fa, fb in zip(c.model.factors, d.model.factors):
         assert np.array_equal(fa, fb)
+
+
+@pytest.mark.parametrize("dims,rank", [((40, 36, 32), 8), ((20, 18, 16, 14), 6), ((256, 256, 256), 20),
+                                       ((64, 64, 64, 64), 16)])
+def test_gate_prediction_bit_identical(monkeypatch, dims, rank):
+    """Before the beta gate opens, the next sweep's first update is issued on
+    the prediction that it stays closed; on the sweep where it opens the
+    update is taken back and issued again with beta (once per run).  Same
+    bits as waiting for the gate on the device (CPDB_PREDICT_GATE=0), with
+    and without the boundary reuse, also when the stop test fires on the
+    activation sweep itself."""
+    import paper_2503_18759_b200 as cpd
+    ctx = cpd.Context(0)
+    ctx.synth_tensor(0, list(dims), rank, 1e-2, 99)
+
+    def go(predict, reuse, iters, thr=1.0):
+        monkeypatch.setenv("CPDB_PREDICT_GATE", predict)
+        monkeypatch.setenv("CPDB_REUSE_BOUNDARY", reuse)
+        r = ctx.solve(cfg_of(rank, iters, seed=3, fitness_threshold=thr), extrapolate=True)
+        return r, ctx.profile()["gate_mispredictions"]
+
+    def key(r):
+        return [(t.fitness, t.raw_radicand, t.flops, t.beta_used) for t in r.trace]
+
+    base, m0 = go("0", "0", 16)
+    assert m0 == 0
+    act = next(i for i, t in enumerate(base.trace) if t.beta_used != 0.0)  # first extrapolated sweep
+    for reuse in ("0", "1"):
+        got, m = go("1", reuse, 16)
+        assert m == 1  # the gate opened once
+        assert key(got) == key(base)
+        for fa, fb in zip(got.model.factors, base.model.factors):
+            assert np.array_equal(fa, fb)
+    # stop on the sweep whose fitness opens the gate (the one before `act`)
+    f = [t.fitness for t in base.trace]
+    stop = act - 1
+    if stop >= 1 and f[stop] > f[stop - 1]:
+        thr = 0.5 * (f[stop - 1] + f[stop])
+        a, _ = go("1", "1", 16, thr)
+        b, _ = go("0", "0", 16, thr)
+        assert len(a.trace) == len(b.trace) == stop + 1
+        for fa, fb in zip(a.model.factors, b.model.factors):
+            assert np.array_equal(fa, fb)
