@@ -156,6 +156,9 @@ struct Session {
     void acc(cudaStream_t st, const char* what, std::initializer_list<HbCheck::Rg> rd,
              std::initializer_list<HbCheck::Rg> wr) {
         hb.op(st, what, rd, wr);
+        // (legacy-stream accesses are blocking cudaMemcpy calls: the host has
+        // synchronised with them when they return)
+        if (st == nullptr) hb.sync_stream(nullptr);
         if (fpath) {
             if (!fp_light || what[0] == 'v') fp(st, what, "in_after", rd);
             fp(st, what, "out", wr);
