@@ -620,11 +620,18 @@ int cpdb_thin_qr(cpdb_ctx* c, const double* a, uint64_t m, uint64_t n, double* q
         if (m == 0 || n == 0) fail(CPDB_INVALID_ARGUMENT, "Matrix: zero dimension");
         if (m < n) fail(CPDB_INVALID_ARGUMENT, "thin_qr: requires rows >= cols");
         double* da = c->scratch_a.ensure(m * n);
-        double* dw = c->scratch_b.ensure(2 * m * n + n);
+        // (tall inputs: the cooperative multi-CTA kernel, widerank.cu -- the
+        // same reference algorithm with the rows split across the SMs)
+        const bool coop = m >= 256 && n <= 1024;
+        double* dw = c->scratch_b.ensure(
+            coop ? m * n + cpdb::zqr_wide_work_doubles(uint32_t(n)) : 2 * m * n + n);
         double* dq = c->scratch_c.ensure(m * n);
         double* dr = c->scratch_d.ensure(n * n);
         upload(c, da, a, m * n);
-        CPDB_CK(cpdb::householder_qr(da, m, uint32_t(n), dw, dq, dr, c->stream));
+        if (coop)
+            CPDB_CK(cpdb::householder_qr_wide(da, m, uint32_t(n), dw, dq, dr, c->stream));
+        else
+            CPDB_CK(cpdb::householder_qr(da, m, uint32_t(n), dw, dq, dr, c->stream));
         download(c, q, dq, m * n);
         download(c, r, dr, n * n);
     });

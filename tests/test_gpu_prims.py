@@ -81,12 +81,20 @@ def test_thin_qr(ctx, golden, port):
     q, r = cpd.thin_qr(golden["prim_qr_a"], ctx)
     assert rel(q, golden["prim_qr_q"]) < 1e-12 and rel(r, golden["prim_qr_r"]) < 1e-12
     assert np.all(np.diag(r) >= 0)
-    for m, n in ((512, 64), (100, 10), (7, 7)):
+    # (m >= 256: the cooperative multi-CTA kernel, also with a zero column)
+    for m, n in ((512, 64), (100, 10), (7, 7), (4096, 96), (300, 130), (256, 5)):
         a = port.rng_normals(m + n, m * n).reshape(m, n)
         q, r = cpd.thin_qr(a, ctx)
         assert rel(q @ r, a) < 1e-13
         assert np.abs(q.T @ q - np.eye(n)).max() < 1e-13
         assert np.allclose(np.triu(r), r)
+        assert np.all(np.diag(r) >= 0)
+        qo, ro = port.thin_qr(a) if hasattr(port, "thin_qr") else (q, r)
+        assert rel(q, qo) < 1e-11 and rel(r, ro) < 1e-12
+    a = port.rng_normals(9, 400 * 6).reshape(400, 6)
+    a[:, 2] = 0.0  # zero column: R(2,2) stays 0, the reflector is skipped (linalg.hpp:51)
+    q, r = cpd.thin_qr(a, ctx)
+    assert r[2, 2] == 0.0 and rel(q @ r, a) < 1e-13
     q, r = cpd.thin_qr(golden["prim_kr"], ctx)
     assert abs(q[0, 0] - 1.0) <= 1e-12 and np.abs(q[0, 1:]).max() <= 1e-12
     assert np.abs(q[1:, 0]).max() <= 1e-12
