@@ -162,9 +162,15 @@ def init_dist():
 
 
 def barrier(world):
+    """Barrier across the ranks with a device synchronisation on both sides
+    (the session keeps the next sweep's first update in flight between run()
+    calls: the synchronisation drains it before the other ranks are met)."""
+    import torch
+    torch.cuda.synchronize()
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
+        torch.cuda.synchronize()
 
 
 def allmax(world, v):
@@ -293,6 +299,11 @@ def main():
     cfg = cpd.SolverConfig(rank=c["rank"], max_iterations=W + K, seed=INIT_SEED)
 
     # ---- device-timed K sweeps after W warm-up sweeps ---------------------------
+    # (torch's CUDA state is set up here, outside the timed window: the
+    # barriers below call torch.cuda.synchronize())
+    import torch
+    torch.cuda.set_device(local)
+    torch.cuda.synchronize()
     clocks = ClockSampler(local).start()
     sess = ctx.session(cfg, extrapolate=True)
     warm = sess.run(W)
