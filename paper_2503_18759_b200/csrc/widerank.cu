@@ -405,7 +405,6 @@ fit_final_kernel(double nx2, const double* partial, int nb, const double* r0, co
 __global__ void __launch_bounds__(512)
 spd_factor_wide_kernel(const double* g, uint32_t n, double* u, double* ut, int* status, int* reg) {
     __shared__ double red[32];
-    __shared__ int fail;
     double mabs = 0.0, masym = 0.0;
     for (uint32_t e = threadIdx.x; e < n * n; e += 512) {
         const uint32_t i = e / n, j = e % n;
@@ -430,7 +429,6 @@ spd_factor_wide_kernel(const double* g, uint32_t n, double* u, double* ut, int* 
         }
         for (uint32_t e = threadIdx.x; e < n * n; e += 512)
             u[e] = g[e] + ((e / n == e % n) ? delta : 0.0);
-        if (threadIdx.x == 0) fail = 0;
         __syncthreads();
         ok = true;
         for (uint32_t j = 0; j < n; ++j) {
@@ -566,7 +564,6 @@ cudaError_t householder_qr_wide(const double* a, uint64_t m, uint32_t n, double*
     HhArgs h{work, q, r, work + m * n, m, n};
     return hh_launch(h, s);
 }
-
 
 // u_work: 2 n^2 doubles (U and U^T)
 cudaError_t launch_spd_solve_wide(const double* g, uint32_t n, double* u_work, double* x,
