@@ -401,10 +401,15 @@ def main():
             dist.broadcast_object_list(obj, src=0)
             ctx2 = cpd.Context(local, rank=rank, world=world, nccl_id=obj[0])
         cfg2 = cpd.SolverConfig(rank=c["rank"], max_iterations=K, seed=INIT_SEED)
+        # (untimed: the same upload once, synchronously, for the copy's own time)
+        tc = time.perf_counter()
+        ctx2.set_tensor(xh, dims)
+        t_h2d = time.perf_counter() - tc
         barrier(world)
         t0 = time.perf_counter()
-        ctx2.set_tensor(xh, dims)  # synchronous H2D from pinned memory
-        t_h2d = time.perf_counter() - t0
+        # the job: queue the H2D from pinned memory (cpdb_tensor_set_async), set
+        # the solver up under it (the first synchronisation inside waits for it)
+        ctx2.set_tensor(xh, dims, wait=False)
         s2 = ctx2.session(cfg2, extrapolate=True)
         t_begin = time.perf_counter()
         r2 = s2.run(K)
@@ -418,12 +423,14 @@ def main():
         d2h = (sum(f.size for f in m2.factors) + m2.lam.size) * 8 + len(r2) * 128
         e2e = {"value": K / et, "unit": "sweeps/s", "h2d_bytes_per_step": h2d / K,
                "d2h_bytes_per_step": d2h / K, "h2d_ms": t_h2d * 1e3,
-               "begin_ms": (t_begin - t0 - t_h2d) * 1e3, "sweeps_ms": (t_run - t_begin) * 1e3,
-               "end_ms": (t1 - t_run) * 1e3,
+               "upload_and_begin_ms": (t_begin - t0) * 1e3,
+               "sweeps_ms": (t_run - t_begin) * 1e3, "end_ms": (t1 - t_run) * 1e3,
                "h2d_gbs": h2d / t_h2d / 1e9,
                "rest_ms": (et - t_h2d) * 1e3,
-               "note": "one job: H2D of X (pinned; h2d_ms of it) + setup + K sweeps + D2H of "
-                       "the model, bytes amortised over the K sweeps"}
+               "note": "one job: H2D of X from pinned memory (queued, cpdb_tensor_set_async; "
+                       "h2d_ms is the same copy timed alone before the job) with the solver "
+                       "set-up under it + K sweeps + D2H of the model, bytes amortised over "
+                       "the K sweeps"}
 
     # ---- CPU baseline: the reference itself, bounded sample ---------------------
     cpu = None

@@ -161,6 +161,14 @@ int cpdb_shard_rows(uint64_t extent0, int rank, int world, uint64_t* begin, uint
  * leading mode (rows [begin, begin+count) from cpdb_shard_rows) and the
  * GLOBAL dims. */
 int cpdb_tensor_set(cpdb_ctx* ctx, const double* host, const uint64_t* dims, uint32_t order);
+/* The same upload without waiting for it: the copy is queued on the context's
+ * stream and every later call on the context is ordered behind it (the next
+ * call that synchronises -- cpdb_solve, cpdb_session_begin, cpdb_tensor_norm_sq
+ * -- also completes it).  `host` must stay valid and unchanged until then;
+ * page-locked memory makes the copy truly asynchronous, so the host side of
+ * the following cpdb_session_begin / cpdb_solve runs under it. */
+int cpdb_tensor_set_async(cpdb_ctx* ctx, const double* host, const uint64_t* dims,
+                          uint32_t order);
 /* Borrow an existing device buffer (no copy; caller keeps it alive). */
 int cpdb_tensor_set_device(cpdb_ctx* ctx, const double* device_ptr, const uint64_t* dims,
                            uint32_t order);

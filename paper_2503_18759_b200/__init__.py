@@ -188,11 +188,20 @@ class Context:
         return self._h
 
     # ---- X
-    def set_tensor(self, x: np.ndarray, dims: Optional[Sequence[int]] = None):
-        """Upload X (sharded contexts: this rank's slab; ``dims`` = global)."""
+    def set_tensor(self, x: np.ndarray, dims: Optional[Sequence[int]] = None, wait: bool = True):
+        """Upload X (sharded contexts: this rank's slab; ``dims`` = global).
+        ``wait=False`` queues the copy and returns (cpdb_tensor_set_async): the
+        array is kept alive by the context, must not be modified until the
+        next solve / session begin / norm_sq, and should be page-locked for
+        the copy to overlap the host side of that call."""
         x = _f64(x)
         d = _u64(dims if dims is not None else x.shape)
-        _raise(_lib().cpdb_tensor_set(self._h, _p(x), _up(d), len(d)))
+        if wait:
+            _raise(_lib().cpdb_tensor_set(self._h, _p(x), _up(d), len(d)))
+            self._pending_host = None
+        else:
+            self._pending_host = x  # (the upload reads it until the next synchronising call)
+            _raise(_lib().cpdb_tensor_set_async(self._h, _p(x), _up(d), len(d)))
         self.dims = [int(v) for v in d]
 
     def set_tensor_device(self, ptr: int, dims: Sequence[int]):

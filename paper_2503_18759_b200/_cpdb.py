@@ -116,6 +116,7 @@ SIGNATURES = {
     "cpdb_destroy": (None, [CTX]),
     "cpdb_shard_rows": (C.c_int, [C.c_uint64, C.c_int, C.c_int, U64P, U64P]),
     "cpdb_tensor_set": (C.c_int, [CTX, P, U64P, C.c_uint32]),
+    "cpdb_tensor_set_async": (C.c_int, [CTX, P, U64P, C.c_uint32]),
     "cpdb_tensor_set_device": (C.c_int, [CTX, C.c_void_p, U64P, C.c_uint32]),
     "cpdb_tensor_synth": (C.c_int, [CTX, C.c_int32, U64P, C.c_uint32, C.c_uint64, C.c_double,
                                     C.c_uint64]),

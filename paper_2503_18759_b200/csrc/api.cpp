@@ -338,6 +338,19 @@ int cpdb_tensor_set(cpdb_ctx* c, const double* host, const uint64_t* dims, uint3
     });
 }
 
+int cpdb_tensor_set_async(cpdb_ctx* c, const double* host, const uint64_t* dims,
+                          uint32_t order) {
+    return guarded([&] {
+        use_device(c);
+        if (!host) fail(CPDB_INVALID_ARGUMENT, "tensor_set: null data");
+        set_local_geometry(c, dims_of(dims, order));
+        const uint64_t n = cpdb::numel(c->ldims);
+        double* d = c->xown.ensure(n);
+        upload(c, d, host, n);  // on the context's stream: later calls are ordered behind it
+        c->x = d;
+    });
+}
+
 int cpdb_tensor_load_cpdt(cpdb_ctx* c, const char* path) {
     return guarded([&] {
         use_device(c);

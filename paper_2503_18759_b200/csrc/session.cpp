@@ -238,6 +238,24 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     order = static_cast<uint32_t>(c->dims.size());
     if (order < 2) fail(CPDB_INVALID_ARGUMENT, "cp_als_qr: tensor order must be >= 2");
     if (order > CPDB_MAX_ORDER) fail(CPDB_INVALID_ARGUMENT, "cp_als_qr: order above 8");
+    // The reference's initial factors (host Rng, solvers.hpp:116-122) are drawn
+    // before the first synchronisation: after cpdb_tensor_set_async the
+    // upload of X is still running, and this is host time under it.  (Only
+    // when the guards below will pass; nothing here can fail.)
+    std::vector<double> init_pre;
+    {
+        bool sane = !(state && state->factors) && cfg.rank <= 1024;
+        uint64_t nf = 0;
+        for (uint32_t k = 0; k < order; ++k) {
+            sane = sane && cfg.rank <= c->dims[k];
+            nf += c->dims[k] * cfg.rank;
+        }
+        if (sane) {
+            init_pre.resize(nf);
+            cpd::Rng rng(cfg.seed);
+            for (double& v : init_pre) v = rng.normal();
+        }
+    }
     nx2 = ctx_norm_sq(c);
     if (nx2 == 0.0) fail(CPDB_INVALID_ARGUMENT, "cp_als_qr: zero-norm tensor");
     for (uint32_t k = 0; k < order; ++k)
@@ -393,11 +411,14 @@ void Session::begin(cpdb_ctx* ctx, const cpdb_config& config, const cpdb_state* 
     lam.ensure(R);
     lam_alt.ensure(R);
     {
-        std::vector<double> init(nfac);
+        std::vector<double> init;
         const bool given = state && state->factors;
         if (given) {
-            std::memcpy(init.data(), state->factors, nfac * sizeof(double));
+            init.assign(state->factors, state->factors + nfac);
+        } else if (init_pre.size() == nfac) {
+            init.swap(init_pre);  // drawn above, under the upload of X
         } else {
+            init.resize(nfac);
             cpd::Rng rng(cfg.seed);  // initial_factors, solvers.hpp:116-122
             for (double& v : init) v = rng.normal();
         }

@@ -186,3 +186,36 @@ def test_sharded_load_rejects_ragged_leading_extent(port, tmp_path):
     assert all(run_ranks(group, rank_run))
     for c in group:
         c.close()
+
+
+def test_async_upload_matches_synchronous(port):
+    """cpdb_tensor_set_async queues the upload of X on the context's stream;
+    every later call is ordered behind it and the solver's host-side set-up
+    (the reference's Rng draw of the initial factors) runs under it.  Same
+    bits as the synchronous upload, from pinned and from pageable memory."""
+    import numpy as np
+    import torch
+    import paper_2503_18759_b200 as cpd
+    dims, rank = (96, 80, 72), 8
+    x = port.synth_baseline(0, dims, rank, 1e-2, 20250021)
+    cfg = cpd.SolverConfig(rank=rank, max_iterations=6, seed=7)
+    ctx = cpd.Context(0)
+    ctx.set_tensor(x)
+    ref = ctx.solve(cfg, extrapolate=True)
+    pinned = torch.empty(x.size, dtype=torch.float64, pin_memory=True).numpy().reshape(dims)
+    pinned[:] = x
+    for src in (pinned, x):
+        ctx.set_tensor(src, wait=False)
+        assert ctx.norm_sq() == float(ref_norm(ctx, x))
+        ctx.set_tensor(src, wait=False)
+        got = ctx.solve(cfg, extrapolate=True)
+        assert [(t.fitness, t.flops) for t in got.trace] == [(t.fitness, t.flops) for t in ref.trace]
+        for a, b in zip(got.model.factors, ref.model.factors):
+            assert np.array_equal(a, b)
+
+
+def ref_norm(ctx, x):
+    import paper_2503_18759_b200 as cpd
+    c2 = cpd.Context(0)
+    c2.set_tensor(x)
+    return c2.norm_sq()
