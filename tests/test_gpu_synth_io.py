@@ -193,8 +193,8 @@ def test_async_upload_matches_synchronous(port):
     every later call is ordered behind it and the solver's host-side set-up
     (the reference's Rng draw of the initial factors) runs under it.  Same
     bits as the synchronous upload, from pinned and from pageable memory."""
+    import ctypes
     import numpy as np
-    import torch
     import paper_2503_18759_b200 as cpd
     dims, rank = (96, 80, 72), 8
     x = port.synth_baseline(0, dims, rank, 1e-2, 20250021)
@@ -202,9 +202,21 @@ def test_async_upload_matches_synchronous(port):
     ctx = cpd.Context(0)
     ctx.set_tensor(x)
     ref = ctx.solve(cfg, extrapolate=True)
-    pinned = torch.empty(x.size, dtype=torch.float64, pin_memory=True).numpy().reshape(dims)
-    pinned[:] = x
-    for src in (pinned, x):
+    # page-locked host memory straight from the CUDA runtime (no torch here:
+    # importing it after libnccl.so.2 has been loaded by the NCCL tests of
+    # this process would clash with its bundled NCCL)
+    srcs = [x]
+    try:
+        rt = ctypes.CDLL("libcudart.so.12")
+        ptr = ctypes.c_void_p()
+        if rt.cudaMallocHost(ctypes.byref(ptr), ctypes.c_size_t(x.nbytes)) == 0:
+            pinned = np.ctypeslib.as_array((ctypes.c_double * x.size).from_address(ptr.value))
+            pinned = pinned.reshape(dims)
+            pinned[:] = x
+            srcs.insert(0, pinned)
+    except OSError:
+        pass
+    for src in srcs:
         ctx.set_tensor(src, wait=False)
         assert ctx.norm_sq() == float(ref_norm(ctx, x))
         ctx.set_tensor(src, wait=False)
